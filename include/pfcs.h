@@ -1,0 +1,130 @@
+/* pfcs.h — C ABI of libpfcs, the sm_100a pseudo-spectral hot path.
+ *
+ * Plain pointers and sizes only: every array argument is a DEVICE pointer
+ * (fp64 / complex128 = interleaved {re, im} doubles, C order), every
+ * `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ * Calls are asynchronous on `stream` unless stated; the caller owns all
+ * buffers.  Return value: PFCS_OK or a PFCS_E_* code; the message of the most
+ * recent failure on the calling thread is available from pfcs_last_error().
+ *
+ * Each entry point names the reference interface it replaces
+ * (/root/reference/pkg/src/pfcspectral/<file>:<line>).  The reference is a
+ * pure-Python package with no FFI of its own; the Python layer of this repo
+ * (paper_2603_26818_b200/) keeps the reference signatures and binds these
+ * symbols with ctypes (INTEGRATION.md shows the binding).
+ */
+#ifndef PFCS_H
+#define PFCS_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PFCS_OK 0
+#define PFCS_E_ARG 1         /* bad shape / axis / layout  -> ValueError      */
+#define PFCS_E_CUDA 2        /* CUDA runtime failure                           */
+#define PFCS_E_UNSUPPORTED 3 /* size not supported by the kernels              */
+#define PFCS_E_NONFINITE 4   /* non-finite field -> pfc.DivergenceError        */
+
+#define PFCS_DIAG_SLOTS 64
+#define PFCS_DIAG_VALS 4
+
+/* Library version (major*10000 + minor*100 + patch). */
+int pfcs_version(void);
+/* Message of the last failing call on this thread ("" if none). */
+const char* pfcs_last_error(void);
+/* Number of CUDA devices visible to the library (sanity/probe). */
+int pfcs_device_count(int* count);
+
+/* ---- serial line transforms: fftcore.fft_axis (fftcore.py:31-40) ------------
+ * 1D DFT of every line along `axis` (0, 1, 2) of a C-order (n0, n1, n2)
+ * complex128 array.  forward != 0: unnormalised; forward == 0: inverse with
+ * every output scaled by fl(1/n_axis) (numpy ifft convention).  in == out is
+ * allowed (in-place).  Any length: power-of-two lengths <= 4096 take the
+ * Stockham kernels, other lengths the direct DFT kernel. */
+int pfcs_fft_axis_c2c(const void* in, void* out, int64_t n0, int64_t n1, int64_t n2, int axis,
+                      int forward, void* stream);
+
+/* ---- slab-pipeline z-line transforms: distfft.dist_fft_forward/inverse
+ * (distfft.py:150-173) fused with distfft._exchange's concatenate/slice
+ * (distfft.py:110-124).  `nlines` contiguous-z lines of length nz.  When
+ * g_in > 1 the input is "blocked": nz split into g_in balanced slabs
+ * (grid.slab_layout, grid.py:103-111), slab g stored densely as
+ * (nlines, cz_g) at element offset nlines*zoff_g — the all-to-all receive
+ * buffer.  g_out > 1 writes the same blocked layout (the send buffer). */
+int pfcs_fft_zlines(const void* in, void* out, int64_t nlines, int64_t nz, int g_in, int g_out,
+                    int forward, void* stream);
+
+/* ---- real transforms along axis 0 (x) of a C-order array (new: R2C/C2R,
+ * north-star item (1)).  rfft: real (nx, inner) -> complex (nx/2+1, inner),
+ * unnormalised.  irfft: complex (nx/2+1, inner) -> real (nx, inner), scaled
+ * by fl(1/nx); the imaginary parts of modes 0 and nx/2 are ignored (numpy
+ * irfft convention).  nx must be an even power of two in [4, 8192]. */
+int pfcs_rfft_x(const double* in, void* out, int64_t nx, int64_t inner, void* stream);
+int pfcs_irfft_x(const void* in, double* out, int64_t nx, int64_t inner, void* stream);
+
+/* ---- fused PFC step kernels: pfc.pfc_step (pfc.py:96-128) ---------------
+ * Diagnostics block `diag` (device, PFCS_DIAG_SLOTS x 4 doubles; the caller
+ * zeroes it per step and max-reduces the slots): per slot
+ *   [0] = max |Re psi|, [1] = max |Im psi|, [2] = max |psi|
+ *   (of the physical field before the update, pfc.py:100-105,124),
+ *   [3] = non-zero if a non-finite value was produced (pfc.py:122).
+ * CTAs stripe their atomics over the slots (no same-address hot spot).
+ * diag may be NULL (no diagnostics).
+ *
+ * pfcs_pfc_cube_x: x-line pass of the physical-space nonlinearity.  On a
+ * (nxm, inner) spectral-in-x slab (y and z already physical) it performs
+ *   inverse x-transform -> psi -> psi*(psi*psi) -> forward x-transform
+ * in place.  real != 0: half-spectrum data (nxm = nx/2+1, C2R/R2C, psi real);
+ * real == 0: full complex data (nxm = nx, C2C, complex cube as numpy's
+ * `psi ** 3`, pfc.py:109). */
+int pfcs_pfc_cube_x(void* data, int64_t nx, int64_t inner, int real, double* diag, void* stream);
+
+/* pfcs_pfc_update_z: z-line pass of the semi-implicit update (pfc.py:114-124)
+ * for an X-slab spectral field psi_hat (cx, ny, nz) (plain layout, updated
+ * in place).  Reads N-hat's un-transformed z lines from `nl` (blocked over
+ * g_in slabs), forward z-transform, then
+ *     psi_hat <- (psi_hat + dt*(lap*N_hat)) / (1 - dt*lin)
+ * with the symbols of grid.make_symbols (grid.py:155-208) evaluated from the
+ * 1D wavenumber vectors kx (the cx rows owned, already offset), ky, kz with
+ * numpy's operation order, finiteness check into diag[3]; then, if
+ * `next_out` is non-NULL, the inverse z-transform of the new psi_hat written
+ * to `next_out` in the layout blocked over g_out slabs (the first stage of
+ * the next step's inverse transform). */
+int pfcs_pfc_update_z(const void* nl, void* psi_hat, void* next_out, int64_t cx, int64_t ny,
+                      int64_t nz, int g_in, int g_out, const double* kx, const double* ky,
+                      const double* kz, double eps, double dt, double* diag, void* stream);
+
+/* Unfused forms for grids the fused passes do not cover (any size):
+ * pfcs_pfc_cube: in place psi <- psi**3 on a physical slab of n points
+ * (real != 0: float64 data; else complex128 with numpy's complex power
+ * psi*(psi*psi)), diagnostics as above.
+ * pfcs_pfc_update: the pointwise update of pfcs_pfc_update_z on an already
+ * transformed nl_hat (plain (cx, ny, nz) layout), psi_hat in place. */
+int pfcs_pfc_cube(void* data, int64_t n, int real, double* diag, void* stream);
+int pfcs_pfc_update(const void* nl_hat, void* psi_hat, int64_t cx, int64_t ny, int64_t nz,
+                    const double* kx, const double* ky, const double* kz, double eps, double dt,
+                    double* diag, void* stream);
+
+/* ---- deterministic reductions (pfc._reduce_sum / free_energy,
+ * pfc.py:131-162).  out[0] = sum_i f(a_i, b_i) in a fixed order,
+ * independent of the launch: f = 0.5*a*b + 0.25*a^4 (free-energy density,
+ * `b` the real part of F^-1(op*psi_hat)).  Real strided inputs: element i at
+ * a[i*sa], b[i*sb] (sa = 2 reads the real part of a complex array). */
+int pfcs_energy_sum(const double* a, int64_t sa, const double* b, int64_t sb, int64_t n,
+                    double* out, double* scratch, void* stream);
+/* out[0] = max_i |a_i| (strided like above); NaN propagates. */
+int pfcs_absmax(const double* a, int64_t sa, int64_t n, double* out, void* stream);
+/* Multiply complex x-slab data by the PFC operator symbol op = eps +
+ * two_ring (grid.py:192-194), out = op*in, symbols from wavenumbers. */
+int pfcs_apply_op(const void* in, void* out, int64_t cx, int64_t ny, int64_t nz, const double* kx,
+                  const double* ky, const double* kz, double eps, void* stream);
+/* Scratch bytes pfcs_energy_sum needs for n elements. */
+int64_t pfcs_energy_scratch_bytes(int64_t n);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PFCS_H */

@@ -1,0 +1,115 @@
+"""ctypes binding of libpfcs.so (include/pfcs.h) and the device plumbing.
+
+This module is the only place that touches the C ABI.  It fails loudly:
+there is no CPU fallback anywhere in the product path — if the library is
+missing or no CUDA device is present every compute call raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import threading
+from pathlib import Path
+
+import torch
+
+_HERE = Path(__file__).resolve().parent
+LIB_PATH = _HERE / "libpfcs.so"
+
+PFCS_OK = 0
+PFCS_E_ARG = 1
+PFCS_E_CUDA = 2
+PFCS_E_UNSUPPORTED = 3
+PFCS_E_NONFINITE = 4
+DIAG_SLOTS = 64
+DIAG_VALS = 4
+
+_c_i64 = ctypes.c_int64
+_c_int = ctypes.c_int
+_c_p = ctypes.c_void_p
+_c_d = ctypes.c_double
+
+# symbol -> argtypes (every function returns int unless listed in _RESTYPE)
+_SIGS = {
+    "pfcs_version": [],
+    "pfcs_last_error": [],
+    "pfcs_device_count": [ctypes.POINTER(_c_int)],
+    "pfcs_fft_axis_c2c": [_c_p, _c_p, _c_i64, _c_i64, _c_i64, _c_int, _c_int, _c_p],
+    "pfcs_fft_zlines": [_c_p, _c_p, _c_i64, _c_i64, _c_int, _c_int, _c_int, _c_p],
+    "pfcs_rfft_x": [_c_p, _c_p, _c_i64, _c_i64, _c_p],
+    "pfcs_irfft_x": [_c_p, _c_p, _c_i64, _c_i64, _c_p],
+    "pfcs_pfc_cube_x": [_c_p, _c_i64, _c_i64, _c_int, _c_p, _c_p],
+    "pfcs_pfc_update_z": [_c_p, _c_p, _c_p, _c_i64, _c_i64, _c_i64, _c_int, _c_int,
+                          _c_p, _c_p, _c_p, _c_d, _c_d, _c_p, _c_p],
+    "pfcs_pfc_cube": [_c_p, _c_i64, _c_int, _c_p, _c_p],
+    "pfcs_pfc_update": [_c_p, _c_p, _c_i64, _c_i64, _c_i64, _c_p, _c_p, _c_p, _c_d, _c_d, _c_p, _c_p],
+    "pfcs_energy_sum": [_c_p, _c_i64, _c_p, _c_i64, _c_i64, _c_p, _c_p, _c_p],
+    "pfcs_energy_scratch_bytes": [_c_i64],
+    "pfcs_absmax": [_c_p, _c_i64, _c_i64, _c_p, _c_p],
+    "pfcs_apply_op": [_c_p, _c_p, _c_i64, _c_i64, _c_i64, _c_p, _c_p, _c_p, _c_d, _c_p],
+}
+_RESTYPE = {"pfcs_last_error": ctypes.c_char_p, "pfcs_energy_scratch_bytes": _c_i64}
+
+_lib = None
+_lock = threading.Lock()
+
+
+class NativeError(RuntimeError):
+    """A libpfcs call failed (CUDA error or unsupported size)."""
+
+
+def exported_symbols() -> list[str]:
+    return list(_SIGS)
+
+
+def load(require_cuda: bool = True):
+    """Load libpfcs.so (once).  Raises if it is absent or, by default, if
+    no CUDA device is visible — there is no host fallback."""
+    global _lib
+    if _lib is None:
+        with _lock:
+            if _lib is None:
+                if not LIB_PATH.exists():
+                    raise NativeError(
+                        f"{LIB_PATH} is missing: run __graft_entry__.build() "
+                        "(nvcc, sm_100a) before using the CUDA path")
+                lib = ctypes.CDLL(str(LIB_PATH))
+                for name, args in _SIGS.items():
+                    fn = getattr(lib, name)
+                    fn.argtypes = args
+                    fn.restype = _RESTYPE.get(name, _c_int)
+                _lib = lib
+    if require_cuda and not torch.cuda.is_available():
+        raise NativeError("no CUDA device visible: the pfcspectral B200 path has no CPU fallback")
+    return _lib
+
+
+def last_error() -> str:
+    msg = load(require_cuda=False).pfcs_last_error()
+    return msg.decode() if msg else ""
+
+
+def check(rc: int, what: str) -> None:
+    if rc == PFCS_OK:
+        return
+    msg = f"{what}: {last_error()}"
+    if rc == PFCS_E_ARG:
+        raise ValueError(msg)
+    raise NativeError(msg)
+
+
+def call(name: str, *args) -> None:
+    check(getattr(load(), name)(*args), name)
+
+
+def stream_ptr(stream: torch.cuda.Stream | None = None) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def ptr(t: torch.Tensor | None) -> int | None:
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise ValueError("expected a CUDA tensor")
+    return t.data_ptr()

@@ -1,0 +1,226 @@
+// pfcs_api.cu — the extern "C" boundary of libpfcs (see include/pfcs.h) plus
+// host utilities: thread-local errors, per-device twiddle tables, shared
+// memory opt-in.  No torch types cross this boundary: device pointers, sizes
+// and a cudaStream_t passed as void*.
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "pfcs_internal.h"
+
+namespace pfcs {
+
+static thread_local std::string g_err;
+
+void set_error(const std::string& msg) { g_err = msg; }
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+int check_cuda(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return PFCS_OK;
+  g_err = std::string(what) + ": " + cudaGetErrorString(e);
+  return PFCS_E_CUDA;
+}
+int check_launch(const char* what) { return check_cuda(cudaGetLastError(), what); }
+
+// exp(-2 pi i m / N) with exact values at the quadrant points and the octant
+// symmetry built in; long double keeps every entry within 0.5 ulp + epsilon.
+static void twiddle_value(long long m, long long N, double* c, double* s) {
+  m %= N;
+  const long long q = (4 * m) / N;  // quadrant
+  long long r = 4 * m - q * N;      // theta = (pi/2) * (q + r/N)
+  long double cp, sp;
+  const long double half_pi = 1.5707963267948966192313216916397514L;
+  if (r == 0) {
+    cp = 1.0L;
+    sp = 0.0L;
+  } else if (2 * r <= N) {
+    const long double phi = half_pi * (long double)r / (long double)N;
+    cp = cosl(phi);
+    sp = sinl(phi);
+  } else {
+    const long double phi = half_pi * (long double)(N - r) / (long double)N;
+    cp = sinl(phi);
+    sp = cosl(phi);
+  }
+  long double ct, st;
+  switch (q) {
+    case 0: ct = cp; st = sp; break;
+    case 1: ct = -sp; st = cp; break;
+    case 2: ct = -cp; st = -sp; break;
+    default: ct = sp; st = -cp; break;
+  }
+  *c = (double)ct;
+  *s = -(double)st;  // exp(-i theta)
+}
+
+static std::mutex g_tw_mu;
+static std::map<std::pair<int, int>, double2*> g_tw;
+
+const double2* twiddles(int N) {
+  int dev = 0;
+  if (check_cuda(cudaGetDevice(&dev), "cudaGetDevice")) return nullptr;
+  std::lock_guard<std::mutex> lk(g_tw_mu);
+  auto key = std::make_pair(dev, N);
+  auto it = g_tw.find(key);
+  if (it != g_tw.end()) return it->second;
+  std::vector<double2> h((size_t)N);
+  for (int m = 0; m < N; ++m) twiddle_value(m, N, &h[m].x, &h[m].y);
+  double2* d = nullptr;
+  if (check_cuda(cudaMalloc(&d, sizeof(double2) * (size_t)N), "cudaMalloc twiddles")) return nullptr;
+  if (check_cuda(cudaMemcpy(d, h.data(), sizeof(double2) * (size_t)N, cudaMemcpyHostToDevice),
+                 "cudaMemcpy twiddles")) {
+    cudaFree(d);
+    return nullptr;
+  }
+  g_tw[key] = d;
+  return d;
+}
+
+static std::mutex g_smem_mu;
+static std::map<std::pair<int, const void*>, size_t> g_smem;
+
+int ensure_smem(const void* func, size_t bytes) {
+  if (bytes <= 48 * 1024) return PFCS_OK;
+  int dev = 0;
+  if (check_cuda(cudaGetDevice(&dev), "cudaGetDevice")) return PFCS_E_CUDA;
+  std::lock_guard<std::mutex> lk(g_smem_mu);
+  auto key = std::make_pair(dev, func);
+  auto it = g_smem.find(key);
+  if (it != g_smem.end() && it->second >= bytes) return PFCS_OK;
+  if (check_cuda(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes),
+                 "cudaFuncSetAttribute(smem)"))
+    return PFCS_E_CUDA;
+  g_smem[key] = bytes;
+  return PFCS_OK;
+}
+
+// defined in the other translation units
+int launch_real_x(const void* in, void* out, long long nx, long long inner, int mode, double* diag,
+                  cudaStream_t st);
+int launch_cube_c2c(void* data, long long nx, long long inner, double* diag, cudaStream_t st);
+int launch_pfc_z(const double2* nl, double2* psi_hat, double2* next, long long cx, long long ny,
+                 long long nz, int g_in, int g_out, const double* kx, const double* ky,
+                 const double* kz, double eps, double dt, double* diag, cudaStream_t st);
+int launch_pfc_cube(void* data, long long n, int real, double* diag, cudaStream_t st);
+int launch_pfc_update(const double2* nl, double2* psi_hat, long long cx, long long ny, long long nz,
+                      const double* kx, const double* ky, const double* kz, double eps, double dt,
+                      double* diag, cudaStream_t st);
+int launch_apply_op(const double2* in, double2* out, long long cx, long long ny, long long nz,
+                    const double* kx, const double* ky, const double* kz, double eps,
+                    cudaStream_t st);
+int launch_energy_sum(const double* a, long long sa, const double* b, long long sb, long long n,
+                      double* out, double* scratch, cudaStream_t st);
+long long energy_scratch_bytes(long long n);
+int launch_absmax(const double* a, long long sa, long long n, double* out, cudaStream_t st);
+
+}  // namespace pfcs
+
+using namespace pfcs;
+
+static inline cudaStream_t S(void* s) { return (cudaStream_t)s; }
+
+extern "C" {
+
+int pfcs_version(void) { return 100; }  // 0.1.0
+
+const char* pfcs_last_error(void) { return g_err.c_str(); }
+
+int pfcs_device_count(int* count) { return check_cuda(cudaGetDeviceCount(count), "cudaGetDeviceCount"); }
+
+int pfcs_fft_axis_c2c(const void* in, void* out, int64_t n0, int64_t n1, int64_t n2, int axis,
+                      int forward, void* stream) {
+  if (axis < 0 || axis > 2) return fail(PFCS_E_ARG, "axis must be 0, 1 or 2");
+  if (n0 < 0 || n1 < 0 || n2 < 0) return fail(PFCS_E_ARG, "negative extent");
+  const int64_t total = n0 * n1 * n2;
+  if (total == 0) return PFCS_OK;
+  const int64_t n = axis == 0 ? n0 : (axis == 1 ? n1 : n2);
+  if (n == 1) {  // fftcore.py:36-37: length-1 axes are copied
+    if (in != out)
+      return check_cuda(cudaMemcpyAsync(out, in, (size_t)total * 16, cudaMemcpyDeviceToDevice, S(stream)),
+                        "copy");
+    return PFCS_OK;
+  }
+  if (n > 16384) return fail(PFCS_E_UNSUPPORTED, "line length > 16384");
+  const int64_t outer = axis == 0 ? 1 : (axis == 1 ? n0 : n0 * n1);
+  const int64_t inner = axis == 0 ? n1 * n2 : (axis == 1 ? n2 : 1);
+  if (inner == 1)
+    return launch_lines_c2c((const double2*)in, (double2*)out, outer, (int)n, 1, 1, forward != 0, S(stream));
+  return launch_strided_c2c((const double2*)in, (double2*)out, outer, (int)n, inner, forward != 0, S(stream));
+}
+
+int pfcs_fft_zlines(const void* in, void* out, int64_t nlines, int64_t nz, int g_in, int g_out,
+                    int forward, void* stream) {
+  if (nlines < 0 || nz < 1 || g_in < 1 || g_out < 1) return fail(PFCS_E_ARG, "bad z-line geometry");
+  if (nlines == 0) return PFCS_OK;
+  if (nz == 1) {
+    if (in != out)
+      return check_cuda(cudaMemcpyAsync(out, in, (size_t)nlines * 16, cudaMemcpyDeviceToDevice, S(stream)),
+                        "copy");
+    return PFCS_OK;
+  }
+  if (nz > 16384) return fail(PFCS_E_UNSUPPORTED, "line length > 16384");
+  return launch_lines_c2c((const double2*)in, (double2*)out, nlines, (int)nz, g_in, g_out, forward != 0,
+                          S(stream));
+}
+
+int pfcs_rfft_x(const double* in, void* out, int64_t nx, int64_t inner, void* stream) {
+  if (nx < 1 || inner < 0) return fail(PFCS_E_ARG, "bad shape");
+  return launch_real_x(in, out, nx, inner, 0, nullptr, S(stream));
+}
+
+int pfcs_irfft_x(const void* in, double* out, int64_t nx, int64_t inner, void* stream) {
+  if (nx < 1 || inner < 0) return fail(PFCS_E_ARG, "bad shape");
+  return launch_real_x(in, out, nx, inner, 1, nullptr, S(stream));
+}
+
+int pfcs_pfc_cube_x(void* data, int64_t nx, int64_t inner, int real, double* diag, void* stream) {
+  if (nx < 1 || inner < 0) return fail(PFCS_E_ARG, "bad shape");
+  if (real) return launch_real_x(data, data, nx, inner, 2, diag, S(stream));
+  return launch_cube_c2c(data, nx, inner, diag, S(stream));
+}
+
+int pfcs_pfc_update_z(const void* nl, void* psi_hat, void* next_out, int64_t cx, int64_t ny,
+                      int64_t nz, int g_in, int g_out, const double* kx, const double* ky,
+                      const double* kz, double eps, double dt, double* diag, void* stream) {
+  if (cx < 0 || ny < 1 || nz < 1 || g_in < 1 || g_out < 1) return fail(PFCS_E_ARG, "bad slab geometry");
+  return launch_pfc_z((const double2*)nl, (double2*)psi_hat, (double2*)next_out, cx, ny, nz, g_in, g_out,
+                      kx, ky, kz, eps, dt, diag, S(stream));
+}
+
+int pfcs_pfc_cube(void* data, int64_t n, int real, double* diag, void* stream) {
+  if (n < 0) return fail(PFCS_E_ARG, "negative count");
+  return launch_pfc_cube(data, n, real, diag, S(stream));
+}
+
+int pfcs_pfc_update(const void* nl_hat, void* psi_hat, int64_t cx, int64_t ny, int64_t nz,
+                    const double* kx, const double* ky, const double* kz, double eps, double dt,
+                    double* diag, void* stream) {
+  if (cx < 0 || ny < 1 || nz < 1) return fail(PFCS_E_ARG, "bad slab geometry");
+  return launch_pfc_update((const double2*)nl_hat, (double2*)psi_hat, cx, ny, nz, kx, ky, kz, eps, dt,
+                           diag, S(stream));
+}
+
+int pfcs_energy_sum(const double* a, int64_t sa, const double* b, int64_t sb, int64_t n, double* out,
+                    double* scratch, void* stream) {
+  if (n < 0) return fail(PFCS_E_ARG, "negative count");
+  return launch_energy_sum(a, sa, b, sb, n, out, scratch, S(stream));
+}
+
+int64_t pfcs_energy_scratch_bytes(int64_t n) { return energy_scratch_bytes(n); }
+
+int pfcs_absmax(const double* a, int64_t sa, int64_t n, double* out, void* stream) {
+  if (n < 0) return fail(PFCS_E_ARG, "negative count");
+  return launch_absmax(a, sa, n, out, S(stream));
+}
+
+int pfcs_apply_op(const void* in, void* out, int64_t cx, int64_t ny, int64_t nz, const double* kx,
+                  const double* ky, const double* kz, double eps, void* stream) {
+  return launch_apply_op((const double2*)in, (double2*)out, cx, ny, nz, kx, ky, kz, eps, S(stream));
+}
+
+}  // extern "C"

@@ -1,0 +1,315 @@
+// pfcs_c2c.cu — batched complex-to-complex line transforms (fp64, sm_100a).
+//
+// Reference semantics: fftcore.fft_axis (pkg/src/pfcspectral/fftcore.py:31-40)
+// for the three axes of a C-order (n0, n1, n2) complex128 buffer, plus the
+// z-line transforms of the slab pipeline that read the all-to-all receive
+// buffer / write the send buffer directly (distfft._exchange,
+// distfft.py:110-124, whose concatenate/slice pack and unpack are fused into
+// the z-line prologue/epilogue here).
+//
+//  * k_lines    : contiguous lines (axis 2).  Input and output addressing may
+//                 each be "plain" (line*N + z) or "blocked": the z axis split
+//                 into G balanced slabs, slab g stored as a dense
+//                 (nlines, cz_g) block at offset nlines*zoff_g — exactly the
+//                 layout an all-to-all of per-rank z-slabs produces/consumes.
+//  * k_strided  : one transform axis with a contiguous "inner" extent
+//                 (axes 0 and 1).  A CTA takes T adjacent inner columns so each
+//                 row of the tile is one T*16-byte coalesced segment.
+//  * k_dft      : direct O(N^2) DFT for non-power-of-two N (the reference
+//                 accepts any N, SPEC sizes 1..16 and primes).
+#include "pfcs_fft.cuh"
+#include "pfcs_internal.h"
+
+namespace pfcs {
+
+template <int N, int T, bool FWD, bool BIN, bool BOUT>
+__global__ void __launch_bounds__(T*(N / radix_R(N)))
+    k_lines(const double2* in, double2* out, i64 nlines, SlabSplit sin, SlabSplit sout,
+            const double2* __restrict__ tw, double scale) {
+  constexpr int R = radix_R(N);
+  constexpr int P = N / R;
+  extern __shared__ double2 smem[];
+  const int tid = threadIdx.x;
+  const int t = tid / P;
+  const int j = tid - t * P;
+  const i64 l = (i64)blockIdx.x * T + t;
+  const bool active = l < nlines;
+  double2* sl = smem + t * line_stride(N);
+  double2 v[R];
+#pragma unroll
+  for (int e = 0; e < R; ++e) {
+    const int z = j + P * e;
+    i64 a;
+    if (BIN) {
+      int zoff, cz;
+      sin.locate(z, zoff, cz);
+      a = nlines * zoff + l * cz + (z - zoff);
+    } else {
+      a = l * N + z;
+    }
+    v[e] = active ? in[a] : make_double2(0.0, 0.0);
+  }
+  fft_line<N, FWD>(v, j, sl, tw);
+  if (active) {
+#pragma unroll
+    for (int e = 0; e < R; ++e) {
+      const int z = j + P * e;
+      i64 a;
+      if (BOUT) {
+        int zoff, cz;
+        sout.locate(z, zoff, cz);
+        a = nlines * zoff + l * cz + (z - zoff);
+      } else {
+        a = l * N + z;
+      }
+      double2 r = v[e];
+      if (!FWD) r = make_double2(r.x * scale, r.y * scale);
+      out[a] = r;
+    }
+  }
+}
+
+template <int N, int T, bool FWD>
+__global__ void __launch_bounds__(T*(N / radix_R(N)))
+    k_strided(const double2* in, double2* out, i64 outer, i64 inner, i64 tpo,
+              const double2* __restrict__ tw, double scale) {
+  constexpr int R = radix_R(N);
+  constexpr int P = N / R;
+  extern __shared__ double2 smem[];
+  const int tid = threadIdx.x;
+  const int t = tid % T;
+  const int j = tid / T;
+  const i64 o = (i64)blockIdx.x / tpo;
+  const i64 i = ((i64)blockIdx.x - o * tpo) * T + t;
+  const bool active = i < inner;
+  const i64 base = o * (i64)N * inner + i;
+  double2* sl = smem + t * line_stride(N);
+  double2 v[R];
+#pragma unroll
+  for (int e = 0; e < R; ++e)
+    v[e] = active ? in[base + (i64)(j + P * e) * inner] : make_double2(0.0, 0.0);
+  fft_line<N, FWD>(v, j, sl, tw);
+  if (active) {
+#pragma unroll
+    for (int e = 0; e < R; ++e) {
+      double2 r = v[e];
+      if (!FWD) r = make_double2(r.x * scale, r.y * scale);
+      out[base + (i64)(j + P * e) * inner] = r;
+    }
+  }
+}
+
+// Direct DFT for arbitrary N: a CTA loads a tile of T lines (T adjacent inner
+// columns when inner > 1) into shared memory and every thread produces
+// outputs X[k] = sum_n x[n] w[(n k) mod N] with the index advanced
+// incrementally (no integer multiply in the inner loop).
+__global__ void k_dft(const double2* in, double2* out, int N, i64 outer, i64 inner, int T,
+                      i64 tpo, const double2* __restrict__ tw, int fwd, double scale) {
+  extern __shared__ double2 sm[];
+  const bool contig = inner == 1;
+  i64 o0, i0;
+  if (contig) {
+    o0 = (i64)blockIdx.x * T;
+    i0 = 0;
+  } else {
+    o0 = (i64)blockIdx.x / tpo;
+    i0 = ((i64)blockIdx.x - o0 * tpo) * T;
+  }
+  const int tot = T * N;
+  for (int idx = threadIdx.x; idx < tot; idx += blockDim.x) {
+    int t, n;
+    if (contig) {
+      t = idx / N;
+      n = idx - t * N;
+    } else {
+      n = idx / T;
+      t = idx - n * T;
+    }
+    const i64 o = contig ? o0 + t : o0;
+    const i64 i = contig ? 0 : i0 + t;
+    double2 val = make_double2(0.0, 0.0);
+    if (o < outer && i < inner) val = in[o * (i64)N * inner + (i64)n * inner + i];
+    sm[t * N + n] = val;
+  }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < tot; idx += blockDim.x) {
+    int t, k;
+    if (contig) {
+      t = idx / N;
+      k = idx - t * N;
+    } else {
+      k = idx / T;
+      t = idx - k * T;
+    }
+    const i64 o = contig ? o0 + t : o0;
+    const i64 i = contig ? 0 : i0 + t;
+    const double2* x = sm + t * N;
+    double ar = 0.0, ai = 0.0;
+    int m = 0;
+    for (int n = 0; n < N; ++n) {
+      const double2 w = __ldg(&tw[m]);
+      const double2 a = x[n];
+      if (fwd) {
+        ar = fma(a.x, w.x, fma(-a.y, w.y, ar));
+        ai = fma(a.x, w.y, fma(a.y, w.x, ai));
+      } else {
+        ar = fma(a.x, w.x, fma(a.y, w.y, ar));
+        ai = fma(a.y, w.x, fma(-a.x, w.y, ai));
+      }
+      m += k;
+      if (m >= N) m -= N;
+    }
+    if (o < outer && i < inner) {
+      if (!fwd) {
+        ar *= scale;
+        ai *= scale;
+      }
+      out[o * (i64)N * inner + (i64)k * inner + i] = make_double2(ar, ai);
+    }
+  }
+}
+
+// Copy between plain and blocked z-line layouts (the np.concatenate /
+// slicing of distfft._exchange for sizes the fused kernels do not cover).
+__global__ void k_reblock(const double2* in, double2* out, i64 nlines, int n, SlabSplit a, SlabSplit b) {
+  const i64 total = nlines * n;
+  for (i64 idx = (i64)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += (i64)gridDim.x * blockDim.x) {
+    const i64 l = idx / n;
+    const int z = (int)(idx - l * n);
+    int zo, cz;
+    a.locate(z, zo, cz);
+    const i64 ia = nlines * zo + l * cz + (z - zo);
+    b.locate(z, zo, cz);
+    const i64 ib = nlines * zo + l * cz + (z - zo);
+    out[ib] = in[ia];
+  }
+}
+
+static int reblock(const double2* in, double2* out, i64 nlines, int n, SlabSplitH a, SlabSplitH b,
+                   cudaStream_t st) {
+  i64 blocks = (nlines * n + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  if (blocks < 1) return PFCS_OK;
+  k_reblock<<<(unsigned)blocks, 256, 0, st>>>(in, out, nlines, n, SlabSplit{a.G, a.base, a.extra},
+                                              SlabSplit{b.G, b.base, b.extra});
+  return check_launch("k_reblock");
+}
+
+// ---------------------------------------------------------------- dispatch --
+
+template <int N, bool FWD>
+static int lines_n(const double2* in, double2* out, i64 nlines, SlabSplitH si, SlabSplitH so,
+                   cudaStream_t st) {
+  constexpr int T = TileCfg<N>::T_CONTIG;
+  constexpr int P = TileCfg<N>::P;
+  const size_t smem = (size_t)T * line_stride(N) * sizeof(double2);
+  const double2* tw = twiddles(N);
+  if (!tw) return PFCS_E_CUDA;
+  SlabSplit a{si.G, si.base, si.extra}, b{so.G, so.base, so.extra};
+  const double scale = 1.0 / (double)N;
+  const i64 blocks = (nlines + T - 1) / T;
+  const bool bin = si.G > 1, bout = so.G > 1;
+  const void* f;
+#define PFCS_LK(BI, BO) (const void*)k_lines<N, T, FWD, BI, BO>
+  if (bin && bout) f = PFCS_LK(true, true);
+  else if (bin) f = PFCS_LK(true, false);
+  else if (bout) f = PFCS_LK(false, true);
+  else f = PFCS_LK(false, false);
+#undef PFCS_LK
+  if (ensure_smem(f, smem)) return PFCS_E_CUDA;
+  dim3 grid((unsigned)blocks), block(T * P);
+  if (bin && bout) k_lines<N, T, FWD, true, true><<<grid, block, smem, st>>>(in, out, nlines, a, b, tw, scale);
+  else if (bin) k_lines<N, T, FWD, true, false><<<grid, block, smem, st>>>(in, out, nlines, a, b, tw, scale);
+  else if (bout) k_lines<N, T, FWD, false, true><<<grid, block, smem, st>>>(in, out, nlines, a, b, tw, scale);
+  else k_lines<N, T, FWD, false, false><<<grid, block, smem, st>>>(in, out, nlines, a, b, tw, scale);
+  return check_launch("k_lines");
+}
+
+template <int N, bool FWD>
+static int strided_n(const double2* in, double2* out, i64 outer, i64 inner, cudaStream_t st) {
+  constexpr int T = TileCfg<N>::T_STRIDED;
+  constexpr int P = TileCfg<N>::P;
+  const size_t smem = (size_t)T * line_stride(N) * sizeof(double2);
+  const double2* tw = twiddles(N);
+  if (!tw) return PFCS_E_CUDA;
+  const i64 tpo = (inner + T - 1) / T;
+  const void* f = (const void*)k_strided<N, T, FWD>;
+  if (ensure_smem(f, smem)) return PFCS_E_CUDA;
+  k_strided<N, T, FWD><<<(unsigned)(outer * tpo), T * P, smem, st>>>(in, out, outer, inner, tpo, tw,
+                                                                     1.0 / (double)N);
+  return check_launch("k_strided");
+}
+
+#define PFCS_POW2_CASES(MACRO) \
+  MACRO(2) MACRO(4) MACRO(8) MACRO(16) MACRO(32) MACRO(64) MACRO(128) MACRO(256) MACRO(512) \
+      MACRO(1024) MACRO(2048) MACRO(4096)
+
+int launch_lines_c2c(const double2* in, double2* out, long long nlines, int n, int g_in, int g_out,
+                     bool forward, cudaStream_t st) {
+  if (nlines <= 0) return PFCS_OK;
+  const SlabSplitH si = slab_split(n, g_in), so = slab_split(n, g_out);
+  if (!is_pow2(n) || n > 4096) {
+    // generic sizes: re-block through a plain temporary around the direct DFT
+    if (g_in == 1 && g_out == 1) return launch_dft(in, out, nlines, n, 1, forward, st);
+    double2* tmp = nullptr;
+    const size_t bytes = (size_t)nlines * n * sizeof(double2);
+    if (int rc = check_cuda(cudaMallocAsync((void**)&tmp, bytes, st), "cudaMallocAsync")) return rc;
+    int rc = reblock(in, tmp, nlines, n, si, slab_split(n, 1), st);
+    if (!rc) rc = launch_dft(tmp, tmp, nlines, n, 1, forward, st);
+    if (!rc) rc = reblock(tmp, out, nlines, n, slab_split(n, 1), so, st);
+    cudaFreeAsync(tmp, st);
+    return rc;
+  }
+  switch (n) {
+#define PFCS_CASE(NN) \
+  case NN:            \
+    return forward ? lines_n<NN, true>(in, out, nlines, si, so, st) : lines_n<NN, false>(in, out, nlines, si, so, st);
+    PFCS_POW2_CASES(PFCS_CASE)
+#undef PFCS_CASE
+    default:
+      break;
+  }
+  return fail(PFCS_E_UNSUPPORTED, "unsupported line length");
+}
+
+int launch_strided_c2c(const double2* in, double2* out, long long outer, int n, long long inner,
+                       bool forward, cudaStream_t st) {
+  if (outer <= 0 || inner <= 0) return PFCS_OK;
+  if (inner == 1) return launch_lines_c2c(in, out, outer, n, 1, 1, forward, st);
+  if (!is_pow2(n) || n > 4096) return launch_dft(in, out, outer, n, inner, forward, st);
+  switch (n) {
+#define PFCS_CASE(NN) \
+  case NN:            \
+    return forward ? strided_n<NN, true>(in, out, outer, inner, st) : strided_n<NN, false>(in, out, outer, inner, st);
+    PFCS_POW2_CASES(PFCS_CASE)
+#undef PFCS_CASE
+    default:
+      break;
+  }
+  return fail(PFCS_E_UNSUPPORTED, "unsupported line length");
+}
+
+int launch_dft(const double2* in, double2* out, long long outer, int n, long long inner, bool forward,
+               cudaStream_t st) {
+  if (outer <= 0 || inner <= 0) return PFCS_OK;
+  if (n > 16384) return fail(PFCS_E_UNSUPPORTED, "direct DFT limited to N <= 16384");
+  const double2* tw = twiddles(n);
+  if (!tw) return PFCS_E_CUDA;
+  int T = 2048 / n;
+  if (T < 1) T = 1;
+  if (T > 16) T = 16;
+  const bool contig = inner == 1;
+  const i64 tpo = contig ? 1 : (inner + T - 1) / T;
+  const i64 blocks = contig ? (outer + T - 1) / T : outer * tpo;
+  const size_t smem = (size_t)T * n * sizeof(double2);
+  if (ensure_smem((const void*)k_dft, smem)) return PFCS_E_CUDA;
+  int threads = T * n;
+  if (threads > 256) threads = 256;
+  if (threads < 32) threads = 32;
+  k_dft<<<(unsigned)blocks, threads, smem, st>>>(in, out, n, outer, inner, T, tpo, tw, forward ? 1 : 0,
+                                                 1.0 / (double)n);
+  return check_launch("k_dft");
+}
+
+}  // namespace pfcs

@@ -1,0 +1,259 @@
+// pfcs_x.cu — x-axis (slowest, strided) passes: real transforms and the fused
+// physical-space nonlinearity of the PFC step.
+//
+// Reference path replaced: the x stage of fftcore.fft_2d (fftcore.py:43-45,
+// forward axis order 0,1,2 pinned in fftcore.py:4-11) inside
+// distfft.dist_fft_forward/inverse (distfft.py:150-173), and the pointwise
+// `nl = psi.local ** 3` of pfc.pfc_step (pfc.py:109) with its realness /
+// max|psi| diagnostics (pfc.py:100-105, 124).
+//
+// Real transforms use the half-length packing: a real x-line of length N = 2M
+// is read as z[m] = x[2m] + i x[2m+1], transformed with an M-point complex
+// FFT, and split into the N/2+1 = M+1 Hermitian modes
+//     X[k] = 1/2 (Z_k + conj Z_{M-k}) - i/2 W_N^k (Z_k - conj Z_{M-k}),
+// the inverse (C2R) runs the same relations backwards, so every x pass moves
+// only the half spectrum through HBM.
+//
+// The fused cube pass (MODE_CUBE) keeps the whole x-line in shared memory:
+//   C2R pre-twiddle -> M-point inverse FFT -> scale fl(1/N) -> x^3 per real
+//   sample -> M-point forward FFT -> R2C post-twiddle
+// so the physical field never reaches HBM (1 read + 1 write per mode).
+#include "pfcs_fft.cuh"
+#include "pfcs_internal.h"
+#include "pfcs_diag.cuh"
+
+namespace pfcs {
+
+enum { MODE_R2C = 0, MODE_C2R = 1, MODE_CUBE = 2 };
+
+template <int M, int T, int MODE>
+__global__ void __launch_bounds__(T*(M / radix_R(M)))
+    k_real_x(const void* in_, void* out_, i64 inner, i64 tpo, const double2* __restrict__ twN,
+             double scale, double* diag) {
+  constexpr int R = radix_R(M);
+  constexpr int P = M / R;
+  constexpr int LS = line_stride(M);
+  extern __shared__ double2 smem[];
+  const int tid = threadIdx.x;
+  const int t = tid % T;
+  const int j = tid / T;
+  const i64 i = (i64)blockIdx.x * T + t;
+  const bool active = i < inner;
+  double2* sl = smem + t * LS;
+  double2 v[R];
+  double m_re = 0.0, m_im = 0.0;
+
+  if (MODE == MODE_R2C) {
+    const double* in = (const double*)in_;
+#pragma unroll
+    for (int e = 0; e < R; ++e) {
+      const i64 m = j + P * e;
+      v[e] = active ? make_double2(in[(2 * m) * inner + i], in[(2 * m + 1) * inner + i])
+                    : make_double2(0.0, 0.0);
+    }
+  } else {
+    // load the M+1 half-spectrum rows, then build Z'[k] from X[k], X[M-k]
+    const double2* in = (const double2*)in_;
+#pragma unroll
+    for (int e = 0; e < R; ++e) {
+      const i64 k = j + P * e;
+      double2 x = active ? in[k * inner + i] : make_double2(0.0, 0.0);
+      if (k == 0) x.y = 0.0;
+      sl[pad_idx((int)k)] = x;
+    }
+    if (j == 0) {
+      double2 x = active ? in[(i64)M * inner + i] : make_double2(0.0, 0.0);
+      x.y = 0.0;
+      sl[pad_idx(M)] = x;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int e = 0; e < R; ++e) {
+      const int k = j + P * e;
+      const double2 a = sl[pad_idx(k)];
+      const double2 bm = sl[pad_idx(M - k)];
+      const double2 b = make_double2(bm.x, -bm.y);  // conj X[M-k]
+      const double2 s = cadd(a, b);
+      const double2 d = csub(a, b);
+      // i * W_N^{-k} * d  ;  W_N^{-k} = conj(twN[k])
+      const double2 w = __ldg(&twN[k]);
+      const double2 wd = make_double2(fma(d.x, w.x, d.y * w.y), fma(d.y, w.x, -d.x * w.y));
+      v[e] = make_double2(s.x - wd.y, s.y + wd.x);
+    }
+  }
+
+  if (MODE == MODE_C2R || MODE == MODE_CUBE) {
+    fft_line<M, false, 2>(v, j, sl, twN);
+#pragma unroll
+    for (int e = 0; e < R; ++e) v[e] = make_double2(v[e].x * scale, v[e].y * scale);
+  }
+
+  if (MODE == MODE_C2R) {
+    if (active) {
+      double* out = (double*)out_;
+#pragma unroll
+      for (int e = 0; e < R; ++e) {
+        const i64 m = j + P * e;
+        out[(2 * m) * inner + i] = v[e].x;
+        out[(2 * m + 1) * inner + i] = v[e].y;
+      }
+    }
+    return;
+  }
+
+  if (MODE == MODE_CUBE) {
+#pragma unroll
+    for (int e = 0; e < R; ++e) {
+      const double a = v[e].x, b = v[e].y;
+      m_re = dmax_bits(m_re, fmax_nan(fabs(a), fabs(b)));
+      // psi**3 of a real sample; x*x*x in numpy's left-to-right order
+      v[e] = make_double2(__dmul_rn(__dmul_rn(a, a), a), __dmul_rn(__dmul_rn(b, b), b));
+    }
+    if (!active) m_re = 0.0;
+    diag_block_max(diag, m_re, m_im, m_re);
+  }
+
+  // forward M-point FFT, then the R2C split
+  fft_line<M, true, 2>(v, j, sl, twN);
+  __syncthreads();
+  stash_line<M>(v, j, sl);
+  __syncthreads();
+  double2* out = (double2*)out_;
+#pragma unroll
+  for (int e = 0; e < R; ++e) {
+    const int k = j + P * e;
+    const double2 zk = sl[pad_idx(k)];
+    const double2 zm = sl[pad_idx((M - k) & (M - 1))];
+    double2 x;
+    if (k == 0) {
+      x = make_double2(zk.x + zk.y, 0.0);
+    } else {
+      const double2 s = make_double2(zk.x + zm.x, zk.y - zm.y);  // Zk + conj Zm
+      const double2 d = make_double2(zk.x - zm.x, zk.y + zm.y);  // Zk - conj Zm
+      const double2 w = __ldg(&twN[k]);
+      const double2 wd = make_double2(fma(d.x, w.x, -d.y * w.y), fma(d.x, w.y, d.y * w.x));
+      // 1/2 (s - i wd)
+      x = make_double2(0.5 * (s.x + wd.y), 0.5 * (s.y - wd.x));
+    }
+    if (active) out[(i64)k * inner + i] = x;
+  }
+  if (j == 0 && active) {
+    const double2 z0 = sl[pad_idx(0)];
+    out[(i64)M * inner + i] = make_double2(z0.x - z0.y, 0.0);
+  }
+}
+
+// Fused complex-data cube pass (C2C mode, reference-layout fields):
+// inverse x FFT -> psi*(psi*psi) (numpy complex power, pfc.py:109) -> forward.
+template <int N, int T>
+__global__ void __launch_bounds__(T*(N / radix_R(N)))
+    k_cube_c2c(double2* data, i64 inner, i64 tpo, const double2* __restrict__ tw, double scale,
+               double* diag) {
+  constexpr int R = radix_R(N);
+  constexpr int P = N / R;
+  extern __shared__ double2 smem[];
+  const int tid = threadIdx.x;
+  const int t = tid % T;
+  const int j = tid / T;
+  const i64 i = (i64)blockIdx.x * T + t;
+  const bool active = i < inner;
+  double2* sl = smem + t * line_stride(N);
+  double2 v[R];
+#pragma unroll
+  for (int e = 0; e < R; ++e)
+    v[e] = active ? data[(i64)(j + P * e) * inner + i] : make_double2(0.0, 0.0);
+  fft_line<N, false>(v, j, sl, tw);
+  double m_re = 0.0, m_im = 0.0, m_abs = 0.0;
+#pragma unroll
+  for (int e = 0; e < R; ++e) {
+    const double a = v[e].x * scale, b = v[e].y * scale;
+    m_re = dmax_bits(m_re, fabs(a));
+    m_im = dmax_bits(m_im, fabs(b));
+    m_abs = dmax_bits(m_abs, hypot(a, b));
+    // c = psi*psi ; psi*c, no contraction (numpy cmul)
+    const double cr = __dsub_rn(__dmul_rn(a, a), __dmul_rn(b, b));
+    const double ci = __dadd_rn(__dmul_rn(a, b), __dmul_rn(b, a));
+    v[e] = make_double2(__dsub_rn(__dmul_rn(a, cr), __dmul_rn(b, ci)),
+                        __dadd_rn(__dmul_rn(a, ci), __dmul_rn(b, cr)));
+  }
+  if (!active) m_re = m_im = m_abs = 0.0;
+  diag_block_max(diag, m_re, m_im, m_abs);
+  fft_line<N, true>(v, j, sl, tw);
+  if (active) {
+#pragma unroll
+    for (int e = 0; e < R; ++e) data[(i64)(j + P * e) * inner + i] = v[e];
+  }
+}
+
+// ---------------------------------------------------------------- dispatch --
+
+template <int M, int MODE>
+static int real_x_m(const void* in, void* out, i64 inner, double* diag, cudaStream_t st) {
+  constexpr int T = TileCfg<M>::T_STRIDED;
+  constexpr int P = TileCfg<M>::P;
+  const size_t smem = (size_t)T * line_stride(M) * sizeof(double2);
+  const double2* twN = twiddles(2 * M);
+  if (!twN) return PFCS_E_CUDA;
+  const i64 blocks = (inner + T - 1) / T;
+  const void* f = (const void*)k_real_x<M, T, MODE>;
+  if (ensure_smem(f, smem)) return PFCS_E_CUDA;
+  k_real_x<M, T, MODE><<<(unsigned)blocks, T * P, smem, st>>>(in, out, inner, blocks, twN,
+                                                              1.0 / (double)(2 * M), diag);
+  return check_launch("k_real_x");
+}
+
+template <int N>
+static int cube_c2c_n(double2* data, i64 inner, double* diag, cudaStream_t st) {
+  constexpr int T = TileCfg<N>::T_STRIDED;
+  constexpr int P = TileCfg<N>::P;
+  const size_t smem = (size_t)T * line_stride(N) * sizeof(double2);
+  const double2* tw = twiddles(N);
+  if (!tw) return PFCS_E_CUDA;
+  const i64 blocks = (inner + T - 1) / T;
+  const void* f = (const void*)k_cube_c2c<N, T>;
+  if (ensure_smem(f, smem)) return PFCS_E_CUDA;
+  k_cube_c2c<N, T><<<(unsigned)blocks, T * P, smem, st>>>(data, inner, blocks, tw, 1.0 / (double)N, diag);
+  return check_launch("k_cube_c2c");
+}
+
+#define PFCS_M_CASES(MACRO) \
+  MACRO(2) MACRO(4) MACRO(8) MACRO(16) MACRO(32) MACRO(64) MACRO(128) MACRO(256) MACRO(512) \
+      MACRO(1024) MACRO(2048) MACRO(4096)
+
+int launch_real_x(const void* in, void* out, long long nx, long long inner, int mode, double* diag,
+                  cudaStream_t st) {
+  if (inner <= 0) return PFCS_OK;
+  if (!is_pow2(nx) || nx < 4 || nx > 8192)
+    return fail(PFCS_E_UNSUPPORTED, "real x transforms need a power-of-two nx in [4, 8192]");
+  const int M = (int)(nx / 2);
+  switch (M) {
+#define PFCS_CASE(MM)                                                      \
+  case MM:                                                                 \
+    if (mode == MODE_R2C) return real_x_m<MM, MODE_R2C>(in, out, inner, diag, st); \
+    if (mode == MODE_C2R) return real_x_m<MM, MODE_C2R>(in, out, inner, diag, st); \
+    return real_x_m<MM, MODE_CUBE>(in, out, inner, diag, st);
+    PFCS_M_CASES(PFCS_CASE)
+#undef PFCS_CASE
+    default:
+      break;
+  }
+  return fail(PFCS_E_UNSUPPORTED, "unsupported nx");
+}
+
+int launch_cube_c2c(void* data, long long nx, long long inner, double* diag, cudaStream_t st) {
+  if (inner <= 0) return PFCS_OK;
+  if (!is_pow2(nx) || nx < 2 || nx > 4096)
+    return fail(PFCS_E_UNSUPPORTED, "fused complex cube pass needs a power-of-two nx in [2, 4096]");
+  switch (nx) {
+#define PFCS_CASE(NN) \
+  case NN:            \
+    return cube_c2c_n<NN>((double2*)data, inner, diag, st);
+    PFCS_M_CASES(PFCS_CASE)
+#undef PFCS_CASE
+    default:
+      break;
+  }
+  return fail(PFCS_E_UNSUPPORTED, "unsupported nx");
+}
+
+}  // namespace pfcs
