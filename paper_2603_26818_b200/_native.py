@@ -98,8 +98,29 @@ def check(rc: int, what: str) -> None:
     raise NativeError(msg)
 
 
+# Launch accounting for bench.py: `launches` counts every kernel-launching
+# call; when `trace` is a list, each call appends (name, start, end) CUDA
+# events recorded on the current stream around the launch.
+launches = 0
+trace: list | None = None
+_NO_LAUNCH = {"pfcs_version", "pfcs_last_error", "pfcs_device_count", "pfcs_energy_scratch_bytes"}
+
+
 def call(name: str, *args) -> None:
-    check(getattr(load(), name)(*args), name)
+    global launches
+    fn = getattr(load(), name)
+    if trace is not None and name not in _NO_LAUNCH:
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record()
+        rc = fn(*args)
+        b.record()
+        trace.append((name, args, a, b))
+    else:
+        rc = fn(*args)
+    if name not in _NO_LAUNCH:
+        launches += 1
+    check(rc, name)
 
 
 def stream_ptr(stream: torch.cuda.Stream | None = None) -> int:

@@ -155,17 +155,19 @@ class _StepEngine:
     def invalidate(self) -> None:
         self.prepared_for = None
 
-    def step(self, state: PfcState, params: PfcParams) -> tuple[float, float, float, bool]:
+    def launch(self, state: PfcState, params: PfcParams, diag: torch.Tensor) -> None:
+        """Enqueue one step on the current stream (no host synchronisation);
+        ``diag`` (zeroed) receives the step's diagnostics."""
         g = self.g
         st = nat.stream_ptr()
         psi = state.psi_hat.dev
         if psi.dtype != torch.complex128 or not psi.is_contiguous():
             raise ValueError("psi_hat must be a contiguous complex128 slab")
         kx, ky, kz = self._sym_ptrs(state.symbols)
-        self.diag.zero_()
-        dptr = nat.ptr(self.diag)
+        dptr = nat.ptr(diag)
         key = (psi.data_ptr(), state.psi_hat._version)
         nlines = g.cx * g.ny
+        eps, dt = float(state.symbols.eps), float(params.dt)
         if self.fused:
             if self.prepared_for != key:
                 nat.call("pfcs_fft_zlines", nat.ptr(psi), nat.ptr(self.send), nlines, g.nz, 1, self.G, 0, st)
@@ -182,13 +184,17 @@ class _StepEngine:
                 sc, rc = g.fwd_counts()
                 self.worker.exchange(z, sc, self.recv_x, rc)
             nat.call("pfcs_pfc_update_z", nat.ptr(self.recv_x), nat.ptr(psi), nat.ptr(self.send),
-                     g.cx, g.ny, g.nz, self.G, self.G, kx, ky, kz, float(state.symbols.eps),
-                     float(params.dt), dptr, st)
-            self.prepared_for = (psi.data_ptr(), state.psi_hat._version)
+                     g.cx, g.ny, g.nz, self.G, self.G, kx, ky, kz, eps, dt, dptr, st)
         else:
             self._unfused(state, params, kx, ky, kz, dptr, st)
-        d = self.diag.view(nat.DIAG_SLOTS, nat.DIAG_VALS).cpu().numpy()
-        return float(d[:, 0].max()), float(d[:, 1].max()), float(d[:, 2].max()), bool(d[:, 3].max() > 0)
+        state.psi_hat._version += 1
+        self.prepared_for = (psi.data_ptr(), state.psi_hat._version) if self.fused else None
+
+    @staticmethod
+    def reduce_diag(d: np.ndarray) -> tuple[float, float, float, bool]:
+        d = d.reshape(-1, nat.DIAG_SLOTS, nat.DIAG_VALS)
+        return (d[..., 0].max(axis=1), d[..., 1].max(axis=1), d[..., 2].max(axis=1),
+                d[..., 3].max(axis=1) > 0)
 
     def _unfused(self, state, params, kx, ky, kz, dptr, st) -> None:
         w = self.worker
@@ -231,26 +237,45 @@ def _engine(state: PfcState) -> _StepEngine:
     return eng
 
 
+def _finish(state: PfcState, params: PfcParams, d: np.ndarray, first_index: int) -> None:
+    m_re, m_im, m_abs, bad = _StepEngine.reduce_diag(d)
+    for s in range(len(m_re)):
+        if state.psi_hat.dev.numel():
+            state.last_max_imag_ratio = float(m_im[s] / m_re[s]) if m_re[s] > 0 else 0.0
+        if bad[s]:
+            state.step_index = first_index + s
+            raise DivergenceError(first_index + s, float(m_abs[s]))
+    state.step_index = first_index + len(m_re)
+    for _ in range(len(m_re)):
+        state.sim_time += params.dt
+
+
 def pfc_step(state: PfcState, params: PfcParams) -> PfcState:
-    """Advance one semi-implicit step in place (pfc.py:96-128)."""
+    """Advance one semi-implicit step in place (pfc.py:96-128).  Reads the
+    step's diagnostics back (one small device->host copy) so a non-finite
+    field raises DivergenceError at this step, as in the reference."""
     eng = _engine(state)
-    m_re, m_im, m_abs, bad = eng.step(state, params)
-    state.psi_hat._version += 1
-    eng.prepared_for = (state.psi_hat.dev.data_ptr(), state.psi_hat._version) \
-        if eng.prepared_for is not None else None
-    if state.psi_hat.dev.numel():
-        state.last_max_imag_ratio = m_im / m_re if m_re > 0 else 0.0
-    if bad:
-        raise DivergenceError(state.step_index, m_abs)
-    state.step_index += 1
-    state.sim_time += params.dt
+    eng.diag.zero_()
+    eng.launch(state, params, eng.diag)
+    _finish(state, params, eng.diag.cpu().numpy(), state.step_index)
     return state
 
 
 def pfc_run(state: PfcState, params: PfcParams, n_steps: int) -> PfcState:
-    """``n_steps`` calls of :func:`pfc_step` (the batched hot loop)."""
-    for _ in range(int(n_steps)):
-        pfc_step(state, params)
+    """``n_steps`` steps enqueued back to back without host round trips (the
+    hot loop): per-step diagnostics land in a device array that is read once
+    at the end.  Divergence is still reported with the index of the first
+    non-finite step (the state has then advanced past it)."""
+    n_steps = int(n_steps)
+    if n_steps <= 0:
+        return state
+    eng = _engine(state)
+    per = nat.DIAG_SLOTS * nat.DIAG_VALS
+    diag = torch.zeros(n_steps * per, dtype=torch.float64, device=eng.device)
+    first = state.step_index
+    for s in range(n_steps):
+        eng.launch(state, params, diag[s * per:(s + 1) * per])
+    _finish(state, params, diag.cpu().numpy(), first)
     return state
 
 
