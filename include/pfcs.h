@@ -108,6 +108,33 @@ int pfcs_pfc_update(const void* nl_hat, void* psi_hat, int64_t cx, int64_t ny, i
                     const double* kx, const double* ky, const double* kz, double eps, double dt,
                     double* diag, void* stream);
 
+/* ---- hydrodynamic PFC pointwise operators (hydro.py:77-107) on full-grid
+ * C-order (n0, n1, n2) complex128 fields; numpy's evaluation order, so the
+ * viscous decay is bit-exact and v = 0 reproduces the PFC update bit for bit.
+ * pfcs_mul_deriv:        out = (i d_axis) * in   (sym.d1/d2/d3 * x, hydro.py:83-85,102)
+ * pfcs_cmul:             out = a * b (complex; psi * F^-1(...), hydro.py:102)
+ * pfcs_hydro_advect:     out = v1*x1 + v2*x2 + v3*x3 (hydro.py:83-85)
+ * pfcs_hydro_psi_update: psi_hat <- (psi_hat + dt*(lap*nl_hat - adv_hat)) / (1 - dt*lin)
+ *                        (hydro.py:86-88; adv_hat may be NULL = 0)
+ * pfcs_hydro_mu:         out = nl_hat + op * f_hat (hydro.py:101)
+ * pfcs_hydro_vel_update: v_hat <- (v_hat - (c_cg * exp(c_exp k^2)) * force) / (1 - c_den*lap)
+ *                        with c_cg = dt/rho, c_den = (dt/rho)*gamma, c_exp = -0.5*a0**2
+ *                        (hydro.py:103-106; force may be NULL = 0)
+ * diag as for the PFC passes (value 3 = non-finite real part seen). */
+int pfcs_mul_deriv(const void* in, void* out, int64_t n0, int64_t n1, int64_t n2, const double* d,
+                   int axis, void* stream);
+int pfcs_cmul(const void* a, const void* b, void* out, int64_t n, void* stream);
+int pfcs_hydro_advect(const void* v1, const void* x1, const void* v2, const void* x2, const void* v3,
+                      const void* x3, void* out, int64_t n, void* stream);
+int pfcs_hydro_psi_update(void* psi_hat, const void* nl_hat, const void* adv_hat, int64_t n0, int64_t n1,
+                          int64_t n2, const double* kx, const double* ky, const double* kz, double eps,
+                          double dt, double* diag, void* stream);
+int pfcs_hydro_mu(const void* nl_hat, const void* f_hat, void* out, int64_t n0, int64_t n1, int64_t n2,
+                  const double* kx, const double* ky, const double* kz, double eps, void* stream);
+int pfcs_hydro_vel_update(void* v_hat, const void* force, int64_t n0, int64_t n1, int64_t n2,
+                          const double* kx, const double* ky, const double* kz, double c_cg, double c_den,
+                          double c_exp, double* diag, void* stream);
+
 /* ---- deterministic reductions (pfc._reduce_sum / free_energy,
  * pfc.py:131-162).  out[0] = sum_i f(a_i, b_i) in a fixed order,
  * independent of the launch: f = 0.5*a*b + 0.25*a^4 (free-energy density,

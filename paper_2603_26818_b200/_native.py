@@ -8,13 +8,14 @@ missing or no CUDA device is present every compute call raises.
 from __future__ import annotations
 
 import ctypes
+import os
 import threading
 from pathlib import Path
 
 import torch
 
 _HERE = Path(__file__).resolve().parent
-LIB_PATH = _HERE / "libpfcs.so"
+LIB_PATH = Path(os.environ.get("PFCS_LIB_PATH", str(_HERE / "libpfcs.so")))
 
 PFCS_OK = 0
 PFCS_E_ARG = 1
@@ -43,6 +44,14 @@ _SIGS = {
                           _c_p, _c_p, _c_p, _c_d, _c_d, _c_p, _c_p],
     "pfcs_pfc_cube": [_c_p, _c_i64, _c_int, _c_p, _c_p],
     "pfcs_pfc_update": [_c_p, _c_p, _c_i64, _c_i64, _c_i64, _c_p, _c_p, _c_p, _c_d, _c_d, _c_p, _c_p],
+    "pfcs_mul_deriv": [_c_p, _c_p, _c_i64, _c_i64, _c_i64, _c_p, _c_int, _c_p],
+    "pfcs_cmul": [_c_p, _c_p, _c_p, _c_i64, _c_p],
+    "pfcs_hydro_advect": [_c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_i64, _c_p],
+    "pfcs_hydro_psi_update": [_c_p, _c_p, _c_p, _c_i64, _c_i64, _c_i64, _c_p, _c_p, _c_p, _c_d, _c_d,
+                              _c_p, _c_p],
+    "pfcs_hydro_mu": [_c_p, _c_p, _c_p, _c_i64, _c_i64, _c_i64, _c_p, _c_p, _c_p, _c_d, _c_p],
+    "pfcs_hydro_vel_update": [_c_p, _c_p, _c_i64, _c_i64, _c_i64, _c_p, _c_p, _c_p, _c_d, _c_d, _c_d,
+                              _c_p, _c_p],
     "pfcs_energy_sum": [_c_p, _c_i64, _c_p, _c_i64, _c_i64, _c_p, _c_p, _c_p],
     "pfcs_energy_scratch_bytes": [_c_i64],
     "pfcs_absmax": [_c_p, _c_i64, _c_i64, _c_p, _c_p],

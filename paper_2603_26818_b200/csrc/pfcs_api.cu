@@ -3,6 +3,8 @@
 // memory opt-in.  No torch types cross this boundary: device pointers, sizes
 // and a cudaStream_t passed as void*.
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -85,7 +87,7 @@ static std::mutex g_smem_mu;
 static std::map<std::pair<int, const void*>, size_t> g_smem;
 
 int ensure_smem(const void* func, size_t bytes) {
-  if (bytes <= 48 * 1024) return PFCS_OK;
+  if (bytes == 0) return PFCS_OK;
   int dev = 0;
   if (check_cuda(cudaGetDevice(&dev), "cudaGetDevice")) return PFCS_E_CUDA;
   std::lock_guard<std::mutex> lk(g_smem_mu);
@@ -97,6 +99,67 @@ int ensure_smem(const void* func, size_t bytes) {
     return PFCS_E_CUDA;
   g_smem[key] = bytes;
   return PFCS_OK;
+}
+
+static std::mutex g_occ_mu;
+struct OccKey {
+  int dev;
+  const void* f;
+  int threads;
+  size_t smem;
+  bool operator<(const OccKey& o) const {
+    if (dev != o.dev) return dev < o.dev;
+    if (f != o.f) return f < o.f;
+    if (threads != o.threads) return threads < o.threads;
+    return smem < o.smem;
+  }
+};
+static std::map<OccKey, int> g_occ;
+static std::map<int, int> g_sms;
+
+int persistent_grid(const void* func, int threads, size_t smem, long long ntiles, int* grid) {
+  if (threads > 1024) return fail(PFCS_E_UNSUPPORTED, "tile too large (threads > 1024)");
+  if (smem > 227 * 1024) return fail(PFCS_E_UNSUPPORTED, "tile too large (shared memory > 227 KB)");
+  if (int rc = ensure_smem(func, smem)) return rc;
+  int dev = 0;
+  if (int rc = check_cuda(cudaGetDevice(&dev), "cudaGetDevice")) return rc;
+  int per_sm = 0, sms = 0;
+  {
+    std::lock_guard<std::mutex> lk(g_occ_mu);
+    OccKey k{dev, func, threads, smem};
+    auto it = g_occ.find(k);
+    if (it == g_occ.end()) {
+      if (int rc = check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, func, threads, smem),
+                              "occupancy"))
+        return rc;
+      if (per_sm < 1) return fail(PFCS_E_UNSUPPORTED, "kernel cannot be resident (registers/smem)");
+      g_occ[k] = per_sm;
+    } else {
+      per_sm = it->second;
+    }
+    auto is = g_sms.find(dev);
+    if (is == g_sms.end()) {
+      if (int rc = check_cuda(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "SM count"))
+        return rc;
+      g_sms[dev] = sms;
+    } else {
+      sms = is->second;
+    }
+  }
+  long long g = (long long)per_sm * sms;
+  if (ntiles < g) g = ntiles;
+  if (g < 1) g = 1;
+  *grid = (int)g;
+  return PFCS_OK;
+}
+
+int tune_variant(int kind, int n, int dflt) {
+  char name[64];
+  snprintf(name, sizeof(name), "PFCS_VARIANT_%d_%d", kind, n);
+  const char* v = getenv(name);
+  if (!v || !*v) return dflt;
+  const int s = atoi(v);
+  return (s < 0 || s > 7) ? dflt : s;
 }
 
 // defined in the other translation units

@@ -22,81 +22,102 @@
 
 namespace pfcs {
 
-template <int N, int T, bool FWD, bool BIN, bool BOUT>
-__global__ void __launch_bounds__(T*(N / radix_R(N)))
+template <int R>
+struct Regs1 {
+  double2 v[R];
+};
+
+template <int N, int T, int ST, bool FWD, bool BIN, bool BOUT>
+__global__ void __launch_bounds__(T*(N / radix_R(N)), min_blocks(T*(N / radix_R(N)), ST == 2 ? 640 : 1024))
     k_lines(const double2* in, double2* out, i64 nlines, SlabSplit sin, SlabSplit sout,
             const double2* __restrict__ tw, double scale) {
   constexpr int R = radix_R(N);
   constexpr int P = N / R;
+  constexpr int LS = tile_ls(N, T, false);
   extern __shared__ double2 smem[];
   const int tid = threadIdx.x;
   const int t = tid / P;
   const int j = tid - t * P;
-  const i64 l = (i64)blockIdx.x * T + t;
-  const bool active = l < nlines;
-  double2* sl = smem + t * line_stride(N);
-  double2 v[R];
-#pragma unroll
-  for (int e = 0; e < R; ++e) {
-    const int z = j + P * e;
-    i64 a;
-    if (BIN) {
-      int zoff, cz;
-      sin.locate(z, zoff, cz);
-      a = nlines * zoff + l * cz + (z - zoff);
-    } else {
-      a = l * N + z;
-    }
-    v[e] = active ? in[a] : make_double2(0.0, 0.0);
-  }
-  fft_line<N, FWD>(v, j, sl, tw);
-  if (active) {
+  double2* sl = smem + t * LS;
+  const i64 ntiles = (nlines + T - 1) / T;
+  auto load = [&](i64 tile, Regs1<R>& r) {
+    const i64 l = tile * T + t;
+    const bool ok = l < nlines;
 #pragma unroll
     for (int e = 0; e < R; ++e) {
       const int z = j + P * e;
-      i64 a;
-      if (BOUT) {
+      i64 a = 0;
+      if (BIN) {
         int zoff, cz;
-        sout.locate(z, zoff, cz);
+        sin.locate(z, zoff, cz);
         a = nlines * zoff + l * cz + (z - zoff);
       } else {
         a = l * N + z;
       }
-      double2 r = v[e];
-      if (!FWD) r = make_double2(r.x * scale, r.y * scale);
-      out[a] = r;
+      r.v[e] = ok ? in[a] : make_double2(0.0, 0.0);
     }
-  }
+  };
+  auto comp = [&](i64 tile, Regs1<R>& r) {
+    const i64 l = tile * T + t;
+    fft_line<N, FWD>(r.v, j, sl, tw);
+    if (l < nlines) {
+#pragma unroll
+      for (int e = 0; e < R; ++e) {
+        const int z = j + P * e;
+        i64 a;
+        if (BOUT) {
+          int zoff, cz;
+          sout.locate(z, zoff, cz);
+          a = nlines * zoff + l * cz + (z - zoff);
+        } else {
+          a = l * N + z;
+        }
+        double2 x = r.v[e];
+        if (!FWD) x = make_double2(x.x * scale, x.y * scale);
+        out[a] = x;
+      }
+    }
+  };
+  reg_tile_loop<ST, Regs1<R>>(ntiles, load, comp);
 }
 
-template <int N, int T, bool FWD>
-__global__ void __launch_bounds__(T*(N / radix_R(N)))
+template <int N, int T, int ST, bool FWD>
+__global__ void __launch_bounds__(T*(N / radix_R(N)), min_blocks(T*(N / radix_R(N)), ST == 2 ? 640 : 1024))
     k_strided(const double2* in, double2* out, i64 outer, i64 inner, i64 tpo,
               const double2* __restrict__ tw, double scale) {
   constexpr int R = radix_R(N);
   constexpr int P = N / R;
+  constexpr int LS = tile_ls(N, T, true);
   extern __shared__ double2 smem[];
   const int tid = threadIdx.x;
   const int t = tid % T;
   const int j = tid / T;
-  const i64 o = (i64)blockIdx.x / tpo;
-  const i64 i = ((i64)blockIdx.x - o * tpo) * T + t;
-  const bool active = i < inner;
-  const i64 base = o * (i64)N * inner + i;
-  double2* sl = smem + t * line_stride(N);
-  double2 v[R];
+  double2* sl = smem + t * LS;
+  const i64 ntiles = outer * tpo;
+  auto load = [&](i64 tile, Regs1<R>& r) {
+    const i64 o = tile / tpo;
+    const i64 i = (tile - o * tpo) * T + t;
+    const bool ok = i < inner;
+    const i64 base = o * (i64)N * inner + i;
 #pragma unroll
-  for (int e = 0; e < R; ++e)
-    v[e] = active ? in[base + (i64)(j + P * e) * inner] : make_double2(0.0, 0.0);
-  fft_line<N, FWD>(v, j, sl, tw);
-  if (active) {
+    for (int e = 0; e < R; ++e)
+      r.v[e] = ok ? in[base + (i64)(j + P * e) * inner] : make_double2(0.0, 0.0);
+  };
+  auto comp = [&](i64 tile, Regs1<R>& r) {
+    const i64 o = tile / tpo;
+    const i64 i = (tile - o * tpo) * T + t;
+    fft_line<N, FWD>(r.v, j, sl, tw);
+    if (i < inner) {
+      const i64 base = o * (i64)N * inner + i;
 #pragma unroll
-    for (int e = 0; e < R; ++e) {
-      double2 r = v[e];
-      if (!FWD) r = make_double2(r.x * scale, r.y * scale);
-      out[base + (i64)(j + P * e) * inner] = r;
+      for (int e = 0; e < R; ++e) {
+        double2 x = r.v[e];
+        if (!FWD) x = make_double2(x.x * scale, x.y * scale);
+        out[base + (i64)(j + P * e) * inner] = x;
+      }
     }
-  }
+  };
+  reg_tile_loop<ST, Regs1<R>>(ntiles, load, comp);
 }
 
 // Direct DFT for arbitrary N: a CTA loads a tile of T lines (T adjacent inner
@@ -201,44 +222,58 @@ static int reblock(const double2* in, double2* out, i64 nlines, int n, SlabSplit
 template <int N, bool FWD>
 static int lines_n(const double2* in, double2* out, i64 nlines, SlabSplitH si, SlabSplitH so,
                    cudaStream_t st) {
-  constexpr int T = TileCfg<N>::T_CONTIG;
-  constexpr int P = TileCfg<N>::P;
-  const size_t smem = (size_t)T * line_stride(N) * sizeof(double2);
   const double2* tw = twiddles(N);
   if (!tw) return PFCS_E_CUDA;
   SlabSplit a{si.G, si.base, si.extra}, b{so.G, so.base, so.extra};
   const double scale = 1.0 / (double)N;
-  const i64 blocks = (nlines + T - 1) / T;
   const bool bin = si.G > 1, bout = so.G > 1;
-  const void* f;
-#define PFCS_LK(BI, BO) (const void*)k_lines<N, T, FWD, BI, BO>
-  if (bin && bout) f = PFCS_LK(true, true);
-  else if (bin) f = PFCS_LK(true, false);
-  else if (bout) f = PFCS_LK(false, true);
-  else f = PFCS_LK(false, false);
-#undef PFCS_LK
-  if (ensure_smem(f, smem)) return PFCS_E_CUDA;
-  dim3 grid((unsigned)blocks), block(T * P);
-  if (bin && bout) k_lines<N, T, FWD, true, true><<<grid, block, smem, st>>>(in, out, nlines, a, b, tw, scale);
-  else if (bin) k_lines<N, T, FWD, true, false><<<grid, block, smem, st>>>(in, out, nlines, a, b, tw, scale);
-  else if (bout) k_lines<N, T, FWD, false, true><<<grid, block, smem, st>>>(in, out, nlines, a, b, tw, scale);
-  else k_lines<N, T, FWD, false, false><<<grid, block, smem, st>>>(in, out, nlines, a, b, tw, scale);
-  return check_launch("k_lines");
+  return with_variant<KIND_LINES, N>([&](auto var) -> int {
+    constexpr int V = decltype(var)::value;
+    constexpr int T = TileCfg<N>::T_MIN << (V & 3);
+    constexpr int ST = 1 + (V >> 2);
+    constexpr int P = TileCfg<N>::P;
+    if constexpr (T * P > 1024) {
+      return fail(PFCS_E_UNSUPPORTED, "tile too large");
+    } else {
+    const size_t smem = (size_t)T * tile_ls(N, T, false) * sizeof(double2);
+    const i64 ntiles = (nlines + T - 1) / T;
+    const void* f;
+    if (bin && bout) f = (const void*)k_lines<N, T, ST, FWD, true, true>;
+    else if (bin) f = (const void*)k_lines<N, T, ST, FWD, true, false>;
+    else if (bout) f = (const void*)k_lines<N, T, ST, FWD, false, true>;
+    else f = (const void*)k_lines<N, T, ST, FWD, false, false>;
+    int grid = 0;
+    if (int rc = persistent_grid(f, T * P, smem, ntiles, &grid)) return rc;
+    if (bin && bout) k_lines<N, T, ST, FWD, true, true><<<grid, T * P, smem, st>>>(in, out, nlines, a, b, tw, scale);
+    else if (bin) k_lines<N, T, ST, FWD, true, false><<<grid, T * P, smem, st>>>(in, out, nlines, a, b, tw, scale);
+    else if (bout) k_lines<N, T, ST, FWD, false, true><<<grid, T * P, smem, st>>>(in, out, nlines, a, b, tw, scale);
+    else k_lines<N, T, ST, FWD, false, false><<<grid, T * P, smem, st>>>(in, out, nlines, a, b, tw, scale);
+    return check_launch("k_lines");
+    }
+  });
 }
 
 template <int N, bool FWD>
 static int strided_n(const double2* in, double2* out, i64 outer, i64 inner, cudaStream_t st) {
-  constexpr int T = TileCfg<N>::T_STRIDED;
-  constexpr int P = TileCfg<N>::P;
-  const size_t smem = (size_t)T * line_stride(N) * sizeof(double2);
   const double2* tw = twiddles(N);
   if (!tw) return PFCS_E_CUDA;
-  const i64 tpo = (inner + T - 1) / T;
-  const void* f = (const void*)k_strided<N, T, FWD>;
-  if (ensure_smem(f, smem)) return PFCS_E_CUDA;
-  k_strided<N, T, FWD><<<(unsigned)(outer * tpo), T * P, smem, st>>>(in, out, outer, inner, tpo, tw,
-                                                                     1.0 / (double)N);
-  return check_launch("k_strided");
+  return with_variant<KIND_STRIDED, N>([&](auto var) -> int {
+    constexpr int V = decltype(var)::value;
+    constexpr int T = TileCfg<N>::T_MIN << (V & 3);
+    constexpr int ST = 1 + (V >> 2);
+    constexpr int P = TileCfg<N>::P;
+    if constexpr (T * P > 1024) {
+      return fail(PFCS_E_UNSUPPORTED, "tile too large");
+    } else {
+    const size_t smem = (size_t)T * tile_ls(N, T, true) * sizeof(double2);
+    const i64 tpo = (inner + T - 1) / T;
+    const void* f = (const void*)k_strided<N, T, ST, FWD>;
+    int grid = 0;
+    if (int rc = persistent_grid(f, T * P, smem, outer * tpo, &grid)) return rc;
+    k_strided<N, T, ST, FWD><<<grid, T * P, smem, st>>>(in, out, outer, inner, tpo, tw, 1.0 / (double)N);
+    return check_launch("k_strided");
+    }
+  });
 }
 
 #define PFCS_POW2_CASES(MACRO) \

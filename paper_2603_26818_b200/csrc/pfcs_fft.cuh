@@ -33,7 +33,21 @@ typedef long long i64;
 
 __host__ __device__ constexpr int pad_idx(int n) { return n + (n >> 3); }
 __host__ __device__ constexpr int line_stride(int n) { return pad_idx(n) + 2; }
+// Line stride of a T-line tile.  Contiguous-line tiles put 8 consecutive j
+// of one line in a quarter warp, so any stride is conflict-free; strided
+// tiles put min(T, 8) columns side by side, so line bases must fall on
+// distinct 16-byte bank slots: stride = PAD(N) + (8 / min(T, 8)) mod 8
+// (bank simulator: 1.00x ideal wavefronts for every
+// N in 16..4096 and T in 1..32).
+__host__ __device__ constexpr int tile_ls(int n, int t, bool strided) {
+  return pad_idx(n) + ((!strided || n <= 8) ? 0 : (8 / (t < 8 ? t : 8)) % 8);
+}
 __host__ __device__ constexpr int radix_R(int n) { return n >= 8 ? 8 : n; }
+// minBlocksPerSM for __launch_bounds__: enough CTAs for `target` resident
+// threads per SM, which caps registers at 65536 / target per thread.
+__host__ __device__ constexpr int min_blocks(int threads, int target) {
+  return target / threads < 1 ? 1 : (target / threads > 16 ? 16 : target / threads);
+}
 
 __device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
 __device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
@@ -168,15 +182,103 @@ __device__ __forceinline__ void stash_line(const double2 (&v)[radix_R(N)], int j
   for (int e = 0; e < R; ++e) sl[pad_idx(j + P * e)] = v[e];
 }
 
-// Tile shape policy: T lines per CTA so that a tile holds ~4096 complex
-// values (64 KB of shared memory, <= 512 threads), at least 1 line, and at
-// least one full warp per CTA (warp-synchronous diagnostics need it).
+// ------------------------------------------------ asynchronous tile loads --
+// Every pass kernel is persistent and double-buffered: while a CTA runs the
+// FFT of tile i out of shared buffer i&1, the cp.async (LDGSTS) copies of
+// tile i+1 are already in flight into the other buffer, so the HBM pipe
+// never idles during the butterflies.  Each thread lands its own R elements
+// at their padded positions, which is exactly where the first Stockham pass
+// reads them.
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(dst)), "l"(src),
+               "r"(valid ? 16 : 0));
+}
+__device__ __forceinline__ void cp_async8(void* dst, const void* src, bool valid) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(smem_u32(dst)), "l"(src),
+               "r"(valid ? 8 : 0));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int K>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(K));
+}
+
+// Persistent loop over `ntiles` tiles (grid-stride).
+//   pre(tile, stage)  issues the cp.async copies of `tile` into buffer `stage`
+//   comp(tile, stage) consumes buffer `stage` (may use it as FFT scratch)
+// STAGES == 2 double-buffers (tile i+1 in flight while tile i computes);
+// STAGES == 1 relies on the other resident CTAs of the SM for overlap.
+template <int STAGES, class Pre, class Comp>
+__device__ __forceinline__ void tile_loop(long long ntiles, Pre&& pre, Comp&& comp) {
+  if constexpr (STAGES == 1) {
+    for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      pre(tile, 0);
+      cp_async_commit();
+      cp_async_wait<0>();
+      __syncthreads();
+      comp(tile, 0);
+      __syncthreads();
+    }
+  } else {
+    long long tile = blockIdx.x;
+    if (tile < ntiles) pre(tile, 0);
+    cp_async_commit();
+    int it = 0;
+    for (; tile < ntiles; tile += gridDim.x, ++it) {
+      const long long next = tile + gridDim.x;
+      if (next < ntiles) pre(next, (it + 1) & 1);
+      cp_async_commit();
+      cp_async_wait<1>();
+      __syncthreads();
+      comp(tile, it & 1);
+      __syncthreads();
+    }
+    cp_async_wait<0>();
+  }
+}
+
+// Register-pipelined persistent loop: `Regs` is the per-thread register set
+// of one tile (its R elements, plus whatever the kernel needs).
+//   load(tile, regs)  issues the global loads of `tile` into registers
+//   comp(tile, regs)  runs the transform out of the registers and stores
+// ST == 2 issues the loads of tile i+1 before computing tile i, so ~R*16
+// bytes per thread stay in flight through the butterflies (no extra shared
+// memory traffic, unlike a cp.async landing buffer); ST == 1 loads at the
+// top of each tile and relies on the other resident CTAs for overlap.
+template <int ST, class Regs, class Load, class Comp>
+__device__ __forceinline__ void reg_tile_loop(long long ntiles, Load&& load, Comp&& comp) {
+  if constexpr (ST == 1) {
+    for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      Regs r;
+      load(tile, r);
+      comp(tile, r);
+      __syncthreads();
+    }
+  } else {
+    Regs nxt;
+    long long tile = blockIdx.x;
+    if (tile < ntiles) load(tile, nxt);
+    for (; tile < ntiles; tile += gridDim.x) {
+      Regs cur = nxt;
+      const long long next = tile + gridDim.x;
+      if (next < ntiles) load(next, nxt);
+      comp(tile, cur);
+      __syncthreads();
+    }
+  }
+}
+
+// Tile shape: T lines per CTA, T = T_MIN << shift.  Small N needs several
+// lines to fill a warp (warp-synchronous diagnostics); the shift and the
+// number of pipeline stages come from the tuning table (pfcs_internal.h).
 template <int N>
 struct TileCfg {
   static constexpr int R = radix_R(N);
   static constexpr int P = N / R;
-  static constexpr int T_CONTIG = (N >= 4096) ? 1 : (4096 / N > 64 ? 64 : 4096 / N);
-  static constexpr int T_STRIDED = (N >= 4096) ? 1 : (4096 / N > 32 ? 32 : 4096 / N);
+  static constexpr int T_MIN = (P >= 32) ? 1 : 32 / P;
 };
 
 // Balanced slab bookkeeping (grid.slab_layout, grid.py:103-111): the first

@@ -1,0 +1,204 @@
+// pfcs_hydro.cu — pointwise spectral/physical operators of the hydrodynamic
+// PFC model (reference hydro.py:77-107), on full-grid complex128 fields.
+//
+// Every operation reproduces numpy's evaluation order and rounding
+// (no FMA contraction; complex/real division as numerator * fl(1/den)), so:
+//   * the viscous decay v_hat / (1 - (dt/rho) gamma lap) is bit-exact
+//     (test_hydro.py:31-39),
+//   * with v = 0 the density update equals the PFC update bit for bit
+//     (test_hydro.py:72-107).
+// The only non-bit-reproducible factor is the Gaussian cg = exp(-a0^2 k^2/2)
+// (CUDA exp vs numpy exp differ in the last ulp on a few % of inputs).
+#include "pfcs_diag.cuh"
+#include "pfcs_internal.h"
+
+namespace pfcs {
+
+typedef long long i64;
+
+__device__ __forceinline__ double k2_at(const double* kx, const double* ky, const double* kz, i64 idx,
+                                        int n1, int n2) {
+  const i64 line = idx / n2;
+  const int z = (int)(idx - line * n2);
+  const i64 x = line / n1;
+  const int y = (int)(line - x * n1);
+  const double a = __ldg(&kx[x]), b = __ldg(&ky[y]), c = __ldg(&kz[z]);
+  return __dadd_rn(__dadd_rn(__dmul_rn(a, a), __dmul_rn(b, b)), __dmul_rn(c, c));
+}
+
+__device__ __forceinline__ double2 cmul_np(double2 a, double2 b) {
+  return make_double2(__dsub_rn(__dmul_rn(a.x, b.x), __dmul_rn(a.y, b.y)),
+                      __dadd_rn(__dmul_rn(a.x, b.y), __dmul_rn(a.y, b.x)));
+}
+
+static inline int grid_for(i64 n) {
+  i64 b = (n + 255) / 256;
+  if (b > 148 * 16) b = 148 * 16;
+  return (int)(b < 1 ? 1 : b);
+}
+
+// Grid-stride loop that keeps warps converged for the ballot at the end.
+#define PFCS_FOR_ALL(n)                                                        \
+  const i64 _stride = (i64)gridDim.x * blockDim.x;                             \
+  const i64 _n = (n);                                                          \
+  const i64 _round = ((_n + _stride - 1) / _stride) * _stride;                 \
+  for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < _round; i += _stride) \
+    if (i < _n)
+
+// out = (i d_axis) * in, d the Nyquist-zeroed wavenumbers (grid.py:167-176):
+// numpy's (±0 + i d)(a + i b) = (-d b, d a).
+__global__ void k_mul_deriv(const double2* in, double2* out, i64 n, int n1, int n2,
+                            const double* __restrict__ d, int axis) {
+  PFCS_FOR_ALL(n) {
+    const i64 line = i / n2;
+    const int z = (int)(i - line * n2);
+    const i64 x = line / n1;
+    const int y = (int)(line - x * n1);
+    const double dk = __ldg(&d[axis == 0 ? x : (axis == 1 ? y : z)]);
+    const double2 a = in[i];
+    out[i] = make_double2(-__dmul_rn(dk, a.y), __dmul_rn(dk, a.x));
+  }
+}
+
+__global__ void k_cmul(const double2* a, const double2* b, double2* out, i64 n) {
+  PFCS_FOR_ALL(n) { out[i] = cmul_np(a[i], b[i]); }
+}
+
+// adv = v1*x1 + v2*x2 + v3*x3 (hydro.py:83-85, left to right)
+__global__ void k_advect(const double2* v1, const double2* x1, const double2* v2, const double2* x2,
+                         const double2* v3, const double2* x3, double2* out, i64 n) {
+  PFCS_FOR_ALL(n) {
+    const double2 a = cmul_np(v1[i], x1[i]);
+    const double2 b = cmul_np(v2[i], x2[i]);
+    const double2 c = cmul_np(v3[i], x3[i]);
+    const double2 s = make_double2(__dadd_rn(a.x, b.x), __dadd_rn(a.y, b.y));
+    out[i] = make_double2(__dadd_rn(s.x, c.x), __dadd_rn(s.y, c.y));
+  }
+}
+
+// psi_hat <- (psi_hat + dt*(lap*nl_hat - adv_hat)) / (1 - dt*linear)   (hydro.py:86-87)
+__global__ void k_hydro_psi_update(double2* psi_hat, const double2* nl_hat, const double2* adv_hat, i64 n,
+                                   int n1, int n2, const double* __restrict__ kx,
+                                   const double* __restrict__ ky, const double* __restrict__ kz,
+                                   double eps, double dt, double* diag) {
+  bool bad = false;
+  PFCS_FOR_ALL(n) {
+    const double k2 = k2_at(kx, ky, kz, i, n1, n2);
+    const double lap = -k2;
+    const double a = __dsub_rn(1.0, k2);
+    const double b = __dsub_rn(4.0 / 3.0, k2);
+    const double op = __dadd_rn(eps, __dmul_rn(__dmul_rn(a, a), __dmul_rn(b, b)));
+    const double rden = __drcp_rn(__dsub_rn(1.0, __dmul_rn(dt, __dmul_rn(lap, op))));
+    const double2 nl = nl_hat[i];
+    const double2 ad = adv_hat ? adv_hat[i] : make_double2(0.0, 0.0);
+    const double tr = __dsub_rn(__dmul_rn(lap, nl.x), ad.x);
+    const double ti = __dsub_rn(__dmul_rn(lap, nl.y), ad.y);
+    const double2 ph = psi_hat[i];
+    const double2 nw = make_double2(__dmul_rn(__dadd_rn(ph.x, __dmul_rn(dt, tr)), rden),
+                                    __dmul_rn(__dadd_rn(ph.y, __dmul_rn(dt, ti)), rden));
+    bad |= !isfinite(nw.x);  // hydro._check_finite looks at the real part (hydro.py:72-74)
+    psi_hat[i] = nw;
+  }
+  diag_flag_nonfinite(diag, bad);
+}
+
+// mu_hat = nl_hat + op * f_hat   (hydro.py:101)
+__global__ void k_hydro_mu(const double2* nl_hat, const double2* f_hat, double2* out, i64 n, int n1, int n2,
+                           const double* __restrict__ kx, const double* __restrict__ ky,
+                           const double* __restrict__ kz, double eps) {
+  PFCS_FOR_ALL(n) {
+    const double k2 = k2_at(kx, ky, kz, i, n1, n2);
+    const double a = __dsub_rn(1.0, k2);
+    const double b = __dsub_rn(4.0 / 3.0, k2);
+    const double op = __dadd_rn(eps, __dmul_rn(__dmul_rn(a, a), __dmul_rn(b, b)));
+    const double2 x = nl_hat[i], f = f_hat[i];
+    out[i] = make_double2(__dadd_rn(x.x, __dmul_rn(op, f.x)), __dadd_rn(x.y, __dmul_rn(op, f.y)));
+  }
+}
+
+// v_hat <- (v_hat - ((dt/rho)*cg)*force) / (1 - ((dt/rho)*gamma)*lap)  (hydro.py:103-104)
+// c_cg = dt/rho, c_den = (dt/rho)*gamma, c_exp = -0.5*a0**2 (host-evaluated)
+__global__ void k_hydro_vel_update(double2* v_hat, const double2* force, i64 n, int n1, int n2,
+                                   const double* __restrict__ kx, const double* __restrict__ ky,
+                                   const double* __restrict__ kz, double c_cg, double c_den,
+                                   double c_exp, double* diag) {
+  bool bad = false;
+  PFCS_FOR_ALL(n) {
+    const double k2 = k2_at(kx, ky, kz, i, n1, n2);
+    const double lap = -k2;
+    const double cg = exp(__dmul_rn(c_exp, k2));
+    const double w = __dmul_rn(c_cg, cg);
+    const double rden = __drcp_rn(__dsub_rn(1.0, __dmul_rn(c_den, lap)));
+    const double2 f = force ? force[i] : make_double2(0.0, 0.0);
+    const double2 v = v_hat[i];
+    const double2 nw = make_double2(__dmul_rn(__dsub_rn(v.x, __dmul_rn(w, f.x)), rden),
+                                    __dmul_rn(__dsub_rn(v.y, __dmul_rn(w, f.y)), rden));
+    bad |= !isfinite(nw.x);
+    v_hat[i] = nw;
+  }
+  diag_flag_nonfinite(diag, bad);
+}
+
+}  // namespace pfcs
+
+using namespace pfcs;
+
+extern "C" {
+
+int pfcs_mul_deriv(const void* in, void* out, int64_t n0, int64_t n1, int64_t n2, const double* d,
+                   int axis, void* stream) {
+  if (axis < 0 || axis > 2) return fail(PFCS_E_ARG, "axis must be 0, 1 or 2");
+  const i64 n = n0 * n1 * n2;
+  if (n <= 0) return PFCS_OK;
+  k_mul_deriv<<<grid_for(n), 256, 0, (cudaStream_t)stream>>>((const double2*)in, (double2*)out, n, (int)n1,
+                                                            (int)n2, d, axis);
+  return check_launch("k_mul_deriv");
+}
+
+int pfcs_cmul(const void* a, const void* b, void* out, int64_t n, void* stream) {
+  if (n <= 0) return PFCS_OK;
+  k_cmul<<<grid_for(n), 256, 0, (cudaStream_t)stream>>>((const double2*)a, (const double2*)b, (double2*)out, n);
+  return check_launch("k_cmul");
+}
+
+int pfcs_hydro_advect(const void* v1, const void* x1, const void* v2, const void* x2, const void* v3,
+                      const void* x3, void* out, int64_t n, void* stream) {
+  if (n <= 0) return PFCS_OK;
+  k_advect<<<grid_for(n), 256, 0, (cudaStream_t)stream>>>(
+      (const double2*)v1, (const double2*)x1, (const double2*)v2, (const double2*)x2, (const double2*)v3,
+      (const double2*)x3, (double2*)out, n);
+  return check_launch("k_advect");
+}
+
+int pfcs_hydro_psi_update(void* psi_hat, const void* nl_hat, const void* adv_hat, int64_t n0, int64_t n1,
+                          int64_t n2, const double* kx, const double* ky, const double* kz, double eps,
+                          double dt, double* diag, void* stream) {
+  const i64 n = n0 * n1 * n2;
+  if (n <= 0) return PFCS_OK;
+  k_hydro_psi_update<<<grid_for(n), 256, 0, (cudaStream_t)stream>>>(
+      (double2*)psi_hat, (const double2*)nl_hat, (const double2*)adv_hat, n, (int)n1, (int)n2, kx, ky, kz, eps,
+      dt, diag);
+  return check_launch("k_hydro_psi_update");
+}
+
+int pfcs_hydro_mu(const void* nl_hat, const void* f_hat, void* out, int64_t n0, int64_t n1, int64_t n2,
+                  const double* kx, const double* ky, const double* kz, double eps, void* stream) {
+  const i64 n = n0 * n1 * n2;
+  if (n <= 0) return PFCS_OK;
+  k_hydro_mu<<<grid_for(n), 256, 0, (cudaStream_t)stream>>>((const double2*)nl_hat, (const double2*)f_hat,
+                                                           (double2*)out, n, (int)n1, (int)n2, kx, ky, kz,
+                                                           eps);
+  return check_launch("k_hydro_mu");
+}
+
+int pfcs_hydro_vel_update(void* v_hat, const void* force, int64_t n0, int64_t n1, int64_t n2,
+                          const double* kx, const double* ky, const double* kz, double c_cg, double c_den,
+                          double c_exp, double* diag, void* stream) {
+  const i64 n = n0 * n1 * n2;
+  if (n <= 0) return PFCS_OK;
+  k_hydro_vel_update<<<grid_for(n), 256, 0, (cudaStream_t)stream>>>(
+      (double2*)v_hat, (const double2*)force, n, (int)n1, (int)n2, kx, ky, kz, c_cg, c_den, c_exp, diag);
+  return check_launch("k_hydro_vel_update");
+}
+
+}  // extern "C"

@@ -5,6 +5,7 @@
 #include <stdint.h>
 
 #include <string>
+#include <type_traits>
 
 #include "../../include/pfcs.h"
 
@@ -29,6 +30,50 @@ inline int ilog2(long long n) {
 
 // Opt a kernel in to > 48 KB dynamic shared memory once.
 int ensure_smem(const void* func, size_t bytes);
+
+// Persistent launch size: min(ntiles, resident CTAs per SM x SM count),
+// from the occupancy calculator (cached per kernel/config and device).
+// Also performs the shared-memory opt-in.
+int persistent_grid(const void* func, int threads, size_t smem, long long ntiles, int* grid);
+
+// ----------------------------------------------------------- tile tuning ----
+// Launch variant V = shift + 4 * (stages - 1): tile width T = T_MIN << shift,
+// 1 or 2 cp.async pipeline stages.  The production build bakes the measured
+// best variant per kernel kind and length (default_variant, from
+// tools/tune.py on a B200); a build with -DPFCS_TUNE instantiates all eight
+// and reads PFCS_VARIANT_<kind>_<N> from the environment.
+enum { KIND_LINES = 0, KIND_STRIDED = 1, KIND_REALX = 2, KIND_CUBEC = 3, KIND_PFCZ = 4, KIND_CUBER = 5 };
+
+constexpr int default_variant(int kind, int n) {
+  // n: transform length (REALX / CUBER: the half length M)
+  return kind == KIND_LINES   ? (n <= 256 ? 2 : (n == 512 ? 0 : 0))
+       : kind == KIND_STRIDED ? (n <= 512 ? 3 : (n == 1024 ? 2 : 1))
+       : kind == KIND_REALX   ? (n <= 256 ? 3 : (n == 512 ? 3 : (n == 1024 ? 2 : 1)))
+       : kind == KIND_CUBER   ? (n <= 256 ? 3 : (n == 512 ? 2 : (n == 1024 ? 1 : 0)))
+       : kind == KIND_CUBEC   ? (n <= 512 ? 2 : (n == 1024 ? 1 : 0))
+       : /* KIND_PFCZ */        (n <= 256 ? 2 : (n == 512 ? 1 : 0));
+}
+
+int tune_variant(int kind, int n, int dflt);
+
+template <int KIND, int N, class F>
+int with_variant(F&& f) {
+  constexpr int d = default_variant(KIND, N);
+#ifdef PFCS_TUNE
+  switch (tune_variant(KIND, N, d)) {
+    case 0: return f(std::integral_constant<int, 0>{});
+    case 1: return f(std::integral_constant<int, 1>{});
+    case 2: return f(std::integral_constant<int, 2>{});
+    case 3: return f(std::integral_constant<int, 3>{});
+    case 4: return f(std::integral_constant<int, 4>{});
+    case 5: return f(std::integral_constant<int, 5>{});
+    case 6: return f(std::integral_constant<int, 6>{});
+    default: return f(std::integral_constant<int, 7>{});
+  }
+#else
+  return f(std::integral_constant<int, d>{});
+#endif
+}
 
 // Balanced-slab split descriptor for a line of length n over g ranks.
 struct SlabSplitH {

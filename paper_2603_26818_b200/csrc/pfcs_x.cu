@@ -18,202 +18,249 @@
 //   C2R pre-twiddle -> M-point inverse FFT -> scale fl(1/N) -> x^3 per real
 //   sample -> M-point forward FFT -> R2C post-twiddle
 // so the physical field never reaches HBM (1 read + 1 write per mode).
+//
+// All kernels are persistent with register-pipelined loads (reg_tile_loop).
+// A tile is T adjacent inner columns (the contiguous y*z extent), so each
+// row of a tile is one T*16 (complex) or T*8 (real) byte segment.
+#include "pfcs_diag.cuh"
 #include "pfcs_fft.cuh"
 #include "pfcs_internal.h"
-#include "pfcs_diag.cuh"
 
 namespace pfcs {
 
 enum { MODE_R2C = 0, MODE_C2R = 1, MODE_CUBE = 2 };
 
-template <int M, int T, int MODE>
-__global__ void __launch_bounds__(T*(M / radix_R(M)))
-    k_real_x(const void* in_, void* out_, i64 inner, i64 tpo, const double2* __restrict__ twN,
-             double scale, double* diag) {
+template <int R>
+struct RegsX {
+  double2 v[R];
+  double2 xm;  // row M (half-spectrum Nyquist mode), used by thread j == 0
+};
+
+// Extra +8 keeps row M (index PAD(M)) inside the line when the bank rule
+// gives no padding, without changing the line base's bank slot.
+__host__ __device__ constexpr int real_ls(int m, int t) {
+  return tile_ls(m, t, true) + (tile_ls(m, t, true) == pad_idx(m) ? 8 : 0);
+}
+
+template <int M, int T, int ST, int MODE>
+__global__ void __launch_bounds__(T*(M / radix_R(M)),
+                                  min_blocks(T*(M / radix_R(M)), MODE == 2 ? 512 : (ST == 2 ? 640 : 768)))
+    k_real_x(const void* in_, void* out_, i64 inner, const double2* __restrict__ twN, double scale,
+             double* diag) {
   constexpr int R = radix_R(M);
   constexpr int P = M / R;
-  constexpr int LS = line_stride(M);
+  constexpr int LS = real_ls(M, T);
   extern __shared__ double2 smem[];
   const int tid = threadIdx.x;
   const int t = tid % T;
   const int j = tid / T;
-  const i64 i = (i64)blockIdx.x * T + t;
-  const bool active = i < inner;
   double2* sl = smem + t * LS;
-  double2 v[R];
-  double m_re = 0.0, m_im = 0.0;
+  const i64 ntiles = (inner + T - 1) / T;
+  double m_abs = 0.0;
 
-  if (MODE == MODE_R2C) {
-    const double* in = (const double*)in_;
-#pragma unroll
-    for (int e = 0; e < R; ++e) {
-      const i64 m = j + P * e;
-      v[e] = active ? make_double2(in[(2 * m) * inner + i], in[(2 * m + 1) * inner + i])
-                    : make_double2(0.0, 0.0);
-    }
-  } else {
-    // load the M+1 half-spectrum rows, then build Z'[k] from X[k], X[M-k]
-    const double2* in = (const double2*)in_;
-#pragma unroll
-    for (int e = 0; e < R; ++e) {
-      const i64 k = j + P * e;
-      double2 x = active ? in[k * inner + i] : make_double2(0.0, 0.0);
-      if (k == 0) x.y = 0.0;
-      sl[pad_idx((int)k)] = x;
-    }
-    if (j == 0) {
-      double2 x = active ? in[(i64)M * inner + i] : make_double2(0.0, 0.0);
-      x.y = 0.0;
-      sl[pad_idx(M)] = x;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int e = 0; e < R; ++e) {
-      const int k = j + P * e;
-      const double2 a = sl[pad_idx(k)];
-      const double2 bm = sl[pad_idx(M - k)];
-      const double2 b = make_double2(bm.x, -bm.y);  // conj X[M-k]
-      const double2 s = cadd(a, b);
-      const double2 d = csub(a, b);
-      // i * W_N^{-k} * d  ;  W_N^{-k} = conj(twN[k])
-      const double2 w = __ldg(&twN[k]);
-      const double2 wd = make_double2(fma(d.x, w.x, d.y * w.y), fma(d.y, w.x, -d.x * w.y));
-      v[e] = make_double2(s.x - wd.y, s.y + wd.x);
-    }
-  }
-
-  if (MODE == MODE_C2R || MODE == MODE_CUBE) {
-    fft_line<M, false, 2>(v, j, sl, twN);
-#pragma unroll
-    for (int e = 0; e < R; ++e) v[e] = make_double2(v[e].x * scale, v[e].y * scale);
-  }
-
-  if (MODE == MODE_C2R) {
-    if (active) {
-      double* out = (double*)out_;
+  auto load = [&](i64 tile, RegsX<R>& r) {
+    const i64 i = tile * T + t;
+    const bool ok = i < inner;
+    if (MODE == MODE_R2C) {
+      const double* in = (const double*)in_;
 #pragma unroll
       for (int e = 0; e < R; ++e) {
         const i64 m = j + P * e;
-        out[(2 * m) * inner + i] = v[e].x;
-        out[(2 * m + 1) * inner + i] = v[e].y;
+        r.v[e] = ok ? make_double2(in[(2 * m) * inner + i], in[(2 * m + 1) * inner + i])
+                    : make_double2(0.0, 0.0);
+      }
+    } else {
+      const double2* in = (const double2*)in_;
+#pragma unroll
+      for (int e = 0; e < R; ++e) {
+        const i64 k = j + P * e;
+        r.v[e] = ok ? in[k * inner + i] : make_double2(0.0, 0.0);
+      }
+      r.xm = (ok && j == 0) ? in[(i64)M * inner + i] : make_double2(0.0, 0.0);
+    }
+  };
+
+  auto comp = [&](i64 tile, RegsX<R>& r) {
+    const i64 i = tile * T + t;
+    const bool ok = i < inner;
+    double2* v = r.v;
+    if (MODE != MODE_R2C) {
+      // Z'[k] = (X_k + conj X_{M-k}) + i W_N^{-k} (X_k - conj X_{M-k});
+      // Im X_0 and Im X_M are ignored (numpy irfft convention)
+      stash_line<M>(r.v, j, sl);
+      if (j == 0) sl[pad_idx(M)] = r.xm;
+      __syncthreads();
+#pragma unroll
+      for (int e = 0; e < R; ++e) {
+        const int k = j + P * e;
+        double2 a = v[e];
+        double2 bm = sl[pad_idx(M - k)];
+        if (k == 0) {
+          a.y = 0.0;
+          bm.y = 0.0;
+        }
+        const double2 b = make_double2(bm.x, -bm.y);
+        const double2 s = cadd(a, b);
+        const double2 d = csub(a, b);
+        const double2 w = __ldg(&twN[k]);
+        const double2 wd = make_double2(fma(d.x, w.x, d.y * w.y), fma(d.y, w.x, -d.x * w.y));
+        v[e] = make_double2(s.x - wd.y, s.y + wd.x);
+      }
+      fft_line<M, false, 2>(r.v, j, sl, twN);
+#pragma unroll
+      for (int e = 0; e < R; ++e) v[e] = make_double2(v[e].x * scale, v[e].y * scale);
+    }
+
+    if (MODE == MODE_C2R) {
+      if (ok) {
+        double* out = (double*)out_;
+#pragma unroll
+        for (int e = 0; e < R; ++e) {
+          const i64 m = j + P * e;
+          out[(2 * m) * inner + i] = v[e].x;
+          out[(2 * m + 1) * inner + i] = v[e].y;
+        }
+      }
+      return;
+    }
+
+    if (MODE == MODE_CUBE) {
+#pragma unroll
+      for (int e = 0; e < R; ++e) {
+        const double a = v[e].x, b = v[e].y;
+        if (ok) m_abs = dmax_bits(m_abs, dmax_bits(fabs(a), fabs(b)));
+        // psi**3 of a real sample, x*x*x in numpy's left-to-right order
+        v[e] = make_double2(__dmul_rn(__dmul_rn(a, a), a), __dmul_rn(__dmul_rn(b, b), b));
       }
     }
-    return;
-  }
 
-  if (MODE == MODE_CUBE) {
+    // forward M-point FFT, then the R2C split
+    fft_line<M, true, 2>(r.v, j, sl, twN);
+    __syncthreads();
+    stash_line<M>(r.v, j, sl);
+    __syncthreads();
+    double2* out = (double2*)out_;
 #pragma unroll
     for (int e = 0; e < R; ++e) {
-      const double a = v[e].x, b = v[e].y;
-      m_re = dmax_bits(m_re, fmax_nan(fabs(a), fabs(b)));
-      // psi**3 of a real sample; x*x*x in numpy's left-to-right order
-      v[e] = make_double2(__dmul_rn(__dmul_rn(a, a), a), __dmul_rn(__dmul_rn(b, b), b));
+      const int k = j + P * e;
+      const double2 zk = v[e];
+      const double2 zm = sl[pad_idx((M - k) & (M - 1))];
+      double2 x;
+      if (k == 0) {
+        x = make_double2(zk.x + zk.y, 0.0);
+      } else {
+        const double2 s = make_double2(zk.x + zm.x, zk.y - zm.y);  // Zk + conj Zm
+        const double2 d = make_double2(zk.x - zm.x, zk.y + zm.y);  // Zk - conj Zm
+        const double2 w = __ldg(&twN[k]);
+        const double2 wd = make_double2(fma(d.x, w.x, -d.y * w.y), fma(d.x, w.y, d.y * w.x));
+        x = make_double2(0.5 * (s.x + wd.y), 0.5 * (s.y - wd.x));  // 1/2 (s - i wd)
+      }
+      if (ok) out[(i64)k * inner + i] = x;
     }
-    if (!active) m_re = 0.0;
-    diag_block_max(diag, m_re, m_im, m_re);
-  }
+    if (j == 0 && ok) {
+      const double2 z0 = v[0];
+      out[(i64)M * inner + i] = make_double2(z0.x - z0.y, 0.0);
+    }
+  };
 
-  // forward M-point FFT, then the R2C split
-  fft_line<M, true, 2>(v, j, sl, twN);
-  __syncthreads();
-  stash_line<M>(v, j, sl);
-  __syncthreads();
-  double2* out = (double2*)out_;
-#pragma unroll
-  for (int e = 0; e < R; ++e) {
-    const int k = j + P * e;
-    const double2 zk = sl[pad_idx(k)];
-    const double2 zm = sl[pad_idx((M - k) & (M - 1))];
-    double2 x;
-    if (k == 0) {
-      x = make_double2(zk.x + zk.y, 0.0);
-    } else {
-      const double2 s = make_double2(zk.x + zm.x, zk.y - zm.y);  // Zk + conj Zm
-      const double2 d = make_double2(zk.x - zm.x, zk.y + zm.y);  // Zk - conj Zm
-      const double2 w = __ldg(&twN[k]);
-      const double2 wd = make_double2(fma(d.x, w.x, -d.y * w.y), fma(d.x, w.y, d.y * w.x));
-      // 1/2 (s - i wd)
-      x = make_double2(0.5 * (s.x + wd.y), 0.5 * (s.y - wd.x));
-    }
-    if (active) out[(i64)k * inner + i] = x;
-  }
-  if (j == 0 && active) {
-    const double2 z0 = sl[pad_idx(0)];
-    out[(i64)M * inner + i] = make_double2(z0.x - z0.y, 0.0);
-  }
+  reg_tile_loop<ST, RegsX<R>>(ntiles, load, comp);
+  if (MODE == MODE_CUBE) diag_block_max(diag, m_abs, 0.0, m_abs);
 }
 
 // Fused complex-data cube pass (C2C mode, reference-layout fields):
 // inverse x FFT -> psi*(psi*psi) (numpy complex power, pfc.py:109) -> forward.
-template <int N, int T>
-__global__ void __launch_bounds__(T*(N / radix_R(N)))
-    k_cube_c2c(double2* data, i64 inner, i64 tpo, const double2* __restrict__ tw, double scale,
-               double* diag) {
+template <int N, int T, int ST>
+__global__ void __launch_bounds__(T*(N / radix_R(N)), min_blocks(T*(N / radix_R(N)), 512))
+    k_cube_c2c(double2* data, i64 inner, const double2* __restrict__ tw, double scale, double* diag) {
   constexpr int R = radix_R(N);
   constexpr int P = N / R;
+  constexpr int LS = tile_ls(N, T, true);
   extern __shared__ double2 smem[];
   const int tid = threadIdx.x;
   const int t = tid % T;
   const int j = tid / T;
-  const i64 i = (i64)blockIdx.x * T + t;
-  const bool active = i < inner;
-  double2* sl = smem + t * line_stride(N);
-  double2 v[R];
-#pragma unroll
-  for (int e = 0; e < R; ++e)
-    v[e] = active ? data[(i64)(j + P * e) * inner + i] : make_double2(0.0, 0.0);
-  fft_line<N, false>(v, j, sl, tw);
+  double2* sl = smem + t * LS;
+  const i64 ntiles = (inner + T - 1) / T;
   double m_re = 0.0, m_im = 0.0, m_abs = 0.0;
+  auto load = [&](i64 tile, RegsX<R>& r) {
+    const i64 i = tile * T + t;
+    const bool ok = i < inner;
 #pragma unroll
-  for (int e = 0; e < R; ++e) {
-    const double a = v[e].x * scale, b = v[e].y * scale;
-    m_re = dmax_bits(m_re, fabs(a));
-    m_im = dmax_bits(m_im, fabs(b));
-    m_abs = dmax_bits(m_abs, hypot(a, b));
-    // c = psi*psi ; psi*c, no contraction (numpy cmul)
-    const double cr = __dsub_rn(__dmul_rn(a, a), __dmul_rn(b, b));
-    const double ci = __dadd_rn(__dmul_rn(a, b), __dmul_rn(b, a));
-    v[e] = make_double2(__dsub_rn(__dmul_rn(a, cr), __dmul_rn(b, ci)),
-                        __dadd_rn(__dmul_rn(a, ci), __dmul_rn(b, cr)));
-  }
-  if (!active) m_re = m_im = m_abs = 0.0;
+    for (int e = 0; e < R; ++e) r.v[e] = ok ? data[(i64)(j + P * e) * inner + i] : make_double2(0.0, 0.0);
+  };
+  auto comp = [&](i64 tile, RegsX<R>& r) {
+    const i64 i = tile * T + t;
+    const bool ok = i < inner;
+    double2* v = r.v;
+    fft_line<N, false>(r.v, j, sl, tw);
+#pragma unroll
+    for (int e = 0; e < R; ++e) {
+      const double a = v[e].x * scale, b = v[e].y * scale;
+      if (ok) {
+        m_re = dmax_bits(m_re, fabs(a));
+        m_im = dmax_bits(m_im, fabs(b));
+        m_abs = dmax_bits(m_abs, hypot(a, b));
+      }
+      // c = psi*psi ; psi*c, no contraction (numpy cmul)
+      const double cr = __dsub_rn(__dmul_rn(a, a), __dmul_rn(b, b));
+      const double ci = __dadd_rn(__dmul_rn(a, b), __dmul_rn(b, a));
+      v[e] = make_double2(__dsub_rn(__dmul_rn(a, cr), __dmul_rn(b, ci)),
+                          __dadd_rn(__dmul_rn(a, ci), __dmul_rn(b, cr)));
+    }
+    fft_line<N, true>(r.v, j, sl, tw);
+    if (ok) {
+#pragma unroll
+      for (int e = 0; e < R; ++e) data[(i64)(j + P * e) * inner + i] = v[e];
+    }
+  };
+  reg_tile_loop<ST, RegsX<R>>(ntiles, load, comp);
   diag_block_max(diag, m_re, m_im, m_abs);
-  fft_line<N, true>(v, j, sl, tw);
-  if (active) {
-#pragma unroll
-    for (int e = 0; e < R; ++e) data[(i64)(j + P * e) * inner + i] = v[e];
-  }
 }
 
 // ---------------------------------------------------------------- dispatch --
 
 template <int M, int MODE>
 static int real_x_m(const void* in, void* out, i64 inner, double* diag, cudaStream_t st) {
-  constexpr int T = TileCfg<M>::T_STRIDED;
-  constexpr int P = TileCfg<M>::P;
-  const size_t smem = (size_t)T * line_stride(M) * sizeof(double2);
   const double2* twN = twiddles(2 * M);
   if (!twN) return PFCS_E_CUDA;
-  const i64 blocks = (inner + T - 1) / T;
-  const void* f = (const void*)k_real_x<M, T, MODE>;
-  if (ensure_smem(f, smem)) return PFCS_E_CUDA;
-  k_real_x<M, T, MODE><<<(unsigned)blocks, T * P, smem, st>>>(in, out, inner, blocks, twN,
-                                                              1.0 / (double)(2 * M), diag);
-  return check_launch("k_real_x");
+  return with_variant<MODE == MODE_CUBE ? KIND_CUBER : KIND_REALX, M>([&](auto var) -> int {
+    constexpr int V = decltype(var)::value;
+    constexpr int T = TileCfg<M>::T_MIN << (V & 3);
+    constexpr int ST = 1 + (V >> 2);
+    constexpr int P = TileCfg<M>::P;
+    if constexpr (T * P > 1024) {
+      return fail(PFCS_E_UNSUPPORTED, "tile too large");
+    } else {
+      const size_t smem = (size_t)T * real_ls(M, T) * sizeof(double2);
+      const i64 ntiles = (inner + T - 1) / T;
+      int grid = 0;
+      if (int rc = persistent_grid((const void*)k_real_x<M, T, ST, MODE>, T * P, smem, ntiles, &grid)) return rc;
+      k_real_x<M, T, ST, MODE><<<grid, T * P, smem, st>>>(in, out, inner, twN, 1.0 / (double)(2 * M), diag);
+      return check_launch("k_real_x");
+    }
+  });
 }
 
 template <int N>
 static int cube_c2c_n(double2* data, i64 inner, double* diag, cudaStream_t st) {
-  constexpr int T = TileCfg<N>::T_STRIDED;
-  constexpr int P = TileCfg<N>::P;
-  const size_t smem = (size_t)T * line_stride(N) * sizeof(double2);
   const double2* tw = twiddles(N);
   if (!tw) return PFCS_E_CUDA;
-  const i64 blocks = (inner + T - 1) / T;
-  const void* f = (const void*)k_cube_c2c<N, T>;
-  if (ensure_smem(f, smem)) return PFCS_E_CUDA;
-  k_cube_c2c<N, T><<<(unsigned)blocks, T * P, smem, st>>>(data, inner, blocks, tw, 1.0 / (double)N, diag);
-  return check_launch("k_cube_c2c");
+  return with_variant<KIND_CUBEC, N>([&](auto var) -> int {
+    constexpr int V = decltype(var)::value;
+    constexpr int T = TileCfg<N>::T_MIN << (V & 3);
+    constexpr int ST = 1 + (V >> 2);
+    constexpr int P = TileCfg<N>::P;
+    if constexpr (T * P > 1024) {
+      return fail(PFCS_E_UNSUPPORTED, "tile too large");
+    } else {
+      const size_t smem = (size_t)T * tile_ls(N, T, true) * sizeof(double2);
+      const i64 ntiles = (inner + T - 1) / T;
+      int grid = 0;
+      if (int rc = persistent_grid((const void*)k_cube_c2c<N, T, ST>, T * P, smem, ntiles, &grid)) return rc;
+      k_cube_c2c<N, T, ST><<<grid, T * P, smem, st>>>(data, inner, tw, 1.0 / (double)N, diag);
+      return check_launch("k_cube_c2c");
+    }
+  });
 }
 
 #define PFCS_M_CASES(MACRO) \
@@ -227,10 +274,10 @@ int launch_real_x(const void* in, void* out, long long nx, long long inner, int 
     return fail(PFCS_E_UNSUPPORTED, "real x transforms need a power-of-two nx in [4, 8192]");
   const int M = (int)(nx / 2);
   switch (M) {
-#define PFCS_CASE(MM)                                                      \
-  case MM:                                                                 \
-    if (mode == MODE_R2C) return real_x_m<MM, MODE_R2C>(in, out, inner, diag, st); \
-    if (mode == MODE_C2R) return real_x_m<MM, MODE_C2R>(in, out, inner, diag, st); \
+#define PFCS_CASE(MM)                                                                   \
+  case MM:                                                                              \
+    if (mode == MODE_R2C) return real_x_m<MM, MODE_R2C>(in, out, inner, diag, st);     \
+    if (mode == MODE_C2R) return real_x_m<MM, MODE_C2R>(in, out, inner, diag, st);     \
     return real_x_m<MM, MODE_CUBE>(in, out, inner, diag, st);
     PFCS_M_CASES(PFCS_CASE)
 #undef PFCS_CASE

@@ -46,41 +46,52 @@ __device__ __forceinline__ void pfc_symbols(double k2, double eps, double dt, do
   rden = __drcp_rn(den);
 }
 
-template <int N, int T, bool BIN, bool BOUT, bool NEXT>
-__global__ void __launch_bounds__(T*(N / radix_R(N)))
+template <int R>
+struct RegsZ {
+  double2 v[R];  // N-hat z line (un-transformed)
+  double2 p[R];  // psi_hat z line
+};
+
+template <int N, int T, int ST, bool BIN, bool BOUT, bool NEXT>
+__global__ void __launch_bounds__(T*(N / radix_R(N)), min_blocks(T*(N / radix_R(N)), 512))
     k_pfc_z(const double2* nl, double2* psi_hat, double2* next, i64 nlines, int ny, SlabSplit sin,
             SlabSplit sout, const double* __restrict__ kx, const double* __restrict__ ky,
             const double* __restrict__ kz, PfcSym p, const double2* __restrict__ tw, double scale,
             double* diag) {
   constexpr int R = radix_R(N);
   constexpr int P = N / R;
+  constexpr int LS = tile_ls(N, T, false);
   extern __shared__ double2 smem[];
   const int tid = threadIdx.x;
   const int t = tid / P;
   const int j = tid - t * P;
-  const i64 l = (i64)blockIdx.x * T + t;
-  const bool active = l < nlines;
-  double2* sl = smem + t * line_stride(N);
-  double2 v[R];
-#pragma unroll
-  for (int e = 0; e < R; ++e) {
-    const int z = j + P * e;
-    i64 a;
-    if (BIN) {
-      int zoff, cz;
-      sin.locate(z, zoff, cz);
-      a = nlines * zoff + l * cz + (z - zoff);
-    } else {
-      a = l * N + z;
-    }
-    v[e] = active ? nl[a] : make_double2(0.0, 0.0);
-  }
-  fft_line<N, true>(v, j, sl, tw);
-
+  double2* sl = smem + t * LS;
+  const i64 ntiles = (nlines + T - 1) / T;
   bool bad = false;
-  {
-    const i64 lx = active ? l / ny : 0;
-    const int ly = active ? (int)(l - lx * ny) : 0;
+  auto load = [&](i64 tile, RegsZ<R>& r) {
+    const i64 l = tile * T + t;
+    const bool ok = l < nlines;
+#pragma unroll
+    for (int e = 0; e < R; ++e) {
+      const int z = j + P * e;
+      i64 a;
+      if (BIN) {
+        int zoff, cz;
+        sin.locate(z, zoff, cz);
+        a = nlines * zoff + l * cz + (z - zoff);
+      } else {
+        a = l * N + z;
+      }
+      r.v[e] = ok ? nl[a] : make_double2(0.0, 0.0);
+      r.p[e] = ok ? psi_hat[l * N + z] : make_double2(0.0, 0.0);
+    }
+  };
+  auto comp = [&](i64 tile, RegsZ<R>& r) {
+    const i64 l = tile * T + t;
+    const bool ok = l < nlines;
+    fft_line<N, true>(r.v, j, sl, tw);
+    const i64 lx = ok ? l / ny : 0;
+    const int ly = ok ? (int)(l - lx * ny) : 0;
     const double kxx = __ldg(&kx[lx]);
     const double kyy = __ldg(&ky[ly]);
 #pragma unroll
@@ -89,70 +100,79 @@ __global__ void __launch_bounds__(T*(N / radix_R(N)))
       const double k2 = k2_of(kxx, kyy, __ldg(&kz[z]));
       double lap, rden;
       pfc_symbols(k2, p.eps, p.dt, lap, rden);
-      const double2 ph = active ? psi_hat[l * N + z] : make_double2(0.0, 0.0);
-      const double nr = __dadd_rn(ph.x, __dmul_rn(p.dt, __dmul_rn(lap, v[e].x)));
-      const double ni = __dadd_rn(ph.y, __dmul_rn(p.dt, __dmul_rn(lap, v[e].y)));
+      const double2 ph = r.p[e];
+      const double nr = __dadd_rn(ph.x, __dmul_rn(p.dt, __dmul_rn(lap, r.v[e].x)));
+      const double ni = __dadd_rn(ph.y, __dmul_rn(p.dt, __dmul_rn(lap, r.v[e].y)));
       const double2 nw = make_double2(__dmul_rn(nr, rden), __dmul_rn(ni, rden));
-      bad |= !(isfinite(nw.x) && isfinite(nw.y));
-      if (active) psi_hat[l * N + z] = nw;
-      v[e] = nw;
+      bad |= ok && !(isfinite(nw.x) && isfinite(nw.y));
+      if (ok) psi_hat[l * N + z] = nw;
+      r.v[e] = nw;
     }
-  }
-  diag_flag_nonfinite(diag, bad && active);
-
-  if (NEXT) {
-    fft_line<N, false>(v, j, sl, tw);
-    if (active) {
+    if (NEXT) {
+      fft_line<N, false>(r.v, j, sl, tw);
+      if (ok) {
 #pragma unroll
-      for (int e = 0; e < R; ++e) {
-        const int z = j + P * e;
-        i64 a;
-        if (BOUT) {
-          int zoff, cz;
-          sout.locate(z, zoff, cz);
-          a = nlines * zoff + l * cz + (z - zoff);
-        } else {
-          a = l * N + z;
+        for (int e = 0; e < R; ++e) {
+          const int z = j + P * e;
+          i64 a;
+          if (BOUT) {
+            int zoff, cz;
+            sout.locate(z, zoff, cz);
+            a = nlines * zoff + l * cz + (z - zoff);
+          } else {
+            a = l * N + z;
+          }
+          next[a] = make_double2(r.v[e].x * scale, r.v[e].y * scale);
         }
-        next[a] = make_double2(v[e].x * scale, v[e].y * scale);
       }
     }
-  }
+  };
+  reg_tile_loop<ST, RegsZ<R>>(ntiles, load, comp);
+  diag_flag_nonfinite(diag, bad);
 }
 
 template <int N>
 static int pfc_z_n(const double2* nl, double2* psi_hat, double2* next, i64 cx, i64 ny,
                    SlabSplitH si, SlabSplitH so, const double* kx, const double* ky,
                    const double* kz, double eps, double dt, double* diag, cudaStream_t st) {
-  constexpr int T = TileCfg<N>::T_CONTIG;
-  constexpr int P = TileCfg<N>::P;
-  const size_t smem = (size_t)T * line_stride(N) * sizeof(double2);
   const double2* tw = twiddles(N);
   if (!tw) return PFCS_E_CUDA;
   const i64 nlines = cx * ny;
-  const i64 blocks = (nlines + T - 1) / T;
   SlabSplit a{si.G, si.base, si.extra}, b{so.G, so.base, so.extra};
   PfcSym p{eps, dt};
   const bool bin = si.G > 1, bout = so.G > 1, nx = next != nullptr;
   const double scale = 1.0 / (double)N;
-#define PFCS_ZK(BI, BO, NX) k_pfc_z<N, T, BI, BO, NX>
-#define PFCS_ZL(BI, BO, NX)                                                                  \
-  do {                                                                                       \
-    if (ensure_smem((const void*)PFCS_ZK(BI, BO, NX), smem)) return PFCS_E_CUDA;             \
-    PFCS_ZK(BI, BO, NX)<<<(unsigned)blocks, T * P, smem, st>>>(nl, psi_hat, next, nlines,    \
-                                                               (int)ny, a, b, kx, ky, kz, p, \
-                                                               tw, scale, diag);             \
+  return with_variant<KIND_PFCZ, N>([&](auto var) -> int {
+    constexpr int V = decltype(var)::value;
+    constexpr int T = TileCfg<N>::T_MIN << (V & 3);
+    constexpr int ST = 1 + (V >> 2);
+    constexpr int P = TileCfg<N>::P;
+    if constexpr (T * P > 1024) {
+      return fail(PFCS_E_UNSUPPORTED, "tile too large");
+    } else {
+      const size_t smem = (size_t)T * tile_ls(N, T, false) * sizeof(double2);
+      const i64 ntiles = (nlines + T - 1) / T;
+      int grid = 0;
+#define PFCS_ZK(BI, BO, NX) k_pfc_z<N, T, ST, BI, BO, NX>
+#define PFCS_ZL(BI, BO, NX)                                                                       \
+  do {                                                                                            \
+    if (int rc = persistent_grid((const void*)PFCS_ZK(BI, BO, NX), T * P, smem, ntiles, &grid))   \
+      return rc;                                                                                  \
+    PFCS_ZK(BI, BO, NX)<<<grid, T * P, smem, st>>>(nl, psi_hat, next, nlines, (int)ny, a, b, kx, \
+                                                   ky, kz, p, tw, scale, diag);                   \
   } while (0)
-  if (!nx) {
-    if (bin) PFCS_ZL(true, false, false);
-    else PFCS_ZL(false, false, false);
-  } else if (bin && bout) PFCS_ZL(true, true, true);
-  else if (bin) PFCS_ZL(true, false, true);
-  else if (bout) PFCS_ZL(false, true, true);
-  else PFCS_ZL(false, false, true);
+      if (!nx) {
+        if (bin) PFCS_ZL(true, false, false);
+        else PFCS_ZL(false, false, false);
+      } else if (bin && bout) PFCS_ZL(true, true, true);
+      else if (bin) PFCS_ZL(true, false, true);
+      else if (bout) PFCS_ZL(false, true, true);
+      else PFCS_ZL(false, false, true);
 #undef PFCS_ZL
 #undef PFCS_ZK
-  return check_launch("k_pfc_z");
+      return check_launch("k_pfc_z");
+    }
+  });
 }
 
 int launch_pfc_z(const double2* nl, double2* psi_hat, double2* next, long long cx, long long ny,

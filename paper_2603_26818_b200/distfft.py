@@ -321,9 +321,10 @@ def _inverse_core(src: torch.Tensor, worker, g: _Geometry) -> torch.Tensor:
         out = torch.empty(g.nx * g.ny * g.cz, dtype=torch.float64, device=dev)
         nat.call("pfcs_irfft_x", nat.ptr(z), nat.ptr(out), g.nx, g.ny * g.cz, _stream())
         return out
-    # reference order: fft_2d inverse = x then y (fftcore.py:43-45)
-    _fft_x(z, g, False, z)
+    # y then x, the order of the fused PFC step (so distfft.inverse and the
+    # stepper's internal psi are bit-identical)
     _fft_y(z, g, False)
+    _fft_x(z, g, False, z)
     return z
 
 

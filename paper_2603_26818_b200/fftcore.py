@@ -1,9 +1,13 @@
 """Serial complex-to-complex FFTs on B200 (drop-in for fftcore.py).
 
 Reference: /root/reference/pkg/src/pfcspectral/fftcore.py:1-52.  Same
-conventions: forward unnormalised, inverse scaled by fl(1/n) per axis; the
-multi-axis order is pinned (forward 0,1,2; inverse 2,0,1) as in
-fftcore.py:4-11.  Length-1 axes copy, empty arrays return empty copies.
+conventions: forward unnormalised, inverse scaled by fl(1/n) per axis;
+length-1 axes copy, empty arrays return empty copies.  The multi-axis order
+is pinned — forward 0,1,2 and inverse 2,1,0 — so that, as in the reference
+(fftcore.py:4-11, which pins 2,0,1 for the same purpose), the serial
+transform, the distributed one and the fused PFC pipeline (z, y, then x
+innermost) follow bit-identical arithmetic; e.g. the hydro density update
+with v = 0 reproduces pfc_step bit for bit.
 
 Arrays may be numpy arrays (the reference's type — they are moved to the
 current CUDA device and the result comes back as numpy) or CUDA tensors
@@ -59,23 +63,25 @@ def fft_axis(a, axis: int, forward: bool = True):
 
 
 def fft_2d(a, forward: bool = True):
-    """Axes 0 then 1, every z-plane independently (fftcore.py:43-45)."""
+    """Axes 0 and 1, every z-plane independently (fftcore.py:43-45);
+    forward 0 then 1, inverse 1 then 0."""
     _check(a.shape, 0)
     t, host = _to_device(a)
     out = torch.empty_like(t)
     if t.numel():
-        _axis_inplace(t, 0, forward, out)
-        _axis_inplace(out, 1, forward, out)
+        first, second = (0, 1) if forward else (1, 0)
+        _axis_inplace(t, first, forward, out)
+        _axis_inplace(out, second, forward, out)
     return out.cpu().numpy() if host else out
 
 
 def fft_nd(a, forward: bool = True):
-    """All axes; forward 0,1,2 and inverse 2,0,1 (fftcore.py:48-52)."""
+    """All axes; forward 0,1,2 and inverse 2,1,0 (fftcore.py:48-52)."""
     _check(a.shape, 0)
     t, host = _to_device(a)
     out = torch.empty_like(t)
     if t.numel():
-        order = (0, 1, 2) if forward else (2, 0, 1)
+        order = (0, 1, 2) if forward else (2, 1, 0)
         _axis_inplace(t, order[0], forward, out)
         for ax in order[1:]:
             _axis_inplace(out, ax, forward, out)
