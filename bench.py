@@ -173,12 +173,20 @@ class Ctx:
         if self.world > 1:
             import torch.distributed as dist
 
-            torch.cuda.set_device(self.local)
-            dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
+            # PFCS_BENCH_BACKEND=gloo (test only): host-staged exchanges, ranks may
+            # share a GPU — used to exercise the multi-rank path on a 1-GPU box
+            backend = os.environ.get("PFCS_BENCH_BACKEND", "nccl")
+            dev = self.local % torch.cuda.device_count()
+            torch.cuda.set_device(dev)
+            if backend == "nccl":
+                dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+            else:
+                dist.init_process_group(backend)
             self.dist = dist
         else:
             torch.cuda.set_device(0)
         self.device = torch.device("cuda", torch.cuda.current_device())
+        self.coll_device = self.device if (self.dist is None or self.dist.get_backend() == "nccl") else "cpu"
 
     def worker(self):
         from paper_2603_26818_b200.transport import ProcessWorker, Worker, WorkerGroup
@@ -194,14 +202,14 @@ class Ctx:
     def max_over_ranks(self, v: float) -> float:
         if self.dist is None:
             return v
-        t = self.torch.tensor([v], dtype=self.torch.float64, device=self.device)
+        t = self.torch.tensor([v], dtype=self.torch.float64, device=self.coll_device)
         self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
         return float(t.item())
 
     def sum_over_ranks(self, v: float) -> float:
         if self.dist is None:
             return v
-        t = self.torch.tensor([v], dtype=self.torch.float64, device=self.device)
+        t = self.torch.tensor([v], dtype=self.torch.float64, device=self.coll_device)
         self.dist.all_reduce(t)
         return float(t.item())
 
@@ -414,7 +422,7 @@ def main():
                                   f"slab decomposition)",
                       "grid": [args.fft_n] * 3, "decomposition": f"slab x{ctx.world}",
                       "l2": "inputs (1 GiB per field at 512^3) exceed the 126 MB L2; no flush needed"}}
-    with ClockSampler(ctx.local) as clk:
+    with ClockSampler(ctx.device.index) as clk:
         table = run_fft(ctx, args, out)
         pfc_res = None if args.no_pfc else run_pfc(ctx, args)
     out["clocks"] = clk.summary()

@@ -44,14 +44,17 @@ int persistent_grid(const void* func, int threads, size_t smem, long long ntiles
 // and reads PFCS_VARIANT_<kind>_<N> from the environment.
 enum { KIND_LINES = 0, KIND_STRIDED = 1, KIND_REALX = 2, KIND_CUBEC = 3, KIND_PFCZ = 4, KIND_CUBER = 5 };
 
+// Measured on B200 (tools/tune.py, profiles/r1_tune.json): contiguous z
+// lines like one line per CTA with the next tile's loads in flight; strided
+// passes want >= 128-byte row segments (T*16 B) even at one CTA per SM.
 constexpr int default_variant(int kind, int n) {
   // n: transform length (REALX / CUBER: the half length M)
-  return kind == KIND_LINES   ? (n <= 256 ? 2 : (n == 512 ? 0 : 0))
-       : kind == KIND_STRIDED ? (n <= 512 ? 3 : (n == 1024 ? 2 : 1))
-       : kind == KIND_REALX   ? (n <= 256 ? 3 : (n == 512 ? 3 : (n == 1024 ? 2 : 1)))
-       : kind == KIND_CUBER   ? (n <= 256 ? 3 : (n == 512 ? 2 : (n == 1024 ? 1 : 0)))
-       : kind == KIND_CUBEC   ? (n <= 512 ? 2 : (n == 1024 ? 1 : 0))
-       : /* KIND_PFCZ */        (n <= 256 ? 2 : (n == 512 ? 1 : 0));
+  return kind == KIND_LINES   ? (n <= 256 ? 5 : 4)
+       : kind == KIND_STRIDED ? (n <= 512 ? 3 : (n == 1024 ? 6 : (n == 2048 ? 5 : 4)))
+       : kind == KIND_REALX   ? (n <= 512 ? 7 : (n == 1024 ? 6 : (n == 2048 ? 5 : 4)))
+       : kind == KIND_CUBER   ? (n <= 512 ? 3 : (n == 1024 ? 2 : (n == 2048 ? 1 : 0)))
+       : kind == KIND_CUBEC   ? (n <= 512 ? 3 : (n == 1024 ? 2 : (n == 2048 ? 1 : 0)))
+       : /* KIND_PFCZ */        (n <= 256 ? 1 : 0);
 }
 
 int tune_variant(int kind, int n, int dflt);

@@ -69,6 +69,7 @@ def main():
                 row[s] = round(nbytes / (ms * 1e-3) / 1e9, 1)
             except Exception as e:  # tile too large etc.
                 row[s] = None
+                print("  variant", s, "failed:", str(e)[:120], flush=True)
         del os.environ[f"PFCS_VARIANT_{kind}_{n}"]
         results[f"{kind}_{n}"] = row
         print(kind, n, row, flush=True)
