@@ -253,9 +253,24 @@ def kernel_table(trace, steps):
     return out
 
 
-def roofline_of(table, peak, peak_kind, traffic=None):
+def measured_traffic(workload: str) -> dict:
+    """DRAM read+write bytes per launch from the committed ncu --set full
+    capture of the same workload (profiles/*_traffic.json), if any."""
+    best = {}
+    for p in sorted((ROOT / "profiles").glob("*_traffic.json")):
+        try:
+            d = json.loads(p.read_text())
+        except Exception:
+            continue
+        if d.get("workload") == workload:
+            best = d.get("traffic_bytes_per_launch", {})
+    return best
+
+
+def roofline_of(table, peak, peak_kind, traffic_map=None):
     top = max(table.items(), key=lambda kv: kv[1]["avg_ms"] * kv[1]["launches_per_step"])
     lab, d = top
+    traffic = (traffic_map or {}).get(lab)
     return {"kernel": lab, "bound": "hbm", "achieved": d["gbs"], "peak": peak, "peak_kind": peak_kind,
             "unit": "GB/s", "frac": round(d["gbs"] / peak, 4) if d["gbs"] else None,
             "traffic": traffic, "alg_bytes_per_launch": d["alg_gb_per_launch"] * 1e9}
@@ -426,7 +441,8 @@ def main():
         table = run_fft(ctx, args, out)
         pfc_res = None if args.no_pfc else run_pfc(ctx, args)
     out["clocks"] = clk.summary()
-    out["roofline"] = roofline_of(table, hbm, peak_kind)
+    workload = f"fft{args.fft_n}" if ctx.world == 1 else None
+    out["roofline"] = roofline_of(table, hbm, peak_kind, measured_traffic(workload))
     out["roofline"]["whole_step_frac"] = round(out["value"] / (hbm * ctx.world), 4)
     if pfc_res is not None:
         pr = roofline_of(pfc_res["kernels"], hbm, peak_kind)
