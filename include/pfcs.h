@@ -57,6 +57,16 @@ int pfcs_fft_axis_c2c(const void* in, void* out, int64_t n0, int64_t n1, int64_t
 int pfcs_fft_zlines(const void* in, void* out, int64_t nlines, int64_t nz, int g_in, int g_out,
                     int forward, void* stream);
 
+/* ---- pencil-pipeline line transforms (new: pencil decomposition, north-star
+ * item (2)).  Lines along the middle axis of an (outer, n, inner) array
+ * (inner = 1: contiguous lines).  g_in / g_out > 1 select the "blocked"
+ * layout of the line axis: n split into g balanced slabs, slab g stored
+ * densely as (outer, cn_g, inner) at element offset outer*inner*noff_g —
+ * what a pencil all-to-all over that axis delivers / needs.  Generalises
+ * pfcs_fft_zlines (inner = 1). */
+int pfcs_fft_lines(const void* in, void* out, int64_t outer, int64_t n, int64_t inner, int g_in, int g_out,
+                   int forward, void* stream);
+
 /* ---- real transforms along axis 0 (x) of a C-order array (new: R2C/C2R,
  * north-star item (1)).  rfft: real (nx, inner) -> complex (nx/2+1, inner),
  * unnormalised.  irfft: complex (nx/2+1, inner) -> real (nx, inner), scaled

@@ -37,6 +37,7 @@ _SIGS = {
     "pfcs_device_count": [ctypes.POINTER(_c_int)],
     "pfcs_fft_axis_c2c": [_c_p, _c_p, _c_i64, _c_i64, _c_i64, _c_int, _c_int, _c_p],
     "pfcs_fft_zlines": [_c_p, _c_p, _c_i64, _c_i64, _c_int, _c_int, _c_int, _c_p],
+    "pfcs_fft_lines": [_c_p, _c_p, _c_i64, _c_i64, _c_i64, _c_int, _c_int, _c_int, _c_p],
     "pfcs_rfft_x": [_c_p, _c_p, _c_i64, _c_i64, _c_p],
     "pfcs_irfft_x": [_c_p, _c_p, _c_i64, _c_i64, _c_p],
     "pfcs_pfc_cube_x": [_c_p, _c_i64, _c_i64, _c_int, _c_p, _c_p],

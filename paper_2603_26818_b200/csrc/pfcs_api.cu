@@ -231,6 +231,21 @@ int pfcs_fft_zlines(const void* in, void* out, int64_t nlines, int64_t nz, int g
                           S(stream));
 }
 
+int pfcs_fft_lines(const void* in, void* out, int64_t outer, int64_t n, int64_t inner, int g_in, int g_out,
+                   int forward, void* stream) {
+  if (outer < 0 || n < 1 || inner < 0 || g_in < 1 || g_out < 1) return fail(PFCS_E_ARG, "bad line geometry");
+  if (outer == 0 || inner == 0) return PFCS_OK;
+  if (n == 1) {
+    if (in != out)
+      return check_cuda(cudaMemcpyAsync(out, in, (size_t)(outer * inner) * 16, cudaMemcpyDeviceToDevice,
+                                        S(stream)),
+                        "copy");
+    return PFCS_OK;
+  }
+  return launch_strided_blocked((const double2*)in, (double2*)out, outer, (int)n, inner, g_in, g_out,
+                                forward != 0, S(stream));
+}
+
 int pfcs_rfft_x(const double* in, void* out, int64_t nx, int64_t inner, void* stream) {
   if (nx < 1 || inner < 0) return fail(PFCS_E_ARG, "bad shape");
   return launch_real_x(in, out, nx, inner, 0, nullptr, S(stream));

@@ -81,10 +81,23 @@ __global__ void __launch_bounds__(T*(N / radix_R(N)), min_blocks(T*(N / radix_R(
   reg_tile_loop<ST, Regs1<R>>(ntiles, load, comp);
 }
 
-template <int N, int T, int ST, bool FWD>
+// Address of element (o, n, i) of an (outer, N, inner) array whose line axis
+// n is either plain or "blocked": split into G balanced slabs, slab g stored
+// densely as (outer, cn_g, inner) at element offset outer*inner*noff_g —
+// the layout a pencil exchange over the line axis produces or consumes.
+template <bool BLOCKED>
+__device__ __forceinline__ i64 line_addr(i64 o, int n, i64 i, int N, i64 outer, i64 inner,
+                                         const SlabSplit& s) {
+  if (!BLOCKED) return (o * N + n) * inner + i;
+  int noff, cn;
+  s.locate(n, noff, cn);
+  return outer * inner * noff + (o * cn + (n - noff)) * inner + i;
+}
+
+template <int N, int T, int ST, bool FWD, bool BIN, bool BOUT>
 __global__ void __launch_bounds__(T*(N / radix_R(N)), min_blocks(T*(N / radix_R(N)), ST == 2 ? 640 : 1024))
-    k_strided(const double2* in, double2* out, i64 outer, i64 inner, i64 tpo,
-              const double2* __restrict__ tw, double scale) {
+    k_strided(const double2* in, double2* out, i64 outer, i64 inner, i64 tpo, SlabSplit sin,
+              SlabSplit sout, const double2* __restrict__ tw, double scale) {
   constexpr int R = radix_R(N);
   constexpr int P = N / R;
   constexpr int LS = tile_ls(N, T, true);
@@ -98,22 +111,20 @@ __global__ void __launch_bounds__(T*(N / radix_R(N)), min_blocks(T*(N / radix_R(
     const i64 o = tile / tpo;
     const i64 i = (tile - o * tpo) * T + t;
     const bool ok = i < inner;
-    const i64 base = o * (i64)N * inner + i;
 #pragma unroll
     for (int e = 0; e < R; ++e)
-      r.v[e] = ok ? in[base + (i64)(j + P * e) * inner] : make_double2(0.0, 0.0);
+      r.v[e] = ok ? in[line_addr<BIN>(o, j + P * e, i, N, outer, inner, sin)] : make_double2(0.0, 0.0);
   };
   auto comp = [&](i64 tile, Regs1<R>& r) {
     const i64 o = tile / tpo;
     const i64 i = (tile - o * tpo) * T + t;
     fft_line<N, FWD>(r.v, j, sl, tw);
     if (i < inner) {
-      const i64 base = o * (i64)N * inner + i;
 #pragma unroll
       for (int e = 0; e < R; ++e) {
         double2 x = r.v[e];
         if (!FWD) x = make_double2(x.x * scale, x.y * scale);
-        out[base + (i64)(j + P * e) * inner] = x;
+        out[line_addr<BOUT>(o, j + P * e, i, N, outer, inner, sout)] = x;
       }
     }
   };
@@ -190,31 +201,50 @@ __global__ void k_dft(const double2* in, double2* out, int N, i64 outer, i64 inn
   }
 }
 
-// Copy between plain and blocked z-line layouts (the np.concatenate /
-// slicing of distfft._exchange for sizes the fused kernels do not cover).
-__global__ void k_reblock(const double2* in, double2* out, i64 nlines, int n, SlabSplit a, SlabSplit b) {
-  const i64 total = nlines * n;
+// Copy between plain and blocked layouts of the line axis of an
+// (outer, n, inner) array (the np.concatenate / slicing of
+// distfft._exchange for sizes the fused kernels do not cover).
+__global__ void k_reblock(const double2* in, double2* out, i64 outer, int n, i64 inner, SlabSplit a,
+                          SlabSplit b) {
+  const i64 total = outer * n * inner;
   for (i64 idx = (i64)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
        idx += (i64)gridDim.x * blockDim.x) {
-    const i64 l = idx / n;
-    const int z = (int)(idx - l * n);
+    const i64 o = idx / ((i64)n * inner);
+    const i64 rem = idx - o * n * inner;
+    const int z = (int)(rem / inner);
+    const i64 i = rem - (i64)z * inner;
     int zo, cz;
     a.locate(z, zo, cz);
-    const i64 ia = nlines * zo + l * cz + (z - zo);
+    const i64 ia = outer * inner * zo + (o * cz + (z - zo)) * inner + i;
     b.locate(z, zo, cz);
-    const i64 ib = nlines * zo + l * cz + (z - zo);
+    const i64 ib = outer * inner * zo + (o * cz + (z - zo)) * inner + i;
     out[ib] = in[ia];
   }
 }
 
-static int reblock(const double2* in, double2* out, i64 nlines, int n, SlabSplitH a, SlabSplitH b,
-                   cudaStream_t st) {
-  i64 blocks = (nlines * n + 255) / 256;
+static int reblock(const double2* in, double2* out, i64 outer, int n, i64 inner, SlabSplitH a,
+                   SlabSplitH b, cudaStream_t st) {
+  i64 blocks = (outer * n * inner + 255) / 256;
   if (blocks > 148 * 16) blocks = 148 * 16;
   if (blocks < 1) return PFCS_OK;
-  k_reblock<<<(unsigned)blocks, 256, 0, st>>>(in, out, nlines, n, SlabSplit{a.G, a.base, a.extra},
+  k_reblock<<<(unsigned)blocks, 256, 0, st>>>(in, out, outer, n, inner, SlabSplit{a.G, a.base, a.extra},
                                               SlabSplit{b.G, b.base, b.extra});
   return check_launch("k_reblock");
+}
+
+// Any length with blocked layouts: re-block through a plain temporary
+// around the direct DFT (non-power-of-two sizes are a parity path).
+static int blocked_dft(const double2* in, double2* out, i64 outer, int n, i64 inner, SlabSplitH si,
+                       SlabSplitH so, bool forward, cudaStream_t st) {
+  if (si.G == 1 && so.G == 1) return launch_dft(in, out, outer, n, inner, forward, st);
+  double2* tmp = nullptr;
+  const size_t bytes = (size_t)outer * n * inner * sizeof(double2);
+  if (int rc = check_cuda(cudaMallocAsync((void**)&tmp, bytes, st), "cudaMallocAsync")) return rc;
+  int rc = reblock(in, tmp, outer, n, inner, si, slab_split(n, 1), st);
+  if (!rc) rc = launch_dft(tmp, tmp, outer, n, inner, forward, st);
+  if (!rc) rc = reblock(tmp, out, outer, n, inner, slab_split(n, 1), so, st);
+  cudaFreeAsync(tmp, st);
+  return rc;
 }
 
 // ---------------------------------------------------------------- dispatch --
@@ -254,9 +284,12 @@ static int lines_n(const double2* in, double2* out, i64 nlines, SlabSplitH si, S
 }
 
 template <int N, bool FWD>
-static int strided_n(const double2* in, double2* out, i64 outer, i64 inner, cudaStream_t st) {
+static int strided_n(const double2* in, double2* out, i64 outer, i64 inner, SlabSplitH si, SlabSplitH so,
+                     cudaStream_t st) {
   const double2* tw = twiddles(N);
   if (!tw) return PFCS_E_CUDA;
+  SlabSplit a{si.G, si.base, si.extra}, b{so.G, so.base, so.extra};
+  const bool bin = si.G > 1, bout = so.G > 1;
   return with_variant<KIND_STRIDED, N>([&](auto var) -> int {
     constexpr int V = decltype(var)::value;
     constexpr int T = TileCfg<N>::T_MIN << (V & 3);
@@ -265,13 +298,25 @@ static int strided_n(const double2* in, double2* out, i64 outer, i64 inner, cuda
     if constexpr (T * P > 1024) {
       return fail(PFCS_E_UNSUPPORTED, "tile too large");
     } else {
-    const size_t smem = (size_t)T * tile_ls(N, T, true) * sizeof(double2);
-    const i64 tpo = (inner + T - 1) / T;
-    const void* f = (const void*)k_strided<N, T, ST, FWD>;
-    int grid = 0;
-    if (int rc = persistent_grid(f, T * P, smem, outer * tpo, &grid)) return rc;
-    k_strided<N, T, ST, FWD><<<grid, T * P, smem, st>>>(in, out, outer, inner, tpo, tw, 1.0 / (double)N);
-    return check_launch("k_strided");
+      const size_t smem = (size_t)T * tile_ls(N, T, true) * sizeof(double2);
+      const i64 tpo = (inner + T - 1) / T;
+      const void* f;
+      if (bin && bout) f = (const void*)k_strided<N, T, ST, FWD, true, true>;
+      else if (bin) f = (const void*)k_strided<N, T, ST, FWD, true, false>;
+      else if (bout) f = (const void*)k_strided<N, T, ST, FWD, false, true>;
+      else f = (const void*)k_strided<N, T, ST, FWD, false, false>;
+      int grid = 0;
+      if (int rc = persistent_grid(f, T * P, smem, outer * tpo, &grid)) return rc;
+      const double sc = 1.0 / (double)N;
+      if (bin && bout)
+        k_strided<N, T, ST, FWD, true, true><<<grid, T * P, smem, st>>>(in, out, outer, inner, tpo, a, b, tw, sc);
+      else if (bin)
+        k_strided<N, T, ST, FWD, true, false><<<grid, T * P, smem, st>>>(in, out, outer, inner, tpo, a, b, tw, sc);
+      else if (bout)
+        k_strided<N, T, ST, FWD, false, true><<<grid, T * P, smem, st>>>(in, out, outer, inner, tpo, a, b, tw, sc);
+      else
+        k_strided<N, T, ST, FWD, false, false><<<grid, T * P, smem, st>>>(in, out, outer, inner, tpo, a, b, tw, sc);
+      return check_launch("k_strided");
     }
   });
 }
@@ -285,16 +330,7 @@ int launch_lines_c2c(const double2* in, double2* out, long long nlines, int n, i
   if (nlines <= 0) return PFCS_OK;
   const SlabSplitH si = slab_split(n, g_in), so = slab_split(n, g_out);
   if (!is_pow2(n) || n > 4096) {
-    // generic sizes: re-block through a plain temporary around the direct DFT
-    if (g_in == 1 && g_out == 1) return launch_dft(in, out, nlines, n, 1, forward, st);
-    double2* tmp = nullptr;
-    const size_t bytes = (size_t)nlines * n * sizeof(double2);
-    if (int rc = check_cuda(cudaMallocAsync((void**)&tmp, bytes, st), "cudaMallocAsync")) return rc;
-    int rc = reblock(in, tmp, nlines, n, si, slab_split(n, 1), st);
-    if (!rc) rc = launch_dft(tmp, tmp, nlines, n, 1, forward, st);
-    if (!rc) rc = reblock(tmp, out, nlines, n, slab_split(n, 1), so, st);
-    cudaFreeAsync(tmp, st);
-    return rc;
+    return blocked_dft(in, out, nlines, n, 1, si, so, forward, st);
   }
   switch (n) {
 #define PFCS_CASE(NN) \
@@ -310,13 +346,22 @@ int launch_lines_c2c(const double2* in, double2* out, long long nlines, int n, i
 
 int launch_strided_c2c(const double2* in, double2* out, long long outer, int n, long long inner,
                        bool forward, cudaStream_t st) {
+  return launch_strided_blocked(in, out, outer, n, inner, 1, 1, forward, st);
+}
+
+int launch_strided_blocked(const double2* in, double2* out, long long outer, int n, long long inner, int g_in,
+                           int g_out, bool forward, cudaStream_t st) {
   if (outer <= 0 || inner <= 0) return PFCS_OK;
-  if (inner == 1) return launch_lines_c2c(in, out, outer, n, 1, 1, forward, st);
-  if (!is_pow2(n) || n > 4096) return launch_dft(in, out, outer, n, inner, forward, st);
+  const SlabSplitH si = slab_split(n, g_in), so = slab_split(n, g_out);
+  if (inner == 1) return launch_lines_c2c(in, out, outer, n, g_in, g_out, forward, st);
+  if (!is_pow2(n) || n > 4096) {
+    return blocked_dft(in, out, outer, n, inner, si, so, forward, st);
+  }
   switch (n) {
-#define PFCS_CASE(NN) \
-  case NN:            \
-    return forward ? strided_n<NN, true>(in, out, outer, inner, st) : strided_n<NN, false>(in, out, outer, inner, st);
+#define PFCS_CASE(NN)                                                                  \
+  case NN:                                                                             \
+    return forward ? strided_n<NN, true>(in, out, outer, inner, si, so, st)            \
+                   : strided_n<NN, false>(in, out, outer, inner, si, so, st);
     PFCS_POW2_CASES(PFCS_CASE)
 #undef PFCS_CASE
     default:

@@ -95,6 +95,8 @@ int launch_lines_c2c(const double2* in, double2* out, long long nlines, int n, i
                      int g_out, bool forward, cudaStream_t st);
 int launch_strided_c2c(const double2* in, double2* out, long long outer, int n, long long inner,
                        bool forward, cudaStream_t st);
+int launch_strided_blocked(const double2* in, double2* out, long long outer, int n, long long inner, int g_in,
+                           int g_out, bool forward, cudaStream_t st);
 int launch_dft(const double2* in, double2* out, long long outer, int n, long long inner,
                bool forward, cudaStream_t st);
 

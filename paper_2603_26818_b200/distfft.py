@@ -209,6 +209,10 @@ def _expand_half(half: np.ndarray, nx: int) -> np.ndarray:
 def gather(field: DistField, worker) -> np.ndarray:
     """Reassemble the full array on every rank (distfft.py:103-107).  A
     half-spectrum field is returned as the full (Hermitian) spectrum."""
+    if not isinstance(field.layout, Layout):
+        from .pencil import pencil_gather
+
+        return pencil_gather(field, worker)
     received = worker.all_to_all([field.local] * worker.size)
     lay = _layout(field.grid, field.layout, worker.size, field.half)
     full = np.concatenate(received, axis=lay.axis)
@@ -386,14 +390,24 @@ def dist_fft_2d_inverse(field: DistField, worker) -> DistField:
 
 
 def forward(field: DistField, worker) -> DistField:
-    """Dimension-dispatching forward transform (distfft.py:198-202)."""
+    """Dimension-dispatching forward transform (distfft.py:198-202); pencil
+    layouts (pencil.PencilLayout) take the pencil pipeline."""
+    if not isinstance(field.layout, Layout):
+        from .pencil import pencil_forward
+
+        return pencil_forward(field, worker)
     if field.grid.is_2d:
         return dist_fft_2d_forward(field, worker)
     return dist_fft_forward(field, worker)
 
 
 def inverse(field: DistField, worker) -> DistField:
-    """Dimension-dispatching inverse transform (distfft.py:205-209)."""
+    """Dimension-dispatching inverse transform (distfft.py:205-209); pencil
+    layouts take the pencil pipeline."""
+    if not isinstance(field.layout, Layout):
+        from .pencil import pencil_inverse
+
+        return pencil_inverse(field, worker)
     if field.grid.is_2d:
         return dist_fft_2d_inverse(field, worker)
     return dist_fft_inverse(field, worker)

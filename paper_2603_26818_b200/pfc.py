@@ -228,13 +228,36 @@ def slab_kvectors(grid: GridSpec, sym: SymbolTable, g: _Geometry, device):
                  for v in (kx_np, ky_np, kz_np))
 
 
-def _engine(state: PfcState) -> _StepEngine:
+def _is_pencil(field: DistField) -> bool:
+    return not isinstance(field.layout, Layout)
+
+
+def _engine(state: PfcState):
     eng = state._engine
     if eng is None or eng.real != state.psi_hat.half or eng.worker is not state.worker \
             or eng.device != state.psi_hat.dev.device:
-        eng = _StepEngine(state)
+        if _is_pencil(state.psi_hat):
+            from .pencil import PencilStepEngine
+
+            eng = PencilStepEngine(state)
+        else:
+            eng = _StepEngine(state)
         state._engine = eng
     return eng
+
+
+def _spectral_geometry(state: PfcState):
+    """(cx, cy, nz, owns_zero_mode, (kx, ky, kz)) of this rank's spectral
+    block in the kernels' view, for slabs and pencils alike."""
+    w = state.worker
+    dev = state.psi_hat.dev.device
+    if _is_pencil(state.psi_hat):
+        from .pencil import PencilGeometry, pencil_kvectors
+
+        g = PencilGeometry(state.grid, state.psi_hat.layout.grid, w.rank, state.psi_hat.half)
+        return g.cx, g.cy2, g.nz, (g.xoff == 0 and g.yoff2 == 0), pencil_kvectors(state.grid, g, dev)
+    g = _Geometry(state.grid, w.size, w.rank, state.psi_hat.half)
+    return g.cx, g.ny, g.nz, g.xoff == 0, slab_kvectors(state.grid, state.symbols, g, dev)
 
 
 def _finish(state: PfcState, params: PfcParams, d: np.ndarray, first_index: int) -> None:
@@ -301,16 +324,15 @@ def _real_part(t: torch.Tensor) -> tuple[torch.Tensor, int]:
 def free_energy(state: PfcState, params: PfcParams) -> float:
     """sum dV [psi (eps+L) psi / 2 + psi^4 / 4], rank-ordered (pfc.py:144-162)."""
     w = state.worker
-    g = _Geometry(state.grid, w.size, w.rank, state.psi_hat.half)
     dev = state.psi_hat.dev.device
     st = nat.stream_ptr()
     psi = distfft.inverse(state.psi_hat, w).dev
-    kx, ky, kz = slab_kvectors(state.grid, state.symbols, g, dev)
+    cx, cy, nz, _, (kx, ky, kz) = _spectral_geometry(state)
     op_hat = torch.empty_like(state.psi_hat.dev)
-    nat.call("pfcs_apply_op", nat.ptr(state.psi_hat.dev), nat.ptr(op_hat), g.cx, g.ny, g.nz,
+    nat.call("pfcs_apply_op", nat.ptr(state.psi_hat.dev), nat.ptr(op_hat), cx, cy, nz,
              nat.ptr(kx), nat.ptr(ky), nat.ptr(kz), float(state.symbols.eps), st)
-    op_field = DistField(state.grid, Layout.X_SLAB, Space.SPECTRAL, op_hat, half=state.psi_hat.half,
-                         device=dev)
+    op_field = DistField(state.grid, state.psi_hat.layout, Space.SPECTRAL, op_hat,
+                         half=state.psi_hat.half, device=dev)
     op_psi = distfft.inverse(op_field, w).dev
     a, sa = _real_part(psi)
     b, sb = _real_part(op_psi)
@@ -327,9 +349,9 @@ def mean_and_max(state: PfcState) -> tuple[float, float]:
     """(mean psi from the zero mode, max |psi|) — collective (pfc.py:165-182)."""
     w = state.worker
     f = state.psi_hat
-    lay = distfft._layout(state.grid, f.layout, w.size, f.half)
+    owns_zero = _spectral_geometry(state)[3]
     local_zero = 0.0
-    if lay.start(w.rank) == 0 and f.dev.numel():
+    if owns_zero and f.dev.numel():
         local_zero = float(f.dev.reshape(-1)[0].real.item())
     zero_mode = _reduce_sum(w, local_zero)
     psi = distfft.inverse(f, w).dev

@@ -85,6 +85,9 @@ class WorkerGroup:
             if self._failure is None:
                 self._failure = WorkerFailure(rank, cause)
             self._cv.notify_all()
+            subs = list(self.__dict__.get("_subgroups", {}).values())
+        for sub in subs:  # cancel waits in row/column sub-groups too
+            sub._fail(rank, cause)
 
     def _raise_if_cancelled(self) -> None:
         if self._failure is not None:
@@ -226,6 +229,29 @@ class Worker:
             return
         self.group._exchange(self.rank, send, send_counts, recv, recv_counts)
 
+    def subgroup(self, ranks: Sequence[int]) -> "Worker":
+        """Handle on the sub-group ``ranks`` (all members must call it with
+        the same tuple).  Used for the row/column exchanges of a pencil
+        decomposition."""
+        ranks = tuple(int(r) for r in ranks)
+        if self.rank not in ranks:
+            raise TransportError(f"rank {self.rank} is not in sub-group {ranks}")
+        g = self.group
+        with g._cv:
+            sub = g.__dict__.setdefault("_subgroups", {}).get(ranks)
+            if sub is None:
+                sub = WorkerGroup(len(ranks), timeout=g.timeout)
+                g._subgroups[ranks] = sub
+        return Worker(sub, ranks.index(self.rank), self.device)
+
+    def pencil_groups(self, pr: int, pc: int) -> tuple:
+        """(row, col) sub-workers of a pr x pc process grid, rank = r*pc + c:
+        the row group shares c (size pr, ordered by r), the column group
+        shares r (size pc, ordered by c)."""
+        r, c = divmod(self.rank, pc)
+        return (self.subgroup([rr * pc + c for rr in range(pr)]),
+                self.subgroup([r * pc + cc for cc in range(pc)]))
+
     def send_tensor(self, dst: int, tag: int, t) -> None:
         """Device point-to-point send (handed over by reference in a thread
         group; the receiver copies).  The sender must not mutate ``t``
@@ -258,13 +284,16 @@ class ProcessWorker:
     host memory.
     """
 
-    def __init__(self, group=None, device=None):
+    def __init__(self, group=None, device=None, ranks=None):
         import torch.distributed as dist
 
         self._dist = dist
         self.pg = group
-        self.rank = dist.get_rank(group)
-        self._size = dist.get_world_size(group)
+        # global ranks of the group members (sub-groups); point-to-point
+        # calls take global ranks
+        self._global = list(ranks) if ranks is not None else list(range(dist.get_world_size()))
+        self.rank = self._global.index(dist.get_rank())
+        self._size = len(self._global)
         self.device = device
         self.meter = None
         self.backend = dist.get_backend(group)
@@ -287,11 +316,11 @@ class ProcessWorker:
     def send(self, dst: int, tag: int, payload: Any) -> None:
         if dst == self.rank:
             raise TransportError(f"send: rank {self.rank} cannot send to itself")
-        self._dist.send_object_list([tag, payload], dst=dst, group=self.pg)
+        self._dist.send_object_list([tag, payload], dst=self._global[dst], group=self.pg)
 
     def receive(self, src: int, tag: int) -> Any:
         box = [None, None]
-        self._dist.recv_object_list(box, src=src, group=self.pg)
+        self._dist.recv_object_list(box, src=self._global[src], group=self.pg)
         if box[0] != tag:
             raise TransportError(f"receive: rank {self.rank} expected tag {tag} from {src}, "
                                  f"got {box[0]}")
@@ -322,18 +351,39 @@ class ProcessWorker:
                                      group=self.pg)
         r.copy_(r_h)
 
+    def pencil_groups(self, pr: int, pc: int) -> tuple:
+        """(row, col) sub-workers of a pr x pc process grid (rank = r*pc + c).
+        Collective: every rank creates every row and column group in the
+        same order (torch.distributed.new_group semantics)."""
+        key = (pr, pc)
+        cache = self.__dict__.setdefault("_pencil", {})
+        if key not in cache:
+            if pr * pc != self._size:
+                raise TransportError(f"process grid {pr}x{pc} does not match {self._size} ranks")
+            rows, cols = {}, {}
+            for c in range(pc):
+                ranks = [r * pc + c for r in range(pr)]
+                rows[c] = (ranks, self._dist.new_group(ranks))
+            for r in range(pr):
+                ranks = [r * pc + c for c in range(pc)]
+                cols[r] = (ranks, self._dist.new_group(ranks))
+            r, c = divmod(self.rank, pc)
+            cache[key] = (ProcessWorker(rows[c][1], self.device, rows[c][0]),
+                          ProcessWorker(cols[r][1], self.device, cols[r][0]))
+        return cache[key]
+
     def send_tensor(self, dst: int, tag: int, t) -> None:
         if self.backend == "nccl":
-            self._dist.send(t.contiguous(), dst=dst, group=self.pg)
+            self._dist.send(t.contiguous(), dst=self._global[dst], group=self.pg)
         else:
-            self._dist.send(t.contiguous().cpu(), dst=dst, group=self.pg)
+            self._dist.send(t.contiguous().cpu(), dst=self._global[dst], group=self.pg)
 
     def recv_tensor(self, src: int, tag: int, out):
         if self.backend == "nccl":
-            self._dist.recv(out, src=src, group=self.pg)
+            self._dist.recv(out, src=self._global[src], group=self.pg)
         else:
             tmp = out.cpu() if out.is_cuda else out
-            self._dist.recv(tmp, src=src, group=self.pg)
+            self._dist.recv(tmp, src=self._global[src], group=self.pg)
             if tmp is not out:
                 out.copy_(tmp)
         return out
