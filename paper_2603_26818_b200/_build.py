@@ -84,5 +84,25 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     return LIB
 
 
+def build_variant(name: str, defines: list[str]) -> Path:
+    """Experimental build with extra -D flags into libpfcs_<name>.so (for A/B
+    timing on the GPU via PFCS_LIB_PATH); not used by the product."""
+    nvcc = _nvcc()
+    bdir = ROOT / "build" / name
+    bdir.mkdir(parents=True, exist_ok=True)
+    flags = [f for f in NVCC_FLAGS if f not in ("-v", "-Xptxas")] + [f"-D{d}" for d in defines]
+    procs, objs = [], []
+    for src in _sources():
+        obj = bdir / (src.stem + ".o")
+        procs.append(subprocess.Popen([nvcc, *ARCH, *flags, "-I", str(INCLUDE), "-c", str(src), "-o", str(obj)]))
+        objs.append(str(obj))
+    for p in procs:
+        if p.wait() != 0:
+            raise RuntimeError(f"variant build {name} failed")
+    out = PKG / f"libpfcs_{name}.so"
+    subprocess.check_call([nvcc, *ARCH, "-shared", "-o", str(out), *objs])
+    return out
+
+
 if __name__ == "__main__":
     print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
