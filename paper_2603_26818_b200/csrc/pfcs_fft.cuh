@@ -129,7 +129,7 @@ __device__ __forceinline__ void dft_r(double2 (&y)[r]) {
 // j + P*e of this pass's input; on exit of the last pass v[e] holds output
 // element j + P*e.  `tw` is the size-N table exp(-2 pi i m / N), m < N,
 // read with stride TWS (so a size-2N table serves an N-point transform).
-template <int N, int Ns, bool FWD, int TWS>
+template <int N, int Ns, bool FWD, int TWS, int TWL = PFCS_TW_LOADS>
 __device__ __forceinline__ void fft_pass(double2 (&v)[radix_R(N)], int j, double2* sl,
                                          const double2* __restrict__ tw) {
   constexpr int R = radix_R(N);
@@ -152,10 +152,10 @@ __device__ __forceinline__ void fft_pass(double2 (&v)[radix_R(N)], int j, double
       const int t1 = TWS * k * (N / (Ns * r));
       double2 w[r];
       w[1] = __ldg(&tw[t1]);
-      if constexpr (r >= 4) w[2] = (PFCS_TW_LOADS >= 3) ? __ldg(&tw[2 * t1]) : cmul(w[1], w[1]);
+      if constexpr (r >= 4) w[2] = (TWL >= 3) ? __ldg(&tw[2 * t1]) : cmul(w[1], w[1]);
       if constexpr (r == 4) w[3] = cmul(w[1], w[2]);
       if constexpr (r == 8) {
-        w[4] = (PFCS_TW_LOADS >= 3) ? __ldg(&tw[4 * t1]) : cmul(w[2], w[2]);
+        w[4] = (TWL >= 3) ? __ldg(&tw[4 * t1]) : cmul(w[2], w[2]);
         w[3] = cmul(w[1], w[2]);
         w[5] = cmul(w[1], w[4]);
         w[6] = cmul(w[2], w[4]);
@@ -181,16 +181,16 @@ __device__ __forceinline__ void fft_pass(double2 (&v)[radix_R(N)], int j, double
     __syncthreads();
 #pragma unroll
     for (int e = 0; e < R; ++e) v[e] = sl[pad_idx(j + P * e)];
-    fft_pass<N, Ns * r, FWD, TWS>(v, j, sl, tw);
+    fft_pass<N, Ns * r, FWD, TWS, TWL>(v, j, sl, tw);
   }
 }
 
 // Full N-point transform of the register set (see fft_pass).  All threads of
 // the CTA must call it (it contains __syncthreads when N > 8).
-template <int N, bool FWD, int TWS = 1>
+template <int N, bool FWD, int TWS = 1, int TWL = PFCS_TW_LOADS>
 __device__ __forceinline__ void fft_line(double2 (&v)[radix_R(N)], int j, double2* sl,
                                          const double2* __restrict__ tw) {
-  fft_pass<N, 1, FWD, TWS>(v, j, sl, tw);
+  fft_pass<N, 1, FWD, TWS, TWL>(v, j, sl, tw);
 }
 
 // Stash register set (element j + P*e in v[e]) into the padded smem line.

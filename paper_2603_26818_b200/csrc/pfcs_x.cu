@@ -30,6 +30,32 @@ namespace pfcs {
 
 enum { MODE_R2C = 0, MODE_C2R = 1, MODE_CUBE = 2 };
 
+// exp(-2 pi i e / 16): for R = 8 the post/pre-twiddle W_N^k of element
+// k = j + P e (N = 2M = 16 P) is W_N^j * W_16^e, one table load per thread.
+__device__ __forceinline__ double2 w16(int e) {
+  constexpr double c1 = 0.92387953251128675613, s1 = 0.38268343236508977173;
+  constexpr double h = 0.70710678118654752440;
+  switch (e & 7) {
+    case 0: return make_double2(1.0, 0.0);
+    case 1: return make_double2(c1, -s1);
+    case 2: return make_double2(h, -h);
+    case 3: return make_double2(s1, -c1);
+    case 4: return make_double2(0.0, -1.0);
+    case 5: return make_double2(-s1, -c1);
+    case 6: return make_double2(-h, -h);
+    default: return make_double2(-c1, -s1);
+  }
+}
+
+template <int R>
+__device__ __forceinline__ double2 twiddle_k(const double2* __restrict__ twN, double2 wj, int j, int e, int P) {
+  if constexpr (R == 8) {
+    return cmul(wj, w16(e));
+  } else {
+    return __ldg(&twN[j + P * e]);
+  }
+}
+
 template <int R>
 struct RegsX {
   double2 v[R];
@@ -89,6 +115,7 @@ __global__ void __launch_bounds__(T*(M / radix_R(M)),
       // Im X_0 and Im X_M are ignored (numpy irfft convention)
       stash_line<M>(r.v, j, sl);
       if (j == 0) sl[pad_idx(M)] = r.xm;
+      const double2 wj = __ldg(&twN[j]);
       __syncthreads();
 #pragma unroll
       for (int e = 0; e < R; ++e) {
@@ -102,7 +129,7 @@ __global__ void __launch_bounds__(T*(M / radix_R(M)),
         const double2 b = make_double2(bm.x, -bm.y);
         const double2 s = cadd(a, b);
         const double2 d = csub(a, b);
-        const double2 w = __ldg(&twN[k]);
+        const double2 w = twiddle_k<R>(twN, wj, j, e, P);
         const double2 wd = make_double2(fma(d.x, w.x, d.y * w.y), fma(d.y, w.x, -d.x * w.y));
         v[e] = make_double2(s.x - wd.y, s.y + wd.x);
       }
@@ -136,6 +163,7 @@ __global__ void __launch_bounds__(T*(M / radix_R(M)),
 
     // forward M-point FFT, then the R2C split
     fft_line<M, true, 2>(r.v, j, sl, twN);
+    const double2 wj = __ldg(&twN[j]);
     __syncthreads();
     stash_line<M>(r.v, j, sl);
     __syncthreads();
@@ -151,7 +179,7 @@ __global__ void __launch_bounds__(T*(M / radix_R(M)),
       } else {
         const double2 s = make_double2(zk.x + zm.x, zk.y - zm.y);  // Zk + conj Zm
         const double2 d = make_double2(zk.x - zm.x, zk.y + zm.y);  // Zk - conj Zm
-        const double2 w = __ldg(&twN[k]);
+        const double2 w = twiddle_k<R>(twN, wj, j, e, P);
         const double2 wd = make_double2(fma(d.x, w.x, -d.y * w.y), fma(d.x, w.y, d.y * w.x));
         x = make_double2(0.5 * (s.x + wd.y), 0.5 * (s.y - wd.x));  // 1/2 (s - i wd)
       }

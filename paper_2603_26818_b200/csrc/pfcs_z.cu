@@ -89,7 +89,7 @@ __global__ void __launch_bounds__(T*(N / radix_R(N)), min_blocks(T*(N / radix_R(
   auto comp = [&](i64 tile, RegsZ<R>& r) {
     const i64 l = tile * T + t;
     const bool ok = l < nlines;
-    fft_line<N, true>(r.v, j, sl, tw);
+    fft_line<N, true, 1, 1>(r.v, j, sl, tw);
     const i64 lx = ok ? l / ny : 0;
     const int ly = ok ? (int)(l - lx * ny) : 0;
     const double kxx = __ldg(&kx[lx]);
@@ -109,7 +109,7 @@ __global__ void __launch_bounds__(T*(N / radix_R(N)), min_blocks(T*(N / radix_R(
       r.v[e] = nw;
     }
     if (NEXT) {
-      fft_line<N, false>(r.v, j, sl, tw);
+      fft_line<N, false, 1, 1>(r.v, j, sl, tw);
       if (ok) {
 #pragma unroll
         for (int e = 0; e < R; ++e) {
