@@ -337,6 +337,40 @@ def run_fft(ctx, args, out):
     return table
 
 
+def run_pfc2d(ctx, args):
+    """configs[0]: 2D PFC 256^2, 100 semi-implicit steps (launch-bound; the
+    single-rank path replays CUDA graphs), reference init and domain."""
+    import torch
+
+    from paper_2603_26818_b200 import distfft, pfc
+    from paper_2603_26818_b200.grid import GridSpec, make_symbols
+
+    n = (256, 256, 1)
+    w = ctx.worker()
+    grid = GridSpec(n, pfc.default_domain_length(n))
+    psi0 = pfc.initial_field("constant_plus_noise", grid, psi_bar=-0.3, seed=0, noise_amplitude=0.01)
+    f0 = distfft.scatter(psi0, w, grid, distfft.Layout.Y_SLAB, real=True)
+    lay = distfft._layout(grid, distfft.Layout.X_SLAB, ctx.world, True)
+    st = pfc.PfcState(psi_hat=distfft.forward(f0, w), grid=grid,
+                      symbols=make_symbols(grid, -0.3, layout=lay, rank=ctx.rank), worker=w)
+    params = pfc.PfcParams()
+    pfc.pfc_run(st, params, 100)  # warm-up run (captures the graph)
+    torch.cuda.synchronize()
+    ctx.barrier()
+    t0 = time.perf_counter()
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    a.record()
+    pfc.pfc_run(st, params, 100)
+    b.record()
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t0
+    ms = ctx.max_over_ranks(a.elapsed_time(b) / 100)
+    return {"metric": "PFC time-steps/sec", "value": round(1000.0 / ms, 1), "unit": "steps/s",
+            "ms_per_step": round(ms, 5), "wall_s_per_100_steps": round(wall, 5),
+            "config": "2D PFC 256x256 fp64 R2C, 100 steps (configs[0]), launch-bound"}
+
+
 def run_pfc(ctx, args):
     import torch
 
@@ -440,6 +474,7 @@ def main():
     with ClockSampler(ctx.device.index) as clk:
         table = run_fft(ctx, args, out)
         pfc_res = None if args.no_pfc else run_pfc(ctx, args)
+        pfc2d = None if args.no_pfc else run_pfc2d(ctx, args)
     out["clocks"] = clk.summary()
     workload = f"fft{args.fft_n}" if ctx.world == 1 else None
     out["roofline"] = roofline_of(table, hbm, peak_kind, measured_traffic(workload))
@@ -450,6 +485,8 @@ def main():
         t_roof = pfc_res["alg_hbm_bytes_per_step"] / (hbm * 1e9)
         pfc_res["roofline_step_frac"] = round(t_roof / (pfc_res["ms_per_step"] * 1e-3), 4)
         out["pfc"] = pfc_res
+    if pfc2d is not None:
+        out["pfc2d"] = pfc2d
     out["gpu_launches"] = int(out.pop("launches_total"))
     if ctx.rank == 0 and ctx.world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_fft_baseline(args.fft_n, args.cpu_seconds)

@@ -262,3 +262,39 @@ def test_r2c_matches_c2c_and_lean_oracle(pkg):
     got = pkg.spawn_group(2, body)[0]
     assert got.dtype == np.float64
     assert rel_l2(got, want) <= 1e-12
+
+
+def test_pfc_run_graph_replay_matches_stepping(pkg):
+    """pfc_run (CUDA-graph replay of 16-step blocks on one rank) is bit-identical
+    to calling pfc_step, and reports divergence at the first bad step."""
+    from paper_2603_26818_b200 import distfft, pfc
+
+    n = (64, 64, 1)
+    grid = pkg.GridSpec(n, pfc.default_domain_length(n))
+    psi0 = pfc.initial_field("constant_plus_noise", grid, seed=3, noise_amplitude=0.02)
+    params = pfc.PfcParams()
+
+    def body(w):
+        a = make_state(pkg, w, grid, psi0, real=True)
+        b = make_state(pkg, w, grid, psi0, real=True)
+        pfc.pfc_run(a, params, 50)
+        for _ in range(50):
+            pfc.pfc_step(b, params)
+        pfc.pfc_run(a, params, 37)
+        for _ in range(37):
+            pfc.pfc_step(b, params)
+        assert a.step_index == b.step_index == 87
+        assert a.sim_time == b.sim_time
+        return a.psi_hat.local, b.psi_hat.local
+
+    x, y = pkg.spawn_group(1, body)[0]
+    np.testing.assert_array_equal(x, y)
+
+    def diverge(w):
+        st = make_state(pkg, w, grid, np.full(grid.shape, 1e120), real=True)
+        pfc.pfc_run(st, params, 40)
+
+    with pytest.raises(Exception) as info:
+        pkg.spawn_group(1, diverge)
+    assert isinstance(info.value.cause, pfc.DivergenceError)
+    assert info.value.cause.step_index == 0
