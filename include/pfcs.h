@@ -145,6 +145,23 @@ int pfcs_hydro_vel_update(void* v_hat, const void* force, int64_t n0, int64_t n1
                           const double* kx, const double* ky, const double* kz, double c_cg, double c_den,
                           double c_exp, double* diag, void* stream);
 
+/* ---- composition field of the multiphysics mode (new; no reference
+ * counterpart — restated in oracle/ref_numpy.py): Cahn-Hilliard c advected
+ * by v,  mu_c = alpha (c^3 - c) - kappa lap c,  dc/dt = M lap mu_c - v.grad c.
+ * pfcs_ch_nonlin: out = alpha * (c*(c*c) - c)
+ * pfcs_ch_update: c_hat <- (c_hat + dt (M lap f_hat - adv_hat)) / (1 + dt M kappa lap^2)
+ * pfcs_ch_mu:     out = f_hat - kappa lap c_hat
+ * pfcs_add3:      out = (a + b) + c      (advection assembled from per-rank products)
+ * pfcs_axpy:      out = a + w * b        (velocity force with the composition term) */
+int pfcs_ch_nonlin(const void* c, void* out, int64_t n, double alpha, void* stream);
+int pfcs_ch_update(void* c_hat, const void* f_hat, const void* adv_hat, int64_t n0, int64_t n1, int64_t n2,
+                   const double* kx, const double* ky, const double* kz, double mobility, double kappa,
+                   double dt, double* diag, void* stream);
+int pfcs_ch_mu(const void* f_hat, const void* c_hat, void* out, int64_t n0, int64_t n1, int64_t n2,
+               const double* kx, const double* ky, const double* kz, double kappa, void* stream);
+int pfcs_add3(const void* a, const void* b, const void* c, void* out, int64_t n, void* stream);
+int pfcs_axpy(const void* a, const void* b, void* out, int64_t n, double w, void* stream);
+
 /* ---- deterministic reductions (pfc._reduce_sum / free_energy,
  * pfc.py:131-162).  out[0] = sum_i f(a_i, b_i) in a fixed order,
  * independent of the launch: f = 0.5*a*b + 0.25*a^4 (free-energy density,

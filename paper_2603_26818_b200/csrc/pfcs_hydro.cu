@@ -139,6 +139,69 @@ __global__ void k_hydro_vel_update(double2* v_hat, const double2* force, i64 n, 
   diag_flag_nonfinite(diag, bad);
 }
 
+// ------------------------------------------------- composition field (new) --
+// Cahn-Hilliard composition c advected by v (multiphysics mode, no reference
+// counterpart; oracle/ref_numpy.py restates it):
+//   mu_c = alpha (c^3 - c) - kappa lap c,   dc/dt = M lap mu_c - v . grad c
+//   c_hat <- (c_hat + dt (M lap F[alpha (c^3 - c)] - F[v . grad c])) / (1 + dt M kappa lap^2)
+
+// out = alpha * (c*(c*c) - c), complex, numpy order
+__global__ void k_ch_nonlin(const double2* c, double2* out, i64 n, double alpha) {
+  PFCS_FOR_ALL(n) {
+    const double2 a = c[i];
+    const double2 c3 = cmul_np(a, cmul_np(a, a));
+    out[i] = make_double2(__dmul_rn(alpha, __dsub_rn(c3.x, a.x)), __dmul_rn(alpha, __dsub_rn(c3.y, a.y)));
+  }
+}
+
+__global__ void k_ch_update(double2* c_hat, const double2* f_hat, const double2* adv_hat, i64 n, int n1, int n2,
+                            const double* __restrict__ kx, const double* __restrict__ ky,
+                            const double* __restrict__ kz, double mob, double kappa, double dt, double* diag) {
+  bool bad = false;
+  PFCS_FOR_ALL(n) {
+    const double lap = -k2_at(kx, ky, kz, i, n1, n2);
+    const double ml = __dmul_rn(mob, lap);
+    const double rden = __drcp_rn(__dadd_rn(1.0, __dmul_rn(__dmul_rn(dt, __dmul_rn(mob, kappa)), __dmul_rn(lap, lap))));
+    const double2 f = f_hat[i];
+    const double2 ad = adv_hat ? adv_hat[i] : make_double2(0.0, 0.0);
+    const double2 ch = c_hat[i];
+    const double tr = __dsub_rn(__dmul_rn(ml, f.x), ad.x);
+    const double ti = __dsub_rn(__dmul_rn(ml, f.y), ad.y);
+    const double2 nw = make_double2(__dmul_rn(__dadd_rn(ch.x, __dmul_rn(dt, tr)), rden),
+                                    __dmul_rn(__dadd_rn(ch.y, __dmul_rn(dt, ti)), rden));
+    bad |= !isfinite(nw.x);
+    c_hat[i] = nw;
+  }
+  diag_flag_nonfinite(diag, bad);
+}
+
+// mu_c_hat = f_hat - kappa * lap * c_hat
+__global__ void k_ch_mu(const double2* f_hat, const double2* c_hat, double2* out, i64 n, int n1, int n2,
+                        const double* __restrict__ kx, const double* __restrict__ ky,
+                        const double* __restrict__ kz, double kappa) {
+  PFCS_FOR_ALL(n) {
+    const double kl = __dmul_rn(kappa, -k2_at(kx, ky, kz, i, n1, n2));
+    const double2 f = f_hat[i], ch = c_hat[i];
+    out[i] = make_double2(__dsub_rn(f.x, __dmul_rn(kl, ch.x)), __dsub_rn(f.y, __dmul_rn(kl, ch.y)));
+  }
+}
+
+// out = (a + b) + c  (the advection sum assembled from per-rank products)
+__global__ void k_add3(const double2* a, const double2* b, const double2* c, double2* out, i64 n) {
+  PFCS_FOR_ALL(n) {
+    const double2 x = a[i], y = b[i], z = c[i];
+    out[i] = make_double2(__dadd_rn(__dadd_rn(x.x, y.x), z.x), __dadd_rn(__dadd_rn(x.y, y.y), z.y));
+  }
+}
+
+// out = a + w * b (force accumulation: F[psi d mu_psi] + beta F[c d mu_c])
+__global__ void k_axpy(const double2* a, const double2* b, double2* out, i64 n, double w) {
+  PFCS_FOR_ALL(n) {
+    const double2 x = a[i], y = b[i];
+    out[i] = make_double2(__dadd_rn(x.x, __dmul_rn(w, y.x)), __dadd_rn(x.y, __dmul_rn(w, y.y)));
+  }
+}
+
 }  // namespace pfcs
 
 using namespace pfcs;
@@ -199,6 +262,45 @@ int pfcs_hydro_vel_update(void* v_hat, const void* force, int64_t n0, int64_t n1
   k_hydro_vel_update<<<grid_for(n), 256, 0, (cudaStream_t)stream>>>(
       (double2*)v_hat, (const double2*)force, n, (int)n1, (int)n2, kx, ky, kz, c_cg, c_den, c_exp, diag);
   return check_launch("k_hydro_vel_update");
+}
+
+int pfcs_ch_nonlin(const void* c, void* out, int64_t n, double alpha, void* stream) {
+  if (n <= 0) return PFCS_OK;
+  k_ch_nonlin<<<grid_for(n), 256, 0, (cudaStream_t)stream>>>((const double2*)c, (double2*)out, n, alpha);
+  return check_launch("k_ch_nonlin");
+}
+
+int pfcs_ch_update(void* c_hat, const void* f_hat, const void* adv_hat, int64_t n0, int64_t n1, int64_t n2,
+                   const double* kx, const double* ky, const double* kz, double mobility, double kappa,
+                   double dt, double* diag, void* stream) {
+  const i64 n = n0 * n1 * n2;
+  if (n <= 0) return PFCS_OK;
+  k_ch_update<<<grid_for(n), 256, 0, (cudaStream_t)stream>>>((double2*)c_hat, (const double2*)f_hat,
+                                                            (const double2*)adv_hat, n, (int)n1, (int)n2, kx,
+                                                            ky, kz, mobility, kappa, dt, diag);
+  return check_launch("k_ch_update");
+}
+
+int pfcs_ch_mu(const void* f_hat, const void* c_hat, void* out, int64_t n0, int64_t n1, int64_t n2,
+               const double* kx, const double* ky, const double* kz, double kappa, void* stream) {
+  const i64 n = n0 * n1 * n2;
+  if (n <= 0) return PFCS_OK;
+  k_ch_mu<<<grid_for(n), 256, 0, (cudaStream_t)stream>>>((const double2*)f_hat, (const double2*)c_hat,
+                                                        (double2*)out, n, (int)n1, (int)n2, kx, ky, kz, kappa);
+  return check_launch("k_ch_mu");
+}
+
+int pfcs_add3(const void* a, const void* b, const void* c, void* out, int64_t n, void* stream) {
+  if (n <= 0) return PFCS_OK;
+  k_add3<<<grid_for(n), 256, 0, (cudaStream_t)stream>>>((const double2*)a, (const double2*)b, (const double2*)c,
+                                                       (double2*)out, n);
+  return check_launch("k_add3");
+}
+
+int pfcs_axpy(const void* a, const void* b, void* out, int64_t n, double w, void* stream) {
+  if (n <= 0) return PFCS_OK;
+  k_axpy<<<grid_for(n), 256, 0, (cudaStream_t)stream>>>((const double2*)a, (const double2*)b, (double2*)out, n, w);
+  return check_launch("k_axpy");
 }
 
 }  // extern "C"

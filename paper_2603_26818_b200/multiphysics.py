@@ -1,0 +1,277 @@
+"""Multiphysics PFC, field-per-GPU: density, composition and three velocity
+components on 1, 5 or 8 GPUs (north-star item (3); BASELINE configs[4]).
+
+The reference has the four-field hydrodynamic model on exactly 1 or 4
+workers (hydro.py:1-15, hydro.py:129-156).  This module adds a composition
+field c — Cahn-Hilliard, advected by the same velocity and optionally
+feeding a Korteweg-type force back into it:
+
+    mu_c  = alpha (c^3 - c) - kappa lap c
+    dc/dt = M lap mu_c - v . grad c
+    c_hat <- (c_hat + dt (M lap F[alpha (c^3 - c)] - F[v . grad c])) / (1 + dt M kappa lap^2)
+    force_i = F[psi d_i mu_psi] + beta F[c d_i mu_c]
+
+With beta = 0 (default) psi and v are bit-identical to the reference
+four-field dataflow (hydro.serial_hydro_step) and c is a passive scalar.
+There is no reference for c: oracle/ref_numpy.py restates these equations
+(`multi_step`) and the tests check the GPU path against it.
+
+Role maps (one field per GPU, rank -> role):
+  G = 1: all roles serially (the oracle of the parallel modes)
+  G = 5: 0 psi, 1..3 v1..v3, 4 c
+  G = 8: as G = 5 plus 5..7 "advection" roles: rank 5+i computes
+         v_i * F^-1(d_i psi_hat) concurrently with rank 0's F[psi^3], so the
+         density step's critical path drops from 6 to 3 transforms.
+Messages per step (device tensors; NCCL p2p between processes):
+  psi_hat 0 -> 5,6,7 (tag 10, G=8) | products 5+i -> 0 (tag 11+i) |
+  psi 0 -> 1,2,3 (tag 2) | c, c_hat 4 -> 1,2,3 (tags 7, 8; beta != 0) |
+  v_i 1+i -> 0, 4 (tags 4,5,6) and -> 5+i (G=8).
+All modes produce bit-identical fields (same kernels, same summation order).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field as dataclass_field
+
+import numpy as np
+import torch
+
+from . import _native as nat
+from .grid import SymbolTable
+from .hydro import (HydroParams, TAG_PSI, V_TAGS, _cube, _dev, _Diag, _fft, _mul_deriv, _out,
+                    _raise_divergence, _vectors)
+
+__all__ = [
+    "MultiParams",
+    "MultiFields",
+    "ROLES",
+    "composition_step",
+    "density_step",
+    "velocity_step",
+    "serial_multi_step",
+    "parallel_multi_step",
+    "initial_role_state",
+]
+
+TAG_C = 7
+TAG_CHAT = 8
+TAG_PSIHAT = 10
+ADV_TAGS = (11, 12, 13)
+
+ROLES = {
+    1: ["all"],
+    5: ["psi", "v1", "v2", "v3", "c"],
+    8: ["psi", "v1", "v2", "v3", "c", "adv1", "adv2", "adv3"],
+}
+
+
+@dataclass
+class MultiParams:
+    hydro: HydroParams = dataclass_field(default_factory=HydroParams)
+    mobility: float = 1.0
+    kappa: float = 1.0
+    alpha: float = 1.0
+    beta: float = 0.0
+
+    def __post_init__(self):
+        if not (self.mobility > 0 and self.kappa >= 0):
+            raise ValueError("mobility must be > 0 and kappa >= 0")
+
+
+@dataclass
+class MultiFields:
+    psi_hat: object
+    psi: object
+    c_hat: object
+    c: object
+    v_hat: list
+    v: list
+    step_index: int = 0
+    sim_time: float = 0.0
+
+
+def _st():
+    return nat.stream_ptr()
+
+
+def _adv_product(x_hat: torch.Tensor, axis: int, v: torch.Tensor, sym) -> torch.Tensor:
+    """v_axis * F^-1(d_axis * x_hat) (one term of v . grad x)."""
+    g = _fft(_mul_deriv(x_hat, axis, None, sym), False)
+    p = torch.empty_like(g)
+    nat.call("pfcs_cmul", nat.ptr(v), nat.ptr(g), nat.ptr(p), p.numel(), _st())
+    return p
+
+
+def _sum3(a, b, c):
+    out = torch.empty_like(a)
+    nat.call("pfcs_add3", nat.ptr(a), nat.ptr(b), nat.ptr(c), nat.ptr(out), out.numel(), _st())
+    return out
+
+
+def density_step(psi_hat, psi, products, sym: SymbolTable, params: MultiParams, step_index=0):
+    """psi update (hydro.py:77-90) from the three advection products
+    v_i * F^-1(d_i psi_hat) (computed here or by the adv roles)."""
+    ph, ps = _dev(psi_hat), _dev(psi)
+    dev = ph.device
+    kx, ky, kz = _vectors(sym, dev)[:3]
+    n0, n1, n2 = ph.shape
+    nl_hat = _fft(_cube(ps), True)
+    adv_hat = _fft(_sum3(*products), True)
+    new = ph.clone()
+    diag = _Diag(dev)
+    nat.call("pfcs_hydro_psi_update", nat.ptr(new), nat.ptr(nl_hat), nat.ptr(adv_hat), n0, n1, n2,
+             nat.ptr(kx), nat.ptr(ky), nat.ptr(kz), float(sym.eps), float(params.hydro.pfc.dt),
+             nat.ptr(diag.t), _st())
+    if diag.bad():
+        _raise_divergence(step_index, new)
+    return new, _fft(new, False)
+
+
+def composition_step(c_hat, c, v, sym: SymbolTable, params: MultiParams, step_index=0):
+    """Advected Cahn-Hilliard update of the composition (see module doc)."""
+    ch, cc = _dev(c_hat), _dev(c)
+    vs = [_dev(x) for x in v]
+    dev = ch.device
+    kx, ky, kz = _vectors(sym, dev)[:3]
+    n0, n1, n2 = ch.shape
+    prods = [_adv_product(ch, i, vs[i], sym) for i in range(3)]
+    adv_hat = _fft(_sum3(*prods), True)
+    del prods
+    f = torch.empty_like(cc)
+    nat.call("pfcs_ch_nonlin", nat.ptr(cc), nat.ptr(f), f.numel(), float(params.alpha), _st())
+    f_hat = _fft(f, True)
+    new = ch.clone()
+    diag = _Diag(dev)
+    nat.call("pfcs_ch_update", nat.ptr(new), nat.ptr(f_hat), nat.ptr(adv_hat), n0, n1, n2, nat.ptr(kx),
+             nat.ptr(ky), nat.ptr(kz), float(params.mobility), float(params.kappa),
+             float(params.hydro.pfc.dt), nat.ptr(diag.t), _st())
+    if diag.bad():
+        _raise_divergence(step_index, new)
+    return new, _fft(new, False)
+
+
+def velocity_step(v_hat, psi, axis: int, sym: SymbolTable, params: MultiParams, c=None, c_hat=None,
+                  step_index=0):
+    """hydro_velocity_step (hydro.py:93-107) plus beta * F[c d_axis mu_c]."""
+    vh, ps = _dev(v_hat), _dev(psi)
+    dev = vh.device
+    kx, ky, kz = _vectors(sym, dev)[:3]
+    n0, n1, n2 = vh.shape
+    st = _st()
+    nl_hat = _fft(_cube(ps), True)
+    f_hat = _fft(ps, True)
+    mu_hat = torch.empty_like(vh)
+    nat.call("pfcs_hydro_mu", nat.ptr(nl_hat), nat.ptr(f_hat), nat.ptr(mu_hat), n0, n1, n2, nat.ptr(kx),
+             nat.ptr(ky), nat.ptr(kz), float(sym.eps), st)
+    del nl_hat, f_hat
+    force = _fft(_adv_product(mu_hat, axis, ps, sym), True)
+    if params.beta != 0.0:
+        cc, chh = _dev(c), _dev(c_hat)
+        fc = torch.empty_like(cc)
+        nat.call("pfcs_ch_nonlin", nat.ptr(cc), nat.ptr(fc), fc.numel(), float(params.alpha), st)
+        fc_hat = _fft(fc, True)
+        muc = torch.empty_like(fc_hat)
+        nat.call("pfcs_ch_mu", nat.ptr(fc_hat), nat.ptr(chh), nat.ptr(muc), n0, n1, n2, nat.ptr(kx), nat.ptr(ky),
+                 nat.ptr(kz), float(params.kappa), st)
+        force_c = _fft(_adv_product(muc, axis, cc, sym), True)
+        total = torch.empty_like(force)
+        nat.call("pfcs_axpy", nat.ptr(force), nat.ptr(force_c), nat.ptr(total), total.numel(),
+                 float(params.beta), st)
+        force = total
+    hp = params.hydro
+    dt, rho = float(hp.pfc.dt), float(hp.rho)
+    new = vh.clone()
+    diag = _Diag(dev)
+    nat.call("pfcs_hydro_vel_update", nat.ptr(new), nat.ptr(force), n0, n1, n2, nat.ptr(kx), nat.ptr(ky),
+             nat.ptr(kz), dt / rho, (dt / rho) * float(hp.gamma), -0.5 * float(sym.a0) ** 2,
+             nat.ptr(diag.t), st)
+    if diag.bad():
+        _raise_divergence(step_index, new)
+    return new, _fft(new, False)
+
+
+def serial_multi_step(fields: MultiFields, sym: SymbolTable, params: MultiParams) -> MultiFields:
+    """All five roles on one GPU: density and composition from the previous
+    velocities, then the velocities from the fresh density (and composition)."""
+    host = isinstance(fields.psi_hat, np.ndarray)
+    ph = _dev(fields.psi_hat)
+    vs = [_dev(v) for v in fields.v]
+    prods = [_adv_product(ph, i, vs[i], sym) for i in range(3)]
+    psi_hat, psi = density_step(ph, fields.psi, prods, sym, params, fields.step_index)
+    del prods
+    c_hat, c = composition_step(fields.c_hat, fields.c, vs, sym, params, fields.step_index)
+    for i in range(3):
+        vh, v = velocity_step(fields.v_hat[i], psi, i, sym, params, c=c, c_hat=c_hat,
+                              step_index=fields.step_index)
+        fields.v_hat[i], fields.v[i] = _out(vh, host), _out(v, host)
+    fields.psi_hat, fields.psi = _out(psi_hat, host), _out(psi, host)
+    fields.c_hat, fields.c = _out(c_hat, host), _out(c, host)
+    fields.step_index += 1
+    fields.sim_time += params.hydro.pfc.dt
+    return fields
+
+
+def initial_role_state(rank: int, G: int, fields: MultiFields) -> dict:
+    """The slice of a MultiFields a rank owns in the G-role map (device)."""
+    role = ROLES[G][rank]
+    st = {"step_index": fields.step_index, "role": role}
+    if role == "psi":
+        st.update(psi_hat=_dev(fields.psi_hat), psi=_dev(fields.psi), v=[_dev(v) for v in fields.v])
+    elif role == "c":
+        st.update(c_hat=_dev(fields.c_hat), c=_dev(fields.c), v=[_dev(v) for v in fields.v])
+    elif role.startswith("v"):
+        i = int(role[1]) - 1
+        st.update(v_hat=_dev(fields.v_hat[i]), v_own=_dev(fields.v[i]), psi=_dev(fields.psi),
+                  c=_dev(fields.c), c_hat=_dev(fields.c_hat))
+    elif role.startswith("adv"):
+        i = int(role[3]) - 1
+        st.update(v_own=_dev(fields.v[i]), psi_hat=_dev(fields.psi_hat))
+    return st
+
+
+def parallel_multi_step(worker, st: dict, sym: SymbolTable, params: MultiParams) -> dict:
+    """One step of the field-per-GPU dataflow (G = 5 or 8, see module doc)."""
+    G = worker.size
+    if G not in (5, 8):
+        raise ValueError(f"multiphysics field-per-GPU mode runs on 5 or 8 workers, got {G}")
+    role = ROLES[G][worker.rank]
+    idx = st["step_index"]
+    beta = params.beta != 0.0
+    if role == "psi":
+        ph = st["psi_hat"]
+        if G == 8:
+            for h in (5, 6, 7):
+                worker.send_tensor(h, TAG_PSIHAT, ph)
+            prods = [worker.recv_tensor(5 + i, ADV_TAGS[i], torch.empty_like(ph)) for i in range(3)]
+        else:
+            prods = [_adv_product(ph, i, st["v"][i], sym) for i in range(3)]
+        st["psi_hat"], st["psi"] = density_step(ph, st["psi"], prods, sym, params, idx)
+        for dst in (1, 2, 3):
+            worker.send_tensor(dst, TAG_PSI, st["psi"])
+        st["v"] = [worker.recv_tensor(1 + i, V_TAGS[i], torch.empty_like(ph)) for i in range(3)]
+    elif role == "c":
+        st["c_hat"], st["c"] = composition_step(st["c_hat"], st["c"], st["v"], sym, params, idx)
+        if beta:
+            for dst in (1, 2, 3):
+                worker.send_tensor(dst, TAG_C, st["c"])
+                worker.send_tensor(dst, TAG_CHAT, st["c_hat"])
+        st["v"] = [worker.recv_tensor(1 + i, V_TAGS[i], torch.empty_like(st["c"])) for i in range(3)]
+    elif role.startswith("v"):
+        i = int(role[1]) - 1
+        psi = worker.recv_tensor(0, TAG_PSI, torch.empty_like(st["psi"]))
+        st["psi"] = psi
+        if beta:
+            st["c"] = worker.recv_tensor(4, TAG_C, torch.empty_like(st["c"]))
+            st["c_hat"] = worker.recv_tensor(4, TAG_CHAT, torch.empty_like(st["c_hat"]))
+        st["v_hat"], st["v_own"] = velocity_step(st["v_hat"], psi, i, sym, params, c=st.get("c"),
+                                                 c_hat=st.get("c_hat"), step_index=idx)
+        dsts = (0, 4) + ((5 + i,) if G == 8 else ())
+        for dst in dsts:
+            worker.send_tensor(dst, V_TAGS[i], st["v_own"])
+    else:  # advection helper (G = 8)
+        i = int(role[3]) - 1
+        ph = worker.recv_tensor(0, TAG_PSIHAT, torch.empty_like(st["psi_hat"]))
+        worker.send_tensor(0, ADV_TAGS[i], _adv_product(ph, i, st["v_own"], sym))
+        st["v_own"] = worker.recv_tensor(1 + i, V_TAGS[i], torch.empty_like(ph))
+    st["step_index"] = idx + 1
+    return st

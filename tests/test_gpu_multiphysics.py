@@ -1,0 +1,117 @@
+"""Multiphysics field-per-GPU mode (density + composition + 3 velocities on
+1, 5 or 8 workers).  No reference exists for the composition: the numpy
+oracle restates the model (oracle/ref_numpy.py: multi_step).  With beta = 0
+density and velocities must equal the reference's four-field dataflow."""
+
+import math
+
+import numpy as np
+import pytest
+
+from conftest import rel_inf
+
+pytestmark = pytest.mark.gpu
+
+EPS = -0.3
+
+
+@pytest.fixture(scope="module")
+def pkg():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2603_26818_b200 as p
+
+    return p
+
+
+def setup(pkg, n=16, beta=0.0, seed=3):
+    from paper_2603_26818_b200.hydro import HydroParams
+    from paper_2603_26818_b200.multiphysics import MultiFields, MultiParams
+    from paper_2603_26818_b200.pfc import PfcParams, initial_field
+
+    grid = pkg.GridSpec((n,) * 3, (2 * math.pi * math.sqrt(3),) * 3)
+    hp = HydroParams(pfc=PfcParams(eps=EPS, dt=0.1), rho=1.0, gamma=1.0, a0=2.0)
+    mp = MultiParams(hydro=hp, mobility=0.7, kappa=0.5, alpha=1.0, beta=beta)
+    sym = pkg.make_symbols(grid, EPS, a0=2.0)
+    psi0 = initial_field("two_mode_fcc_3d", grid, psi_bar=-0.3, amplitude=0.05)
+    c0 = initial_field("constant_plus_noise", grid, psi_bar=0.0, seed=seed, noise_amplitude=0.1)
+    psi_hat = np.fft.fftn(psi0.astype(np.complex128))
+    c_hat = np.fft.fftn(c0.astype(np.complex128))
+    rng = np.random.default_rng(seed)
+    v = [(1e-3 * rng.standard_normal(grid.shape)).astype(np.complex128) for _ in range(3)]
+    fields = MultiFields(psi_hat=psi_hat, psi=np.fft.ifftn(psi_hat), c_hat=c_hat, c=np.fft.ifftn(c_hat),
+                         v_hat=[np.fft.fftn(x) for x in v], v=[x.copy() for x in v])
+    return grid, sym, mp, fields
+
+
+def copy_fields(f):
+    from paper_2603_26818_b200.multiphysics import MultiFields
+
+    return MultiFields(psi_hat=f.psi_hat.copy(), psi=f.psi.copy(), c_hat=f.c_hat.copy(), c=f.c.copy(),
+                       v_hat=[x.copy() for x in f.v_hat], v=[x.copy() for x in f.v])
+
+
+@pytest.mark.parametrize("beta", [0.0, 0.5])
+def test_serial_vs_oracle(pkg, beta):
+    import ref_numpy as ora
+    from paper_2603_26818_b200.multiphysics import serial_multi_step
+
+    grid, sym, mp, f = setup(pkg, beta=beta)
+    o = {"psi_hat": f.psi_hat.copy(), "psi": f.psi.copy(), "c_hat": f.c_hat.copy(), "c": f.c.copy(),
+         "v_hat": [x.copy() for x in f.v_hat], "v": [x.copy() for x in f.v]}
+    osym = ora.symbols(grid.n, grid.length, EPS, a0=2.0)
+    for _ in range(8):
+        serial_multi_step(f, sym, mp)
+        ora.multi_step(o, osym, 0.1, 1.0, 1.0, 0.7, 0.5, 1.0, beta)
+    assert rel_inf(f.psi, o["psi"]) <= 1e-12
+    assert rel_inf(f.c, o["c"]) <= 1e-12
+    for i in range(3):
+        assert rel_inf(f.v[i], o["v"][i]) <= 1e-9
+    assert float(np.max(np.abs(f.c.imag))) <= 1e-12 * float(np.max(np.abs(f.c.real)))
+
+
+def test_beta_zero_reproduces_four_field_hydro(pkg):
+    from paper_2603_26818_b200.hydro import HydroFields, serial_hydro_step
+    from paper_2603_26818_b200.multiphysics import serial_multi_step
+
+    grid, sym, mp, f = setup(pkg)
+    h = HydroFields(psi_hat=f.psi_hat.copy(), psi=f.psi.copy(), v_hat=[x.copy() for x in f.v_hat],
+                    v=[x.copy() for x in f.v])
+    for _ in range(5):
+        serial_multi_step(f, sym, mp)
+        serial_hydro_step(h, sym, mp.hydro)
+    np.testing.assert_array_equal(f.psi_hat, h.psi_hat)
+    for i in range(3):
+        np.testing.assert_array_equal(f.v_hat[i], h.v_hat[i])
+
+
+@pytest.mark.parametrize("G", [5, 8])
+@pytest.mark.parametrize("beta", [0.0, 0.5])
+def test_field_per_gpu_equals_serial_bitwise(pkg, G, beta):
+    from paper_2603_26818_b200.multiphysics import (ROLES, initial_role_state, parallel_multi_step,
+                                                    serial_multi_step)
+
+    grid, sym, mp, f = setup(pkg, beta=beta)
+    ref = copy_fields(f)
+    for _ in range(4):
+        serial_multi_step(ref, sym, mp)
+
+    def body(w):
+        st = initial_role_state(w.rank, G, f)
+        for _ in range(4):
+            parallel_multi_step(w, st, sym, mp)
+        role = ROLES[G][w.rank]
+        key = {"psi": "psi", "c": "c"}.get(role, "v_own")
+        return role, st[key].cpu().numpy()
+
+    for role, val in pkg.spawn_group(G, body):
+        if role == "psi":
+            np.testing.assert_array_equal(val, ref.psi)
+        elif role == "c":
+            np.testing.assert_array_equal(val, ref.c)
+        elif role.startswith("v"):
+            np.testing.assert_array_equal(val, ref.v[int(role[1]) - 1])
+        else:  # adv helpers keep the latest v_i
+            np.testing.assert_array_equal(val, ref.v[int(role[3]) - 1])
