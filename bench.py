@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--fft-n", type=int, default=FFT_N)
     ap.add_argument("--pfc-n", type=int, default=PFC_N)
     ap.add_argument("--no-pfc", action="store_true")
+    ap.add_argument("--multi-n", type=int, default=512)
+    ap.add_argument("--no-multi", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     return ap.parse_args()
@@ -223,13 +225,17 @@ def timed(ctx, fn, steps: int, warmup: int):
     torch.cuda.synchronize()
     ctx.barrier()
     torch.cuda.synchronize()
+    from paper_2603_26818_b200 import _native as nat
+
     a = torch.cuda.Event(enable_timing=True)
     b = torch.cuda.Event(enable_timing=True)
+    n0 = nat.launches
     a.record()
     for _ in range(steps):
         fn()
     b.record()
     torch.cuda.synchronize()
+    ctx.timed_launches = nat.launches - n0  # libpfcs launches inside the timed region
     ctx.barrier()
     torch.cuda.synchronize()
     return ctx.max_over_ranks(a.elapsed_time(b) / steps)
@@ -298,9 +304,8 @@ def run_fft(ctx, args, out):
         spec = distfft.forward(field, w)
         holder["back"] = distfft.inverse(spec, w)
 
-    nat.launches = 0
     ms = timed(ctx, step, args.steps, args.warmup)
-    launches = nat.launches - 0
+    launches = ctx.timed_launches
     # per-kernel device times over a traced pass of the same K steps
     nat.trace = []
     timed(ctx, step, args.steps, 0)
@@ -369,6 +374,58 @@ def run_pfc2d(ctx, args):
     return {"metric": "PFC time-steps/sec", "value": round(1000.0 / ms, 1), "unit": "steps/s",
             "ms_per_step": round(ms, 5), "wall_s_per_100_steps": round(wall, 5),
             "config": "2D PFC 256x256 fp64 R2C, 100 steps (configs[0]), launch-bound"}
+
+
+def run_multi(ctx, args):
+    """configs[4]: multiphysics PFC (density + composition + 3 velocities),
+    field-per-GPU: 1 GPU runs all roles, 4 GPUs the reference's four-role
+    hydro dataflow, 5 / 8 GPUs the multiphysics role maps."""
+    import numpy as np
+    import torch
+
+    from paper_2603_26818_b200 import hydro, multiphysics as mpx
+    from paper_2603_26818_b200.grid import GridSpec, make_symbols
+    from paper_2603_26818_b200.pfc import PfcParams
+
+    G = ctx.world
+    if G not in (1, 4, 5, 8):
+        return None
+    n = args.multi_n
+    grid = GridSpec((n,) * 3, (2 * np.pi * np.sqrt(3) * (n // 8),) * 3)
+    hp = hydro.HydroParams(pfc=PfcParams(eps=-0.3, dt=0.1), rho=1.0, gamma=1.0, a0=2.0)
+    mp = mpx.MultiParams(hydro=hp, mobility=1.0, kappa=1.0, alpha=1.0, beta=0.0)
+    sym = make_symbols(grid, -0.3, a0=2.0)
+    gen = torch.Generator(device=ctx.device).manual_seed(11)
+    C = torch.complex128
+
+    def field(scale, base=0.0):
+        x = torch.rand((n,) * 3, dtype=torch.float64, device=ctx.device, generator=gen)
+        return (base + scale * (x - 0.5)).to(C)
+
+    psi = field(0.02, -0.3)
+    c = field(0.2)
+    zeros = torch.zeros((n,) * 3, dtype=C, device=ctx.device)
+    f = mpx.MultiFields(psi_hat=hydro._fft(psi, True), psi=psi, c_hat=hydro._fft(c, True), c=c,
+                        v_hat=[zeros.clone() for _ in range(3)], v=[zeros.clone() for _ in range(3)])
+    w = ctx.worker()
+    steps = max(2, args.steps // 5)
+    if G == 1:
+        fn = lambda: mpx.serial_multi_step(f, sym, mp)  # noqa: E731
+        mode = "all 5 roles on 1 GPU"
+    elif G == 4:
+        hf = hydro.HydroFields(psi_hat=f.psi_hat, psi=f.psi, v_hat=f.v_hat, v=f.v)
+        st = ({"psi_hat": hf.psi_hat, "psi": hf.psi, "v": list(hf.v), "step_index": 0} if ctx.rank == 0
+              else {"v_hat": zeros.clone(), "psi": zeros.clone(), "step_index": 0})
+        fn = lambda: hydro.parallel_hydro_step(w, st, sym, hp)  # noqa: E731
+        mode = "reference 4-role hydro dataflow (psi, v1..v3), no composition"
+    else:
+        st = mpx.initial_role_state(ctx.rank, G, f)
+        fn = lambda: mpx.parallel_multi_step(w, st, sym, mp)  # noqa: E731
+        mode = f"{G}-role field-per-GPU map {mpx.ROLES[G]}"
+    ms = timed(ctx, fn, steps, 1)
+    return {"metric": "multiphysics PFC time-steps/sec", "value": round(1000.0 / ms, 3), "unit": "steps/s",
+            "ms_per_step": round(ms, 3), "steps": steps,
+            "config": f"{n}^3 complex128 full-grid fields, density+composition+v1..v3; {mode}"}
 
 
 def run_pfc(ctx, args):
@@ -475,6 +532,7 @@ def main():
         table = run_fft(ctx, args, out)
         pfc_res = None if args.no_pfc else run_pfc(ctx, args)
         pfc2d = None if args.no_pfc else run_pfc2d(ctx, args)
+        multi = None if args.no_multi else run_multi(ctx, args)
     out["clocks"] = clk.summary()
     workload = f"fft{args.fft_n}" if ctx.world == 1 else None
     out["roofline"] = roofline_of(table, hbm, peak_kind, measured_traffic(workload))
@@ -487,6 +545,8 @@ def main():
         out["pfc"] = pfc_res
     if pfc2d is not None:
         out["pfc2d"] = pfc2d
+    if multi is not None:
+        out["multiphysics"] = multi
     out["gpu_launches"] = int(out.pop("launches_total"))
     if ctx.rank == 0 and ctx.world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_fft_baseline(args.fft_n, args.cpu_seconds)
