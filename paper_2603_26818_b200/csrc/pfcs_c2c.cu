@@ -370,9 +370,16 @@ int launch_strided_blocked(const double2* in, double2* out, long long outer, int
   return fail(PFCS_E_UNSUPPORTED, "unsupported line length");
 }
 
+int launch_mixed(const double2* in, double2* out, long long outer, int n, long long inner, bool forward,
+                 cudaStream_t st);
+
 int launch_dft(const double2* in, double2* out, long long outer, int n, long long inner, bool forward,
                cudaStream_t st) {
   if (outer <= 0 || inner <= 0) return PFCS_OK;
+  // mixed-radix Stockham first (pfcs_mixed.cu); the O(N^2) sum only for
+  // lengths with a prime factor > 64 or tiles beyond shared memory
+  const int rc = launch_mixed(in, out, outer, n, inner, forward, st);
+  if (rc != -1) return rc;
   if (n > 16384) return fail(PFCS_E_UNSUPPORTED, "direct DFT limited to N <= 16384");
   const double2* tw = twiddles(n);
   if (!tw) return PFCS_E_CUDA;

@@ -30,7 +30,7 @@ def rand(shape, seed=0):
     return rng.standard_normal(shape) + 1j * rng.standard_normal(shape)
 
 
-@pytest.mark.parametrize("n", list(range(1, 17)) + [31, 32, 64, 100, 128, 256, 512, 750, 1024, 2048, 4096])
+@pytest.mark.parametrize("n", list(range(1, 17)) + [31, 32, 64, 100, 128, 243, 256, 512, 750, 1000, 1024, 1400, 2048, 4096, 4099])
 @pytest.mark.parametrize("axis", [0, 1, 2])
 def test_fft_axis_lengths(pkg, n, axis):
     import ref_numpy as ora
