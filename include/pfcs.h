@@ -67,6 +67,38 @@ int pfcs_fft_zlines(const void* in, void* out, int64_t nlines, int64_t nz, int g
 int pfcs_fft_lines(const void* in, void* out, int64_t outer, int64_t n, int64_t inner, int g_in, int g_out,
                    int forward, void* stream);
 
+/* ---- fused exchanges (north-star item (2): the transpose fused into the
+ * FFT epilogue over NVLink peer memory).  `dst` is a HOST array of g_out
+ * device addresses — typically the receive buffers of the g_out ranks,
+ * mapped with pfcs_enable_peer_access (threads) or pfcs_ipc_open_handle
+ * (processes), each already offset to where this rank's block lands.  The
+ * kernel stores every output element straight into its owner's buffer, so
+ * there is no send buffer and no separate all-to-all; the caller only
+ * orders the step with a barrier.
+ * pfcs_fft_zlines_to:     as pfcs_fft_zlines; z block h of line l goes to
+ *                         dst[h] + l*cz_h + (z - zoff_h).
+ * pfcs_fft_lines_scatter: lines along the middle axis of (outer, n, inner)
+ *                         (input plain or blocked over g_in); output row o
+ *                         goes to dst[h] + ((o - ooff_h)*n + k)*inner + i,
+ *                         h the owner of o in slab_layout(outer, g_outer).
+ * pfcs_pfc_update_z_to:   pfcs_pfc_update_z with the next-step inverse
+ *                         scattered like pfcs_fft_zlines_to. */
+int pfcs_fft_zlines_to(const void* in, const uint64_t* dst, int64_t nlines, int64_t nz, int g_in, int g_out,
+                       int forward, void* stream);
+int pfcs_fft_lines_scatter(const void* in, const uint64_t* dst, int64_t outer, int64_t n, int64_t inner,
+                           int g_in, int g_outer, int forward, void* stream);
+int pfcs_pfc_update_z_to(const void* nl, void* psi_hat, const uint64_t* dst, int64_t cx, int64_t ny, int64_t nz,
+                         int g_in, int g_out, const double* kx, const double* ky, const double* kz, double eps,
+                         double dt, double* diag, void* stream);
+/* Peer / IPC plumbing for the fused exchanges. */
+int pfcs_enable_peer_access(int peer_device);
+int pfcs_malloc(int64_t bytes, void** ptr);
+int pfcs_free(void* ptr);
+int pfcs_ipc_get_handle(const void* ptr, void* handle64);
+int pfcs_ipc_open_handle(const void* handle64, void** ptr);
+int pfcs_ipc_close(void* ptr);
+int pfcs_stream_sync(void* stream);
+
 /* ---- real transforms along axis 0 (x) of a C-order array (new: R2C/C2R,
  * north-star item (1)).  rfft: real (nx, inner) -> complex (nx/2+1, inner),
  * unnormalised.  irfft: complex (nx/2+1, inner) -> real (nx, inner), scaled

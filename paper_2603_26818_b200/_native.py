@@ -38,6 +38,17 @@ _SIGS = {
     "pfcs_fft_axis_c2c": [_c_p, _c_p, _c_i64, _c_i64, _c_i64, _c_int, _c_int, _c_p],
     "pfcs_fft_zlines": [_c_p, _c_p, _c_i64, _c_i64, _c_int, _c_int, _c_int, _c_p],
     "pfcs_fft_lines": [_c_p, _c_p, _c_i64, _c_i64, _c_i64, _c_int, _c_int, _c_int, _c_p],
+    "pfcs_fft_zlines_to": [_c_p, _c_p, _c_i64, _c_i64, _c_int, _c_int, _c_int, _c_p],
+    "pfcs_fft_lines_scatter": [_c_p, _c_p, _c_i64, _c_i64, _c_i64, _c_int, _c_int, _c_int, _c_p],
+    "pfcs_pfc_update_z_to": [_c_p, _c_p, _c_p, _c_i64, _c_i64, _c_i64, _c_int, _c_int, _c_p, _c_p, _c_p,
+                             _c_d, _c_d, _c_p, _c_p],
+    "pfcs_enable_peer_access": [_c_int],
+    "pfcs_malloc": [_c_i64, ctypes.POINTER(_c_p)],
+    "pfcs_free": [_c_p],
+    "pfcs_ipc_get_handle": [_c_p, _c_p],
+    "pfcs_ipc_open_handle": [_c_p, ctypes.POINTER(_c_p)],
+    "pfcs_ipc_close": [_c_p],
+    "pfcs_stream_sync": [_c_p],
     "pfcs_rfft_x": [_c_p, _c_p, _c_i64, _c_i64, _c_p],
     "pfcs_irfft_x": [_c_p, _c_p, _c_i64, _c_i64, _c_p],
     "pfcs_pfc_cube_x": [_c_p, _c_i64, _c_i64, _c_int, _c_p, _c_p],

@@ -11,6 +11,7 @@
 #include <string>
 #include <vector>
 
+#include "pfcs_fft.cuh"
 #include "pfcs_internal.h"
 
 namespace pfcs {
@@ -168,7 +169,8 @@ int launch_real_x(const void* in, void* out, long long nx, long long inner, int 
 int launch_cube_c2c(void* data, long long nx, long long inner, double* diag, cudaStream_t st);
 int launch_pfc_z(const double2* nl, double2* psi_hat, double2* next, long long cx, long long ny,
                  long long nz, int g_in, int g_out, const double* kx, const double* ky,
-                 const double* kz, double eps, double dt, double* diag, cudaStream_t st);
+                 const double* kz, double eps, double dt, double* diag, cudaStream_t st,
+                 const PeerTable* dst);
 int launch_pfc_cube(void* data, long long n, int real, double* diag, cudaStream_t st);
 int launch_pfc_update(const double2* nl, double2* psi_hat, long long cx, long long ny, long long nz,
                       const double* kx, const double* ky, const double* kz, double eps, double dt,
@@ -267,8 +269,82 @@ int pfcs_pfc_update_z(const void* nl, void* psi_hat, void* next_out, int64_t cx,
                       const double* kz, double eps, double dt, double* diag, void* stream) {
   if (cx < 0 || ny < 1 || nz < 1 || g_in < 1 || g_out < 1) return fail(PFCS_E_ARG, "bad slab geometry");
   return launch_pfc_z((const double2*)nl, (double2*)psi_hat, (double2*)next_out, cx, ny, nz, g_in, g_out,
-                      kx, ky, kz, eps, dt, diag, S(stream));
+                      kx, ky, kz, eps, dt, diag, S(stream), nullptr);
 }
+
+// ------------------------------------------------------ fused exchanges ----
+
+static int make_table(const uint64_t* dst, int g, PeerTable* t) {
+  if (!dst || g < 1 || g > PFCS_MAX_PEERS) return fail(PFCS_E_ARG, "destination table needs 1..16 entries");
+  *t = PeerTable{};
+  for (int i = 0; i < g; ++i) t->p[i] = (double2*)(uintptr_t)dst[i];
+  return PFCS_OK;
+}
+
+int pfcs_fft_zlines_to(const void* in, const uint64_t* dst, int64_t nlines, int64_t nz, int g_in, int g_out,
+                       int forward, void* stream) {
+  PeerTable t;
+  if (int rc = make_table(dst, g_out, &t)) return rc;
+  if (nlines <= 0) return PFCS_OK;
+  return launch_lines_to((const double2*)in, nullptr, nlines, (int)nz, g_in, g_out, &t, forward != 0,
+                         S(stream));
+}
+
+int pfcs_fft_lines_scatter(const void* in, const uint64_t* dst, int64_t outer, int64_t n, int64_t inner,
+                           int g_in, int g_outer, int forward, void* stream) {
+  PeerTable t;
+  if (int rc = make_table(dst, g_outer, &t)) return rc;
+  return launch_strided_to((const double2*)in, outer, (int)n, inner, g_in, &t, g_outer, forward != 0,
+                           S(stream));
+}
+
+int pfcs_pfc_update_z_to(const void* nl, void* psi_hat, const uint64_t* dst, int64_t cx, int64_t ny, int64_t nz,
+                         int g_in, int g_out, const double* kx, const double* ky, const double* kz, double eps,
+                         double dt, double* diag, void* stream) {
+  PeerTable t;
+  if (int rc = make_table(dst, g_out, &t)) return rc;
+  if (cx < 0 || ny < 1 || nz < 1 || g_in < 1) return fail(PFCS_E_ARG, "bad slab geometry");
+  return launch_pfc_z((const double2*)nl, (double2*)psi_hat, nullptr, cx, ny, nz, g_in, g_out, kx, ky, kz, eps,
+                      dt, diag, S(stream), &t);
+}
+
+int pfcs_enable_peer_access(int peer_device) {
+  int dev = 0;
+  if (int rc = check_cuda(cudaGetDevice(&dev), "cudaGetDevice")) return rc;
+  if (peer_device == dev) return PFCS_OK;
+  int can = 0;
+  if (int rc = check_cuda(cudaDeviceCanAccessPeer(&can, dev, peer_device), "cudaDeviceCanAccessPeer")) return rc;
+  if (!can) return fail(PFCS_E_UNSUPPORTED, "no peer access between these devices");
+  const cudaError_t e = cudaDeviceEnablePeerAccess(peer_device, 0);
+  if (e == cudaErrorPeerAccessAlreadyEnabled) {
+    cudaGetLastError();
+    return PFCS_OK;
+  }
+  return check_cuda(e, "cudaDeviceEnablePeerAccess");
+}
+
+int pfcs_malloc(int64_t bytes, void** ptr) {
+  return check_cuda(cudaMalloc(ptr, (size_t)(bytes > 0 ? bytes : 16)), "cudaMalloc");
+}
+
+int pfcs_free(void* ptr) { return check_cuda(cudaFree(ptr), "cudaFree"); }
+
+int pfcs_ipc_get_handle(const void* ptr, void* handle64) {
+  cudaIpcMemHandle_t h;
+  if (int rc = check_cuda(cudaIpcGetMemHandle(&h, (void*)ptr), "cudaIpcGetMemHandle")) return rc;
+  memcpy(handle64, &h, sizeof(h));
+  return PFCS_OK;
+}
+
+int pfcs_ipc_open_handle(const void* handle64, void** ptr) {
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle64, sizeof(h));
+  return check_cuda(cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+}
+
+int pfcs_ipc_close(void* ptr) { return check_cuda(cudaIpcCloseMemHandle(ptr), "cudaIpcCloseMemHandle"); }
+
+int pfcs_stream_sync(void* stream) { return check_cuda(cudaStreamSynchronize(S(stream)), "cudaStreamSynchronize"); }
 
 int pfcs_pfc_cube(void* data, int64_t n, int real, double* diag, void* stream) {
   if (n < 0) return fail(PFCS_E_ARG, "negative count");

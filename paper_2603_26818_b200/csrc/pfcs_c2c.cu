@@ -29,7 +29,7 @@ struct Regs1 {
 
 template <int N, int T, int ST, bool FWD, bool BIN, bool BOUT>
 __global__ void __launch_bounds__(T*(N / radix_R(N)), min_blocks(T*(N / radix_R(N)), ST == 2 ? 640 : 1024))
-    k_lines(const double2* in, double2* out, i64 nlines, SlabSplit sin, SlabSplit sout,
+    k_lines(const double2* in, double2* out, i64 nlines, SlabSplit sin, SlabSplit sout, PeerTable tout,
             const double2* __restrict__ tw, double scale) {
   constexpr int R = radix_R(N);
   constexpr int P = N / R;
@@ -64,17 +64,15 @@ __global__ void __launch_bounds__(T*(N / radix_R(N)), min_blocks(T*(N / radix_R(
 #pragma unroll
       for (int e = 0; e < R; ++e) {
         const int z = j + P * e;
-        i64 a;
-        if (BOUT) {
-          int zoff, cz;
-          sout.locate(z, zoff, cz);
-          a = nlines * zoff + l * cz + (z - zoff);
-        } else {
-          a = l * N + z;
-        }
         double2 x = r.v[e];
         if (!FWD) x = make_double2(x.x * scale, x.y * scale);
-        out[a] = x;
+        if (BOUT) {  // block h of z -> tout.p[h] (local send slab or the peer's buffer)
+          int h, zoff, cz;
+          sout.locate3(z, h, zoff, cz);
+          tout.p[h][l * cz + (z - zoff)] = x;
+        } else {
+          out[l * N + z] = x;
+        }
       }
     }
   };
@@ -94,10 +92,15 @@ __device__ __forceinline__ i64 line_addr(i64 o, int n, i64 i, int N, i64 outer, 
   return outer * inner * noff + (o * cn + (n - noff)) * inner + i;
 }
 
-template <int N, int T, int ST, bool FWD, bool BIN, bool BOUT>
+// OPEER: the output rows (outer index o) are scattered by owner — row o of
+// the plain result goes to tout.p[h] + ((o - ooff_h) N + n) inner + i, h the
+// slab of o under `souter` (fused forward exchange: the peer's receive
+// buffer, written over NVLink from this epilogue).
+template <int N, int T, int ST, bool FWD, bool BIN, bool BOUT, bool OPEER = false>
 __global__ void __launch_bounds__(T*(N / radix_R(N)), min_blocks(T*(N / radix_R(N)), ST == 2 ? 640 : 1024))
     k_strided(const double2* in, double2* out, i64 outer, i64 inner, i64 tpo, SlabSplit sin,
-              SlabSplit sout, const double2* __restrict__ tw, double scale) {
+              SlabSplit sout, const double2* __restrict__ tw, double scale, SlabSplit souter = SlabSplit{},
+              PeerTable tout = PeerTable{}) {
   constexpr int R = radix_R(N);
   constexpr int P = N / R;
   constexpr int LS = tile_ls(N, T, true);
@@ -120,11 +123,19 @@ __global__ void __launch_bounds__(T*(N / radix_R(N)), min_blocks(T*(N / radix_R(
     const i64 i = (tile - o * tpo) * T + t;
     fft_line<N, FWD>(r.v, j, sl, tw);
     if (i < inner) {
+      double2* dst = out;
+      i64 orow = o;
+      if (OPEER) {
+        int h, ooff, co;
+        souter.locate3((int)o, h, ooff, co);
+        dst = tout.p[h];
+        orow = o - ooff;
+      }
 #pragma unroll
       for (int e = 0; e < R; ++e) {
         double2 x = r.v[e];
         if (!FWD) x = make_double2(x.x * scale, x.y * scale);
-        out[line_addr<BOUT>(o, j + P * e, i, N, outer, inner, sout)] = x;
+        dst[line_addr<BOUT>(orow, j + P * e, i, N, outer, inner, sout)] = x;
       }
     }
   };
@@ -251,12 +262,14 @@ static int blocked_dft(const double2* in, double2* out, i64 outer, int n, i64 in
 
 template <int N, bool FWD>
 static int lines_n(const double2* in, double2* out, i64 nlines, SlabSplitH si, SlabSplitH so,
-                   cudaStream_t st) {
+                   const PeerTable* dst, cudaStream_t st) {
   const double2* tw = twiddles(N);
   if (!tw) return PFCS_E_CUDA;
   SlabSplit a{si.G, si.base, si.extra}, b{so.G, so.base, so.extra};
   const double scale = 1.0 / (double)N;
-  const bool bin = si.G > 1, bout = so.G > 1;
+  const bool bin = si.G > 1, bout = so.G > 1 || dst != nullptr;
+  if (so.G > PFCS_MAX_PEERS) return fail(PFCS_E_UNSUPPORTED, "more than 16 slabs");
+  const PeerTable tab = dst ? *dst : local_table(out, nlines, so.G, so.base, so.extra);
   return with_variant<KIND_LINES, N>([&](auto var) -> int {
     constexpr int V = decltype(var)::value;
     constexpr int T = TileCfg<N>::T_MIN << (V & 3);
@@ -274,10 +287,10 @@ static int lines_n(const double2* in, double2* out, i64 nlines, SlabSplitH si, S
     else f = (const void*)k_lines<N, T, ST, FWD, false, false>;
     int grid = 0;
     if (int rc = persistent_grid(f, T * P, smem, ntiles, &grid)) return rc;
-    if (bin && bout) k_lines<N, T, ST, FWD, true, true><<<grid, T * P, smem, st>>>(in, out, nlines, a, b, tw, scale);
-    else if (bin) k_lines<N, T, ST, FWD, true, false><<<grid, T * P, smem, st>>>(in, out, nlines, a, b, tw, scale);
-    else if (bout) k_lines<N, T, ST, FWD, false, true><<<grid, T * P, smem, st>>>(in, out, nlines, a, b, tw, scale);
-    else k_lines<N, T, ST, FWD, false, false><<<grid, T * P, smem, st>>>(in, out, nlines, a, b, tw, scale);
+    if (bin && bout) k_lines<N, T, ST, FWD, true, true><<<grid, T * P, smem, st>>>(in, out, nlines, a, b, tab, tw, scale);
+    else if (bin) k_lines<N, T, ST, FWD, true, false><<<grid, T * P, smem, st>>>(in, out, nlines, a, b, tab, tw, scale);
+    else if (bout) k_lines<N, T, ST, FWD, false, true><<<grid, T * P, smem, st>>>(in, out, nlines, a, b, tab, tw, scale);
+    else k_lines<N, T, ST, FWD, false, false><<<grid, T * P, smem, st>>>(in, out, nlines, a, b, tab, tw, scale);
     return check_launch("k_lines");
     }
   });
@@ -327,15 +340,24 @@ static int strided_n(const double2* in, double2* out, i64 outer, i64 inner, Slab
 
 int launch_lines_c2c(const double2* in, double2* out, long long nlines, int n, int g_in, int g_out,
                      bool forward, cudaStream_t st) {
+  return launch_lines_to(in, out, nlines, n, g_in, g_out, nullptr, forward, st);
+}
+
+// As launch_lines_c2c; with `dst` the blocked output slab g goes to
+// dst->p[g] instead of out + nlines*zoff_g (fused exchange: peer buffers).
+int launch_lines_to(const double2* in, double2* out, long long nlines, int n, int g_in, int g_out,
+                    const PeerTable* dst, bool forward, cudaStream_t st) {
   if (nlines <= 0) return PFCS_OK;
   const SlabSplitH si = slab_split(n, g_in), so = slab_split(n, g_out);
   if (!is_pow2(n) || n > 4096) {
+    if (dst) return fail(PFCS_E_UNSUPPORTED, "peer-scattered z lines need a power-of-two length");
     return blocked_dft(in, out, nlines, n, 1, si, so, forward, st);
   }
   switch (n) {
 #define PFCS_CASE(NN) \
   case NN:            \
-    return forward ? lines_n<NN, true>(in, out, nlines, si, so, st) : lines_n<NN, false>(in, out, nlines, si, so, st);
+    return forward ? lines_n<NN, true>(in, out, nlines, si, so, dst, st)  \
+                   : lines_n<NN, false>(in, out, nlines, si, so, dst, st);
     PFCS_POW2_CASES(PFCS_CASE)
 #undef PFCS_CASE
     default:
@@ -347,6 +369,59 @@ int launch_lines_c2c(const double2* in, double2* out, long long nlines, int n, i
 int launch_strided_c2c(const double2* in, double2* out, long long outer, int n, long long inner,
                        bool forward, cudaStream_t st) {
   return launch_strided_blocked(in, out, outer, n, inner, 1, 1, forward, st);
+}
+
+template <int N, bool FWD>
+static int strided_to_n(const double2* in, i64 outer, i64 inner, SlabSplitH si, SlabSplitH souter,
+                        const PeerTable& dst, cudaStream_t st) {
+  const double2* tw = twiddles(N);
+  if (!tw) return PFCS_E_CUDA;
+  SlabSplit a{si.G, si.base, si.extra}, so{souter.G, souter.base, souter.extra};
+  const bool bin = si.G > 1;
+  return with_variant<KIND_STRIDED, N>([&](auto var) -> int {
+    constexpr int V = decltype(var)::value;
+    constexpr int T = TileCfg<N>::T_MIN << (V & 3);
+    constexpr int ST = 1 + (V >> 2);
+    constexpr int P = TileCfg<N>::P;
+    if constexpr (T * P > 1024) {
+      return fail(PFCS_E_UNSUPPORTED, "tile too large");
+    } else {
+      const size_t smem = (size_t)T * tile_ls(N, T, true) * sizeof(double2);
+      const i64 tpo = (inner + T - 1) / T;
+      const void* f = bin ? (const void*)k_strided<N, T, ST, FWD, true, false, true>
+                          : (const void*)k_strided<N, T, ST, FWD, false, false, true>;
+      int grid = 0;
+      if (int rc = persistent_grid(f, T * P, smem, outer * tpo, &grid)) return rc;
+      const double sc = 1.0 / (double)N;
+      if (bin)
+        k_strided<N, T, ST, FWD, true, false, true><<<grid, T * P, smem, st>>>(
+            in, nullptr, outer, inner, tpo, a, a, tw, sc, so, dst);
+      else
+        k_strided<N, T, ST, FWD, false, false, true><<<grid, T * P, smem, st>>>(
+            in, nullptr, outer, inner, tpo, a, a, tw, sc, so, dst);
+      return check_launch("k_strided(peer)");
+    }
+  });
+}
+
+int launch_strided_to(const double2* in, long long outer, int n, long long inner, int g_in,
+                      const PeerTable* dst, int g_outer, bool forward, cudaStream_t st) {
+  if (outer <= 0 || inner <= 0) return PFCS_OK;
+  if (!dst || g_outer > PFCS_MAX_PEERS) return fail(PFCS_E_ARG, "bad destination table");
+  if (!is_pow2(n) || n > 4096 || inner == 1)
+    return fail(PFCS_E_UNSUPPORTED, "peer-scattered strided lines need a power-of-two length and inner > 1");
+  const SlabSplitH si = slab_split(n, g_in), so = slab_split(outer, g_outer);
+  switch (n) {
+#define PFCS_CASE(NN)                                                             \
+  case NN:                                                                        \
+    return forward ? strided_to_n<NN, true>(in, outer, inner, si, so, *dst, st)   \
+                   : strided_to_n<NN, false>(in, outer, inner, si, so, *dst, st);
+    PFCS_POW2_CASES(PFCS_CASE)
+#undef PFCS_CASE
+    default:
+      break;
+  }
+  return fail(PFCS_E_UNSUPPORTED, "unsupported line length");
 }
 
 int launch_strided_blocked(const double2* in, double2* out, long long outer, int n, long long inner, int g_in,

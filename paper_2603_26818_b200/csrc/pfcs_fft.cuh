@@ -306,18 +306,43 @@ struct TileCfg {
 struct SlabSplit {
   int G, base, extra;
   __host__ __device__ __forceinline__ void locate(int z, int& zoff, int& cz) const {
+    int g;
+    locate3(z, g, zoff, cz);
+  }
+  __host__ __device__ __forceinline__ void locate3(int z, int& g, int& zoff, int& cz) const {
     const int big = base + 1;
     const int split = extra * big;
     if (z < split) {
-      const int g = z / big;
+      g = z / big;
       zoff = g * big;
       cz = big;
     } else {
-      const int g = (z - split) / base;
-      zoff = split + g * base;
+      g = extra + (z - split) / base;
+      zoff = split + (g - extra) * base;
       cz = base;
     }
   }
 };
+
+// Per-destination base pointers of a scattered ("blocked") output.  Block g
+// of the split axis goes to p[g]: a slab of the local send buffer, or —
+// for the fused exchange — the receive buffer of rank g itself, mapped
+// through CUDA peer access / IPC, so the FFT epilogue stores straight over
+// NVLink (no separate all-to-all).  Passed by value (kernel parameter).
+#define PFCS_MAX_PEERS 16
+struct PeerTable {
+  double2* p[PFCS_MAX_PEERS];
+};
+
+// Table of the local blocked layout: slab g of `out` at nlines * zoff_g.
+inline PeerTable local_table(double2* out, long long nlines, int G, int base, int extra) {
+  PeerTable t{};
+  long long off = 0;
+  for (int g = 0; g < G && g < PFCS_MAX_PEERS; ++g) {
+    t.p[g] = out + nlines * off;
+    off += base + (g < extra ? 1 : 0);
+  }
+  return t;
+}
 
 }  // namespace pfcs

@@ -99,5 +99,10 @@ int launch_strided_blocked(const double2* in, double2* out, long long outer, int
                            int g_out, bool forward, cudaStream_t st);
 int launch_dft(const double2* in, double2* out, long long outer, int n, long long inner,
                bool forward, cudaStream_t st);
+struct PeerTable;
+int launch_lines_to(const double2* in, double2* out, long long nlines, int n, int g_in, int g_out,
+                    const PeerTable* dst, bool forward, cudaStream_t st);
+int launch_strided_to(const double2* in, long long outer, int n, long long inner, int g_in,
+                      const PeerTable* dst, int g_outer, bool forward, cudaStream_t st);
 
 }  // namespace pfcs

@@ -57,7 +57,7 @@ __global__ void __launch_bounds__(T*(N / radix_R(N)), min_blocks(T*(N / radix_R(
     k_pfc_z(const double2* nl, double2* psi_hat, double2* next, i64 nlines, int ny, SlabSplit sin,
             SlabSplit sout, const double* __restrict__ kx, const double* __restrict__ ky,
             const double* __restrict__ kz, PfcSym p, const double2* __restrict__ tw, double scale,
-            double* diag) {
+            double* diag, PeerTable tnext) {
   constexpr int R = radix_R(N);
   constexpr int P = N / R;
   constexpr int LS = tile_ls(N, T, false);
@@ -114,15 +114,14 @@ __global__ void __launch_bounds__(T*(N / radix_R(N)), min_blocks(T*(N / radix_R(
 #pragma unroll
         for (int e = 0; e < R; ++e) {
           const int z = j + P * e;
-          i64 a;
-          if (BOUT) {
-            int zoff, cz;
-            sout.locate(z, zoff, cz);
-            a = nlines * zoff + l * cz + (z - zoff);
+          const double2 x = make_double2(r.v[e].x * scale, r.v[e].y * scale);
+          if (BOUT) {  // z block h -> tnext.p[h]: local send slab or rank h's receive buffer
+            int h, zoff, cz;
+            sout.locate3(z, h, zoff, cz);
+            tnext.p[h][l * cz + (z - zoff)] = x;
           } else {
-            a = l * N + z;
+            next[l * N + z] = x;
           }
-          next[a] = make_double2(r.v[e].x * scale, r.v[e].y * scale);
         }
       }
     }
@@ -134,13 +133,16 @@ __global__ void __launch_bounds__(T*(N / radix_R(N)), min_blocks(T*(N / radix_R(
 template <int N>
 static int pfc_z_n(const double2* nl, double2* psi_hat, double2* next, i64 cx, i64 ny,
                    SlabSplitH si, SlabSplitH so, const double* kx, const double* ky,
-                   const double* kz, double eps, double dt, double* diag, cudaStream_t st) {
+                   const double* kz, double eps, double dt, double* diag, const PeerTable* dst,
+                   cudaStream_t st) {
   const double2* tw = twiddles(N);
   if (!tw) return PFCS_E_CUDA;
   const i64 nlines = cx * ny;
   SlabSplit a{si.G, si.base, si.extra}, b{so.G, so.base, so.extra};
   PfcSym p{eps, dt};
-  const bool bin = si.G > 1, bout = so.G > 1, nx = next != nullptr;
+  if (so.G > PFCS_MAX_PEERS) return fail(PFCS_E_UNSUPPORTED, "more than 16 slabs");
+  const bool bin = si.G > 1, bout = so.G > 1 || dst != nullptr, nx = next != nullptr || dst != nullptr;
+  const PeerTable tab = dst ? *dst : local_table(next, nlines, so.G, so.base, so.extra);
   const double scale = 1.0 / (double)N;
   return with_variant<KIND_PFCZ, N>([&](auto var) -> int {
     constexpr int V = decltype(var)::value;
@@ -159,7 +161,7 @@ static int pfc_z_n(const double2* nl, double2* psi_hat, double2* next, i64 cx, i
     if (int rc = persistent_grid((const void*)PFCS_ZK(BI, BO, NX), T * P, smem, ntiles, &grid))   \
       return rc;                                                                                  \
     PFCS_ZK(BI, BO, NX)<<<grid, T * P, smem, st>>>(nl, psi_hat, next, nlines, (int)ny, a, b, kx, \
-                                                   ky, kz, p, tw, scale, diag);                   \
+                                                   ky, kz, p, tw, scale, diag, tab);              \
   } while (0)
       if (!nx) {
         if (bin) PFCS_ZL(true, false, false);
@@ -177,7 +179,8 @@ static int pfc_z_n(const double2* nl, double2* psi_hat, double2* next, i64 cx, i
 
 int launch_pfc_z(const double2* nl, double2* psi_hat, double2* next, long long cx, long long ny,
                  long long nz, int g_in, int g_out, const double* kx, const double* ky,
-                 const double* kz, double eps, double dt, double* diag, cudaStream_t st) {
+                 const double* kz, double eps, double dt, double* diag, cudaStream_t st,
+                 const PeerTable* dst) {
   if (cx * ny <= 0) return PFCS_OK;
   if (!is_pow2(nz) || nz < 2 || nz > 4096)
     return fail(PFCS_E_UNSUPPORTED, "fused z update needs a power-of-two nz in [2, 4096]");
@@ -185,7 +188,7 @@ int launch_pfc_z(const double2* nl, double2* psi_hat, double2* next, long long c
   switch (nz) {
 #define PFCS_CASE(NN) \
   case NN:            \
-    return pfc_z_n<NN>(nl, psi_hat, next, cx, ny, si, so, kx, ky, kz, eps, dt, diag, st);
+    return pfc_z_n<NN>(nl, psi_hat, next, cx, ny, si, so, kx, ky, kz, eps, dt, diag, dst, st);
     PFCS_CASE(2) PFCS_CASE(4) PFCS_CASE(8) PFCS_CASE(16) PFCS_CASE(32) PFCS_CASE(64)
     PFCS_CASE(128) PFCS_CASE(256) PFCS_CASE(512) PFCS_CASE(1024) PFCS_CASE(2048) PFCS_CASE(4096)
 #undef PFCS_CASE

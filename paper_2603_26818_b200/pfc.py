@@ -116,6 +116,18 @@ def _pow2(n: int) -> bool:
     return n >= 2 and (n & (n - 1)) == 0
 
 
+def exchange_mode() -> str:
+    """'peer' (default): transposes fused into the FFT epilogues, stores to
+    peer-mapped receive buffers; 'collective': separate all-to-all
+    (NCCL all_to_all_single / device copies).  PFCS_EXCHANGE overrides."""
+    import os
+
+    mode = os.environ.get("PFCS_EXCHANGE", "peer").lower()
+    if mode not in ("peer", "collective"):
+        raise ValueError(f"PFCS_EXCHANGE must be 'peer' or 'collective', got {mode!r}")
+    return mode
+
+
 class _StepEngine:
     """Workspaces and launch sequence of one rank's PFC step."""
 
@@ -135,9 +147,12 @@ class _StepEngine:
             (self.real and _pow2(nx3) and 4 <= nx3 <= 8192) or
             (not self.real and _pow2(nx3) and nx3 <= 4096))
         cdt = torch.complex128
+        self.peer = False
         if self.G == 1:
             self.work = torch.empty(max(g.zslab_elems, 1), dtype=cdt, device=self.device)
             self.send = self.recv_z = self.recv_x = self.work
+        elif self.fused and g.ny > 1 and exchange_mode() == "peer":
+            self._setup_peer()
         else:
             self.send = torch.empty(max(g.xslab_elems, 1), dtype=cdt, device=self.device)
             self.recv_z = torch.empty(max(g.zslab_elems, 1), dtype=cdt, device=self.device)
@@ -145,6 +160,27 @@ class _StepEngine:
         self.diag = torch.zeros(nat.DIAG_SLOTS * nat.DIAG_VALS, dtype=torch.float64, device=self.device)
         self.kvec = None
         self.prepared_for = None  # (id(tensor), version) the send buffer was built from
+
+    def _setup_peer(self) -> None:
+        """Fused exchanges: the receive buffers are mapped on every rank and
+        the kernels before each transpose store into them directly (collective:
+        all ranks build their engine in the same step)."""
+        from . import peer
+
+        g, G, me = self.g, self.G, self.rank
+        self._bz = peer.DeviceBuffer(g.zslab_elems, device=self.device)
+        self._bx = peer.DeviceBuffer(g.xslab_elems, device=self.device)
+        mz = peer.map_peers(self.worker, self._bz)
+        mx = peer.map_peers(self.worker, self._bx)
+        self._maps = (mz, mx)
+        self.recv_z, self.recv_x = self._bz.tensor, self._bx.tensor
+        self.send = None
+        zoff = [sum(g.cz_all[:h]) for h in range(G)]
+        # my z-inverse block for rank h lands at rows xoff..xoff+cx of its Z slab
+        self.tab_z = peer.Table([mz.addrs[h] + 16 * g.xoff * g.ny * g.cz_all[h] for h in range(G)])
+        # my y-forward rows for rank h land in its blocked-z buffer, block `me`
+        self.tab_x = peer.Table([mx.addrs[h] + 16 * g.cx_all[h] * g.ny * zoff[me] for h in range(G)])
+        self.peer = True
 
     def _sym_ptrs(self, sym):
         if self.kvec is None or self.kvec[0] is not sym:
@@ -168,7 +204,23 @@ class _StepEngine:
         key = (psi.data_ptr(), state.psi_hat._version)
         nlines = g.cx * g.ny
         eps, dt = float(state.symbols.eps), float(params.dt)
-        if self.fused:
+        if self.peer:
+            # fused exchanges: K_z and K_y store straight into the owners'
+            # receive buffers (NVLink peer / IPC), a fence orders each transpose
+            from .peer import fence
+
+            if self.prepared_for != key:
+                nat.call("pfcs_fft_zlines_to", nat.ptr(psi), self.tab_z.ptr, nlines, g.nz, 1, self.G, 0, st)
+                fence(self.worker)
+            z = self.recv_z
+            nat.call("pfcs_fft_axis_c2c", nat.ptr(z), nat.ptr(z), g.nxm, g.ny, g.cz, 1, 0, st)
+            nat.call("pfcs_pfc_cube_x", nat.ptr(z), g.nx, g.ny * g.cz, 1 if self.real else 0, dptr, st)
+            nat.call("pfcs_fft_lines_scatter", nat.ptr(z), self.tab_x.ptr, g.nxm, g.ny, g.cz, 1, self.G, 1, st)
+            fence(self.worker)
+            nat.call("pfcs_pfc_update_z_to", nat.ptr(self.recv_x), nat.ptr(psi), self.tab_z.ptr, g.cx, g.ny,
+                     g.nz, self.G, self.G, kx, ky, kz, eps, dt, dptr, st)
+            fence(self.worker)
+        elif self.fused:
             if self.prepared_for != key:
                 nat.call("pfcs_fft_zlines", nat.ptr(psi), nat.ptr(self.send), nlines, g.nz, 1, self.G, 0, st)
             if self.G > 1:
