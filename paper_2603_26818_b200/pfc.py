@@ -271,6 +271,8 @@ def slab_kvectors(grid: GridSpec, sym: SymbolTable, g: _Geometry, device):
         kx_np = wavenumbers(grid, 0)[: g.nxm][g.xoff: g.xoff + g.cx]
     else:
         kx_np = sym.kvec[0]
+        if kx_np.shape[0] == g.nx and g.cx != g.nx:  # full-grid table: take this rank's rows
+            kx_np = kx_np[g.xoff: g.xoff + g.cx]
         if kx_np.shape[0] != g.cx:
             raise ValueError(f"symbol table has {kx_np.shape[0]} x modes, slab has {g.cx}")
     ky_np, kz_np = sym.kvec[1], sym.kvec[2]
