@@ -289,6 +289,42 @@ def _ensure(field: DistField, layout: Layout, space: Space) -> None:
                          f"got {field.layout.name}/{field.space.name}")
 
 
+class _PeerPlan:
+    """Receive buffers of one (grid, G, real) slab pipeline mapped on every
+    rank, for the fused exchanges (see peer.py)."""
+
+    def __init__(self, worker, g: "_Geometry"):
+        from . import peer
+
+        self.bz = peer.DeviceBuffer(g.zslab_elems)
+        self.bx = peer.DeviceBuffer(g.xslab_elems)
+        mz = peer.map_peers(worker, self.bz)
+        mx = peer.map_peers(worker, self.bx)
+        self.maps = (mz, mx)
+        zoff = [sum(g.cz_all[:h]) for h in range(g.G)]
+        self.tab_z = peer.Table([mz.addrs[h] + 16 * g.xoff * g.ny * g.cz_all[h] for h in range(g.G)])
+        self.tab_x = peer.Table([mx.addrs[h] + 16 * g.cx_all[h] * g.ny * zoff[g.rank] for h in range(g.G)])
+
+
+def _pow2(n: int) -> bool:
+    return n >= 2 and (n & (n - 1)) == 0
+
+
+def _peer_plan(worker, g: "_Geometry"):
+    """Fused-exchange plan for this pipeline, or None (collective path):
+    needs G > 1, a y axis to carry the forward scatter and power-of-two
+    y/z lines (PFCS_EXCHANGE=collective disables it)."""
+    from .pfc import exchange_mode
+
+    if g.G == 1 or g.ny < 2 or not (_pow2(g.ny) and _pow2(g.nz)) or exchange_mode() != "peer":
+        return None
+    plans = worker.__dict__.setdefault("_pfcs_plans", {})
+    key = (g.nx, g.ny, g.nz, g.real)
+    if key not in plans:
+        plans[key] = _PeerPlan(worker, g)
+    return plans[key]
+
+
 def _forward_core(src: torch.Tensor, worker, g: _Geometry) -> torch.Tensor:
     """Physical Z slab (flat) -> spectral X slab (flat, plain layout)."""
     dev = src.device
@@ -297,6 +333,18 @@ def _forward_core(src: torch.Tensor, worker, g: _Geometry) -> torch.Tensor:
         nat.call("pfcs_rfft_x", nat.ptr(src), nat.ptr(a), g.nx, g.ny * g.cz, _stream())
     else:
         _fft_x(src, g, True, a)
+    plan = _peer_plan(worker, g)
+    if plan is not None:
+        # y lines stored straight into the owners' blocked-z receive buffers
+        from .peer import fence
+
+        fence(worker)  # every rank is done reading its buffer from the last call
+        nat.call("pfcs_fft_lines_scatter", nat.ptr(a), plan.tab_x.ptr, g.nxm, g.ny, g.cz, 1, g.G, 1, _stream())
+        fence(worker)
+        out = torch.empty(g.xslab_elems, dtype=torch.complex128, device=dev)
+        nat.call("pfcs_fft_zlines", nat.ptr(plan.bx.tensor), nat.ptr(out), g.cx * g.ny, g.nz, g.G, 1, 1,
+                 _stream())
+        return out
     _fft_y(a, g, True)
     if g.G == 1:
         nat.call("pfcs_fft_zlines", nat.ptr(a), nat.ptr(a), g.cx * g.ny, g.nz, 1, 1, 1, _stream())
@@ -312,6 +360,23 @@ def _forward_core(src: torch.Tensor, worker, g: _Geometry) -> torch.Tensor:
 def _inverse_core(src: torch.Tensor, worker, g: _Geometry) -> torch.Tensor:
     """Spectral X slab (flat, plain) -> physical Z slab (flat)."""
     dev = src.device
+    plan = _peer_plan(worker, g)
+    if plan is not None:
+        # z lines stored straight into the owners' Z-slab receive buffers
+        from .peer import fence
+
+        fence(worker)
+        nat.call("pfcs_fft_zlines_to", nat.ptr(src), plan.tab_z.ptr, g.cx * g.ny, g.nz, 1, g.G, 0, _stream())
+        fence(worker)
+        z = plan.bz.tensor[:g.zslab_elems]
+        _fft_y(z, g, False)
+        if g.real:
+            out = torch.empty(g.nx * g.ny * g.cz, dtype=torch.float64, device=dev)
+            nat.call("pfcs_irfft_x", nat.ptr(z), nat.ptr(out), g.nx, g.ny * g.cz, _stream())
+            return out
+        out = torch.empty(g.zslab_elems, dtype=torch.complex128, device=dev)
+        _fft_x(z, g, False, out)
+        return out
     send = torch.empty(g.xslab_elems, dtype=torch.complex128, device=dev)
     nat.call("pfcs_fft_zlines", nat.ptr(src), nat.ptr(send), g.cx * g.ny, g.nz, 1, g.G, 0, _stream())
     if g.G == 1:
