@@ -318,6 +318,8 @@ def _peer_plan(worker, g: "_Geometry"):
 
     if g.G == 1 or g.ny < 2 or not (_pow2(g.ny) and _pow2(g.nz)) or exchange_mode() != "peer":
         return None
+    if min(g.cz_all) < 2:  # the y-line scatter tiles need >= 2 contiguous z columns
+        return None
     plans = worker.__dict__.setdefault("_pfcs_plans", {})
     key = (g.nx, g.ny, g.nz, g.real)
     if key not in plans:
