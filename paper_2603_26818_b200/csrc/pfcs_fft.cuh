@@ -70,6 +70,19 @@ __device__ __forceinline__ double2 mul_j(double2 a) {
   return FWD ? make_double2(a.y, -a.x) : make_double2(-a.y, a.x);
 }
 
+// Twiddle load through the read-only path, as volatile asm so the compiler
+// keeps it inside its pass instead of hoisting every pass's twiddles to the
+// top of the kernel (which costs ~30 live registers in the fused passes).
+__device__ __forceinline__ double2 ldg_tw(const double2* p) {
+#ifdef PFCS_TW_HOIST
+  return __ldg(p);
+#else
+  double2 w;
+  asm volatile("ld.global.nc.v2.f64 {%0, %1}, [%2];" : "=d"(w.x), "=d"(w.y) : "l"(p));
+  return w;
+#endif
+}
+
 template <bool FWD>
 __device__ __forceinline__ void dft2(double2& a, double2& b) {
   double2 t = a;
@@ -151,11 +164,11 @@ __device__ __forceinline__ void fft_pass(double2 (&v)[radix_R(N)], int j, double
       // (7 loads -> 3 lifted z-line kernels from 4.3 to 5.9 TB/s on B200)
       const int t1 = TWS * k * (N / (Ns * r));
       double2 w[r];
-      w[1] = __ldg(&tw[t1]);
-      if constexpr (r >= 4) w[2] = (TWL >= 3) ? __ldg(&tw[2 * t1]) : cmul(w[1], w[1]);
+      w[1] = ldg_tw(&tw[t1]);
+      if constexpr (r >= 4) w[2] = (TWL >= 3) ? ldg_tw(&tw[2 * t1]) : cmul(w[1], w[1]);
       if constexpr (r == 4) w[3] = cmul(w[1], w[2]);
       if constexpr (r == 8) {
-        w[4] = (TWL >= 3) ? __ldg(&tw[4 * t1]) : cmul(w[2], w[2]);
+        w[4] = (TWL >= 3) ? ldg_tw(&tw[4 * t1]) : cmul(w[2], w[2]);
         w[3] = cmul(w[1], w[2]);
         w[5] = cmul(w[1], w[4]);
         w[6] = cmul(w[2], w[4]);
