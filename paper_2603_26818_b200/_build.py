@@ -84,15 +84,22 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     return LIB
 
 
-def build_variant(name: str, defines: list[str]) -> Path:
+def build_variant(name: str, defines: list[str], only: list[str] | None = None,
+                  reuse: Path | None = None) -> Path:
     """Experimental build with extra -D flags into libpfcs_<name>.so (for A/B
-    timing on the GPU via PFCS_LIB_PATH); not used by the product."""
+    timing on the GPU via PFCS_LIB_PATH); not used by the product.  With
+    `only` (source stems), the other objects are reused from the main build
+    (or from the object directory `reuse`)."""
     nvcc = _nvcc()
+    build()
     bdir = ROOT / "build" / name
     bdir.mkdir(parents=True, exist_ok=True)
     flags = [f for f in NVCC_FLAGS if f not in ("-v", "-Xptxas")] + [f"-D{d}" for d in defines]
     procs, objs = [], []
     for src in _sources():
+        if only is not None and src.stem not in only:
+            objs.append(str((reuse or BUILD) / (src.stem + ".o")))
+            continue
         obj = bdir / (src.stem + ".o")
         procs.append(subprocess.Popen([nvcc, *ARCH, *flags, "-I", str(INCLUDE), "-c", str(src), "-o", str(obj)]))
         objs.append(str(obj))

@@ -59,11 +59,12 @@ __global__ void __launch_bounds__(T*(N / radix_R(N)), min_blocks(T*(N / radix_R(
   };
   auto comp = [&](i64 tile, Regs1<R>& r) {
     const i64 l = tile * T + t;
-    fft_line<N, FWD>(r.v, j, sl, tw);
+    const int jj = opaque(j);
+    fft_line<N, FWD>(r.v, jj, sl, tw);
     if (l < nlines) {
 #pragma unroll
       for (int e = 0; e < R; ++e) {
-        const int z = j + P * e;
+        const int z = jj + P * e;
         double2 x = r.v[e];
         if (!FWD) x = make_double2(x.x * scale, x.y * scale);
         if (BOUT) {  // block h of z -> tout.p[h] (local send slab or the peer's buffer)
@@ -121,7 +122,8 @@ __global__ void __launch_bounds__(T*(N / radix_R(N)), min_blocks(T*(N / radix_R(
   auto comp = [&](i64 tile, Regs1<R>& r) {
     const i64 o = tile / tpo;
     const i64 i = (tile - o * tpo) * T + t;
-    fft_line<N, FWD>(r.v, j, sl, tw);
+    const int jj = opaque(j);
+    fft_line<N, FWD>(r.v, jj, sl, tw);
     if (i < inner) {
       double2* dst = out;
       i64 orow = o;
@@ -135,7 +137,7 @@ __global__ void __launch_bounds__(T*(N / radix_R(N)), min_blocks(T*(N / radix_R(
       for (int e = 0; e < R; ++e) {
         double2 x = r.v[e];
         if (!FWD) x = make_double2(x.x * scale, x.y * scale);
-        dst[line_addr<BOUT>(orow, j + P * e, i, N, outer, inner, sout)] = x;
+        dst[line_addr<BOUT>(orow, jj + P * e, i, N, outer, inner, sout)] = x;
       }
     }
   };

@@ -70,6 +70,24 @@ __device__ __forceinline__ double2 mul_j(double2 a) {
   return FWD ? make_double2(a.y, -a.x) : make_double2(-a.y, a.x);
 }
 
+// Opaque copy of an index: the compiler must assume it changes here, so the
+// (thread-index-only) address arithmetic of the exchanges is recomputed
+// where it is used instead of being hoisted out of the persistent tile loop
+// or above the previous FFT of a fused pass, where it pinned ~60 registers
+// (the fused cube pass went from 128 registers + spills to 64 without).
+__device__ __forceinline__ int opaque(int x) {
+  asm volatile("" : "+r"(x));
+  return x;
+}
+// threadIdx.x read that cannot be hoisted (recomputing a tile's thread
+// coordinates per tile keeps the whole index/pointer family loop-local)
+// (unsigned, so tid % T and tid / T stay single AND/shift instructions)
+__device__ __forceinline__ unsigned opaque_tid() {
+  unsigned t;
+  asm volatile("mov.u32 %0, %%tid.x;" : "=r"(t));
+  return t;
+}
+
 // Twiddle load through the read-only path, as volatile asm so the compiler
 // keeps it inside its pass instead of hoisting every pass's twiddles to the
 // top of the kernel (which costs ~30 live registers in the fused passes).
@@ -142,13 +160,14 @@ __device__ __forceinline__ void dft_r(double2 (&y)[r]) {
 // j + P*e of this pass's input; on exit of the last pass v[e] holds output
 // element j + P*e.  `tw` is the size-N table exp(-2 pi i m / N), m < N,
 // read with stride TWS (so a size-2N table serves an N-point transform).
-template <int N, int Ns, bool FWD, int TWS, int TWL = PFCS_TW_LOADS>
-__device__ __forceinline__ void fft_pass(double2 (&v)[radix_R(N)], int j, double2* sl,
+template <int N, int Ns, bool FWD, int TWS, int TWL = PFCS_TW_LOADS, int R = radix_R(N)>
+__device__ __forceinline__ void fft_pass(double2 (&v)[R], int j, double2* sl,
                                          const double2* __restrict__ tw) {
-  constexpr int R = radix_R(N);
+  // R = values per thread (8, or 4 for the register-heavy fused passes);
+  // each pass uses radix min(R, remaining) and R/r butterflies per thread
   constexpr int P = N / R;
   constexpr int rem = N / Ns;
-  constexpr int r = (R < 8) ? R : (rem >= 8 ? 8 : rem);
+  constexpr int r = (rem >= R) ? R : rem;
   constexpr int S = R / r;
 #pragma unroll
   for (int s = 0; s < S; ++s) {
@@ -194,22 +213,21 @@ __device__ __forceinline__ void fft_pass(double2 (&v)[radix_R(N)], int j, double
     __syncthreads();
 #pragma unroll
     for (int e = 0; e < R; ++e) v[e] = sl[pad_idx(j + P * e)];
-    fft_pass<N, Ns * r, FWD, TWS, TWL>(v, j, sl, tw);
+    fft_pass<N, Ns * r, FWD, TWS, TWL, R>(v, j, sl, tw);
   }
 }
 
 // Full N-point transform of the register set (see fft_pass).  All threads of
 // the CTA must call it (it contains __syncthreads when N > 8).
-template <int N, bool FWD, int TWS = 1, int TWL = PFCS_TW_LOADS>
-__device__ __forceinline__ void fft_line(double2 (&v)[radix_R(N)], int j, double2* sl,
+template <int N, bool FWD, int TWS = 1, int TWL = PFCS_TW_LOADS, int R = radix_R(N)>
+__device__ __forceinline__ void fft_line(double2 (&v)[R], int j, double2* sl,
                                          const double2* __restrict__ tw) {
-  fft_pass<N, 1, FWD, TWS, TWL>(v, j, sl, tw);
+  fft_pass<N, 1, FWD, TWS, TWL, R>(v, j, sl, tw);
 }
 
 // Stash register set (element j + P*e in v[e]) into the padded smem line.
-template <int N>
-__device__ __forceinline__ void stash_line(const double2 (&v)[radix_R(N)], int j, double2* sl) {
-  constexpr int R = radix_R(N);
+template <int N, int R = radix_R(N)>
+__device__ __forceinline__ void stash_line(const double2 (&v)[R], int j, double2* sl) {
   constexpr int P = N / R;
 #pragma unroll
   for (int e = 0; e < R; ++e) sl[pad_idx(j + P * e)] = v[e];

@@ -49,10 +49,10 @@ enum { KIND_LINES = 0, KIND_STRIDED = 1, KIND_REALX = 2, KIND_CUBEC = 3, KIND_PF
 // passes want >= 128-byte row segments (T*16 B) even at one CTA per SM.
 constexpr int default_variant(int kind, int n) {
   // n: transform length (REALX / CUBER: the half length M)
-  return kind == KIND_LINES   ? (n <= 256 ? 5 : 4)
+  return kind == KIND_LINES   ? (n <= 256 ? 5 : (n == 512 ? 4 : 0))
        : kind == KIND_STRIDED ? (n <= 512 ? 3 : (n == 1024 ? 6 : (n == 2048 ? 5 : 4)))
-       : kind == KIND_REALX   ? (n <= 512 ? 7 : (n == 1024 ? 6 : (n == 2048 ? 5 : 4)))
-       : kind == KIND_CUBER   ? (n <= 512 ? 3 : (n == 1024 ? 2 : (n == 2048 ? 1 : 0)))
+       : kind == KIND_REALX   ? (n == 256 ? 3 : (n <= 512 ? 7 : (n == 1024 ? 6 : (n == 2048 ? 5 : 4))))
+       : kind == KIND_CUBER   ? (n <= 256 ? 3 : (n == 512 ? 7 : (n == 1024 ? 2 : (n == 2048 ? 1 : 0))))
        : kind == KIND_CUBEC   ? (n <= 512 ? 3 : (n == 1024 ? 2 : (n == 2048 ? 1 : 0)))
        : /* KIND_PFCZ */        (n <= 256 ? 1 : 0);
 }

@@ -47,19 +47,57 @@ __device__ __forceinline__ double2 w16(int e) {
   }
 }
 
+// W_N^k for k = j + P e with N = 2M = 2 R P: W_N^j * W_{2R}^e = W_N^j * W_16^{e 8/R}
 template <int R>
 __device__ __forceinline__ double2 twiddle_k(const double2* __restrict__ twN, double2 wj, int j, int e, int P) {
-  if constexpr (R == 8) {
-    return cmul(wj, w16(e));
+  if constexpr (R == 8 || R == 4) {
+    return cmul(wj, w16(e * (8 / R)));
   } else {
     return __ldg(&twN[j + P * e]);
   }
 }
 
-template <int R>
+// values per thread of the fused cube pass (A/B experiments: -DPFCS_CUBE_R,
+// -DPFCS_CUBE_TARGET = resident threads per SM the register cap aims for)
+#ifndef PFCS_CUBE_R
+#define PFCS_CUBE_R 8
+#endif
+#ifndef PFCS_CUBE_TARGET
+#define PFCS_CUBE_TARGET 768
+#endif
+__host__ __device__ constexpr int real_R(int m, int mode) {
+  return (mode == 2 && m >= 64) ? PFCS_CUBE_R : radix_R(m);
+}
+
+// Mirrored pre-step: the C2R pre-twiddle pairs X_k with X_{M-k}.  With
+// MIRROR the tile load fetches both rows straight from global memory (the
+// mirror rows are the same tile's rows, so they hit L1/L2) instead of
+// exchanging them through shared memory, saving one smem round trip and one
+// CTA barrier per tile.
+// PFCS_MIRROR=2 issues the mirror loads at the start of the tile's compute
+// rather than with the (possibly prefetched) tile load: the rows were just
+// fetched by the partner threads, so they come from L1 and cost no registers
+// across the prefetch window.
+#ifndef PFCS_MIRROR
+#define PFCS_MIRROR 2
+#endif
+__host__ __device__ constexpr bool use_mirror(int mode) { return PFCS_MIRROR == 1 && mode == 2; }
+#ifndef PFCS_MIRROR_C2R
+#define PFCS_MIRROR_C2R 0
+#endif
+__host__ __device__ constexpr bool late_mirror(int mode) {
+  return PFCS_MIRROR == 2 && (mode == 2 || (PFCS_MIRROR_C2R && mode == 1));
+}
+
+template <int R, bool MIR>
 struct RegsX {
   double2 v[R];
   double2 xm;  // row M (half-spectrum Nyquist mode), used by thread j == 0
+};
+template <int R>
+struct RegsX<R, true> {
+  double2 v[R];
+  double2 w[R];  // X_{M-k} for k = j + P e (row M for k = 0)
 };
 
 // Extra +8 keeps row M (index PAD(M)) inside the line when the bank rule
@@ -69,13 +107,15 @@ __host__ __device__ constexpr int real_ls(int m, int t) {
 }
 
 template <int M, int T, int ST, int MODE>
-__global__ void __launch_bounds__(T*(M / radix_R(M)),
-                                  min_blocks(T*(M / radix_R(M)), MODE == 2 ? 512 : (ST == 2 ? 640 : 768)))
+__global__ void __launch_bounds__(T*(M / real_R(M, MODE)),
+                                  min_blocks(T*(M / real_R(M, MODE)), MODE == 2 ? PFCS_CUBE_TARGET : (ST == 2 ? 640 : 768)))
     k_real_x(const void* in_, void* out_, i64 inner, const double2* __restrict__ twN, double scale,
              double* diag) {
-  constexpr int R = radix_R(M);
+  constexpr int R = real_R(M, MODE);
   constexpr int P = M / R;
   constexpr int LS = real_ls(M, T);
+  constexpr bool MIR = use_mirror(MODE);
+  constexpr bool LMIR = late_mirror(MODE);
   extern __shared__ double2 smem[];
   const int tid = threadIdx.x;
   const int t = tid % T;
@@ -84,7 +124,7 @@ __global__ void __launch_bounds__(T*(M / radix_R(M)),
   const i64 ntiles = (inner + T - 1) / T;
   double m_abs = 0.0;
 
-  auto load = [&](i64 tile, RegsX<R>& r) {
+  auto load = [&](i64 tile, RegsX<R, MIR>& r) {
     const i64 i = tile * T + t;
     const bool ok = i < inner;
     if (MODE == MODE_R2C) {
@@ -102,26 +142,56 @@ __global__ void __launch_bounds__(T*(M / radix_R(M)),
         const i64 k = j + P * e;
         r.v[e] = ok ? in[k * inner + i] : make_double2(0.0, 0.0);
       }
-      r.xm = (ok && j == 0) ? in[(i64)M * inner + i] : make_double2(0.0, 0.0);
+      if constexpr (MIR) {
+#pragma unroll
+        for (int e = 0; e < R; ++e) {
+          const i64 km = M - (j + P * e);  // in [1, M]
+          r.w[e] = ok ? in[km * inner + i] : make_double2(0.0, 0.0);
+        }
+      } else {
+        r.xm = (ok && j == 0) ? in[(i64)M * inner + i] : make_double2(0.0, 0.0);
+      }
     }
   };
 
-  auto comp = [&](i64 tile, RegsX<R>& r) {
+  auto comp = [&](i64 tile, RegsX<R, MIR>& r) {
+    const unsigned tid_ = opaque_tid();
+    const int t = tid_ % T;
+    const int jj = tid_ / T;
+    double2* sl = smem + t * LS;
     const i64 i = tile * T + t;
     const bool ok = i < inner;
     double2* v = r.v;
     if (MODE != MODE_R2C) {
       // Z'[k] = (X_k + conj X_{M-k}) + i W_N^{-k} (X_k - conj X_{M-k});
       // Im X_0 and Im X_M are ignored (numpy irfft convention)
-      stash_line<M>(r.v, j, sl);
-      if (j == 0) sl[pad_idx(M)] = r.xm;
-      const double2 wj = __ldg(&twN[j]);
-      __syncthreads();
+      double2 wl[LMIR ? R : 1];
+      if constexpr (LMIR) {
+        const double2* in = (const double2*)in_;
+#pragma unroll
+        for (int e = 0; e < R; ++e) {
+          const i64 km = M - (jj + P * e);  // in [1, M]
+          wl[e] = ok ? in[km * inner + i] : make_double2(0.0, 0.0);
+        }
+      }
+      if constexpr (!MIR && !LMIR) {
+        stash_line<M, R>(r.v, jj, sl);
+        if (jj == 0) sl[pad_idx(M)] = r.xm;
+        __syncthreads();
+      }
+      const double2 wj = __ldg(&twN[jj]);
 #pragma unroll
       for (int e = 0; e < R; ++e) {
-        const int k = j + P * e;
+        const int k = jj + P * e;
         double2 a = v[e];
-        double2 bm = sl[pad_idx(M - k)];
+        double2 bm;
+        if constexpr (MIR) {
+          bm = r.w[e];
+        } else if constexpr (LMIR) {
+          bm = wl[e];
+        } else {
+          bm = sl[pad_idx(M - k)];
+        }
         if (k == 0) {
           a.y = 0.0;
           bm.y = 0.0;
@@ -129,11 +199,11 @@ __global__ void __launch_bounds__(T*(M / radix_R(M)),
         const double2 b = make_double2(bm.x, -bm.y);
         const double2 s = cadd(a, b);
         const double2 d = csub(a, b);
-        const double2 w = twiddle_k<R>(twN, wj, j, e, P);
+        const double2 w = twiddle_k<R>(twN, wj, jj, e, P);
         const double2 wd = make_double2(fma(d.x, w.x, d.y * w.y), fma(d.y, w.x, -d.x * w.y));
         v[e] = make_double2(s.x - wd.y, s.y + wd.x);
       }
-      fft_line<M, false, 2>(r.v, j, sl, twN);
+      fft_line<M, false, 2, PFCS_TW_LOADS, R>(r.v, jj, sl, twN);
 #pragma unroll
       for (int e = 0; e < R; ++e) v[e] = make_double2(v[e].x * scale, v[e].y * scale);
     }
@@ -143,7 +213,7 @@ __global__ void __launch_bounds__(T*(M / radix_R(M)),
         double* out = (double*)out_;
 #pragma unroll
         for (int e = 0; e < R; ++e) {
-          const i64 m = j + P * e;
+          const i64 m = jj + P * e;
           out[(2 * m) * inner + i] = v[e].x;
           out[(2 * m + 1) * inner + i] = v[e].y;
         }
@@ -162,15 +232,16 @@ __global__ void __launch_bounds__(T*(M / radix_R(M)),
     }
 
     // forward M-point FFT, then the R2C split
-    fft_line<M, true, 2>(r.v, j, sl, twN);
-    const double2 wj = __ldg(&twN[j]);
+    const int j2 = opaque(jj);  // keep the forward FFT's index math out of the inverse's live range
+    fft_line<M, true, 2, PFCS_TW_LOADS, R>(r.v, j2, sl, twN);
+    const double2 wj = __ldg(&twN[jj]);
     __syncthreads();
-    stash_line<M>(r.v, j, sl);
+    stash_line<M, R>(r.v, jj, sl);
     __syncthreads();
     double2* out = (double2*)out_;
 #pragma unroll
     for (int e = 0; e < R; ++e) {
-      const int k = j + P * e;
+      const int k = jj + P * e;
       const double2 zk = v[e];
       const double2 zm = sl[pad_idx((M - k) & (M - 1))];
       double2 x;
@@ -179,19 +250,19 @@ __global__ void __launch_bounds__(T*(M / radix_R(M)),
       } else {
         const double2 s = make_double2(zk.x + zm.x, zk.y - zm.y);  // Zk + conj Zm
         const double2 d = make_double2(zk.x - zm.x, zk.y + zm.y);  // Zk - conj Zm
-        const double2 w = twiddle_k<R>(twN, wj, j, e, P);
+        const double2 w = twiddle_k<R>(twN, wj, jj, e, P);
         const double2 wd = make_double2(fma(d.x, w.x, -d.y * w.y), fma(d.x, w.y, d.y * w.x));
         x = make_double2(0.5 * (s.x + wd.y), 0.5 * (s.y - wd.x));  // 1/2 (s - i wd)
       }
       if (ok) out[(i64)k * inner + i] = x;
     }
-    if (j == 0 && ok) {
+    if (jj == 0 && ok) {
       const double2 z0 = v[0];
       out[(i64)M * inner + i] = make_double2(z0.x - z0.y, 0.0);
     }
   };
 
-  reg_tile_loop<ST, RegsX<R>>(ntiles, load, comp);
+  reg_tile_loop<ST, RegsX<R, MIR>>(ntiles, load, comp);
   if (MODE == MODE_CUBE) diag_block_max(diag, m_abs, 0.0, m_abs);
 }
 
@@ -210,17 +281,21 @@ __global__ void __launch_bounds__(T*(N / radix_R(N)), min_blocks(T*(N / radix_R(
   double2* sl = smem + t * LS;
   const i64 ntiles = (inner + T - 1) / T;
   double m_re = 0.0, m_im = 0.0, m_abs = 0.0;
-  auto load = [&](i64 tile, RegsX<R>& r) {
+  auto load = [&](i64 tile, RegsX<R, false>& r) {
     const i64 i = tile * T + t;
     const bool ok = i < inner;
 #pragma unroll
     for (int e = 0; e < R; ++e) r.v[e] = ok ? data[(i64)(j + P * e) * inner + i] : make_double2(0.0, 0.0);
   };
-  auto comp = [&](i64 tile, RegsX<R>& r) {
+  auto comp = [&](i64 tile, RegsX<R, false>& r) {
+    const unsigned tid_ = opaque_tid();
+    const int t = tid_ % T;
+    const int jj = tid_ / T;
+    double2* sl = smem + t * LS;
     const i64 i = tile * T + t;
     const bool ok = i < inner;
     double2* v = r.v;
-    fft_line<N, false>(r.v, j, sl, tw);
+    fft_line<N, false>(r.v, jj, sl, tw);
 #pragma unroll
     for (int e = 0; e < R; ++e) {
       const double a = v[e].x * scale, b = v[e].y * scale;
@@ -235,13 +310,14 @@ __global__ void __launch_bounds__(T*(N / radix_R(N)), min_blocks(T*(N / radix_R(
       v[e] = make_double2(__dsub_rn(__dmul_rn(a, cr), __dmul_rn(b, ci)),
                           __dadd_rn(__dmul_rn(a, ci), __dmul_rn(b, cr)));
     }
-    fft_line<N, true>(r.v, j, sl, tw);
+    const int j2 = opaque(jj);
+    fft_line<N, true>(r.v, j2, sl, tw);
     if (ok) {
 #pragma unroll
-      for (int e = 0; e < R; ++e) data[(i64)(j + P * e) * inner + i] = v[e];
+      for (int e = 0; e < R; ++e) data[(i64)(j2 + P * e) * inner + i] = v[e];
     }
   };
-  reg_tile_loop<ST, RegsX<R>>(ntiles, load, comp);
+  reg_tile_loop<ST, RegsX<R, false>>(ntiles, load, comp);
   diag_block_max(diag, m_re, m_im, m_abs);
 }
 
@@ -253,9 +329,9 @@ static int real_x_m(const void* in, void* out, i64 inner, double* diag, cudaStre
   if (!twN) return PFCS_E_CUDA;
   return with_variant<MODE == MODE_CUBE ? KIND_CUBER : KIND_REALX, M>([&](auto var) -> int {
     constexpr int V = decltype(var)::value;
-    constexpr int T = TileCfg<M>::T_MIN << (V & 3);
+    constexpr int P = M / real_R(M, MODE);
+    constexpr int T = (P >= 32 ? 1 : 32 / P) << (V & 3);
     constexpr int ST = 1 + (V >> 2);
-    constexpr int P = TileCfg<M>::P;
     if constexpr (T * P > 1024) {
       return fail(PFCS_E_UNSUPPORTED, "tile too large");
     } else {

@@ -89,14 +89,15 @@ __global__ void __launch_bounds__(T*(N / radix_R(N)), min_blocks(T*(N / radix_R(
   auto comp = [&](i64 tile, RegsZ<R>& r) {
     const i64 l = tile * T + t;
     const bool ok = l < nlines;
-    fft_line<N, true, 1, 1>(r.v, j, sl, tw);
+    const int jj = opaque(j);
+    fft_line<N, true, 1, 1>(r.v, jj, sl, tw);
     const i64 lx = ok ? l / ny : 0;
     const int ly = ok ? (int)(l - lx * ny) : 0;
     const double kxx = __ldg(&kx[lx]);
     const double kyy = __ldg(&ky[ly]);
 #pragma unroll
     for (int e = 0; e < R; ++e) {
-      const int z = j + P * e;
+      const int z = jj + P * e;
       const double k2 = k2_of(kxx, kyy, __ldg(&kz[z]));
       double lap, rden;
       pfc_symbols(k2, p.eps, p.dt, lap, rden);
@@ -109,11 +110,12 @@ __global__ void __launch_bounds__(T*(N / radix_R(N)), min_blocks(T*(N / radix_R(
       r.v[e] = nw;
     }
     if (NEXT) {
-      fft_line<N, false, 1, 1>(r.v, j, sl, tw);
+      const int j2 = opaque(jj);
+      fft_line<N, false, 1, 1>(r.v, j2, sl, tw);
       if (ok) {
 #pragma unroll
         for (int e = 0; e < R; ++e) {
-          const int z = j + P * e;
+          const int z = j2 + P * e;
           const double2 x = make_double2(r.v[e].x * scale, r.v[e].y * scale);
           if (BOUT) {  // z block h -> tnext.p[h]: local send slab or rank h's receive buffer
             int h, zoff, cz;

@@ -1,0 +1,65 @@
+"""Launch one libpfcs pass kernel at a bench size, for `ncu --set full` captures.
+
+    python tools/prof_kernel.py <kind> [n] [reps]
+
+kind: cube_x | update_z | rfft_x | irfft_x | zlines | strided
+The kernel runs `reps` times (default 2: one warm launch + one to capture with
+`ncu -k regex:<kernel> -s 1 -c 1`).  Prints the CUDA-event time per launch
+(never a bench number when run under ncu).
+"""
+import os
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+
+
+def main():
+    kind = sys.argv[1]
+    n = int(sys.argv[2]) if len(sys.argv) > 2 else 1024
+    reps = int(sys.argv[3]) if len(sys.argv) > 3 else 2
+    import torch
+    from paper_2603_26818_b200 import _native as nat
+
+    torch.cuda.set_device(0)
+    st = nat.stream_ptr()
+    nh = n // 2 + 1
+    C = torch.complex128
+    a = torch.empty(nh * n * n, dtype=C, device="cuda")
+    a.real.normal_()
+    a.imag.normal_()
+    diag = torch.zeros(nat.DIAG_SLOTS * 4, dtype=torch.float64, device="cuda")
+    if kind == "cube_x":
+        fn = lambda: nat.call("pfcs_pfc_cube_x", nat.ptr(a), n, n * n, 1, nat.ptr(diag), st)
+    elif kind == "update_z":
+        psi = torch.empty_like(a)
+        psi.real.normal_()
+        kx = torch.linspace(0, 1, nh, dtype=torch.float64, device="cuda")
+        ky = torch.linspace(0, 1, n, dtype=torch.float64, device="cuda")
+        fn = lambda: nat.call("pfcs_pfc_update_z", nat.ptr(a), nat.ptr(psi), nat.ptr(a), nh, n, n, 1, 1,
+                              nat.ptr(kx), nat.ptr(ky), nat.ptr(ky), -0.3, 1e-9, nat.ptr(diag), st)
+    elif kind in ("rfft_x", "irfft_x"):
+        r = torch.randn(n * n * n, dtype=torch.float64, device="cuda")
+        if kind == "rfft_x":
+            fn = lambda: nat.call("pfcs_rfft_x", nat.ptr(r), nat.ptr(a), n, n * n, st)
+        else:
+            fn = lambda: nat.call("pfcs_irfft_x", nat.ptr(a), nat.ptr(r), n, n * n, st)
+    elif kind == "zlines":
+        fn = lambda: nat.call("pfcs_fft_zlines", nat.ptr(a), nat.ptr(a), nh * n, n, 1, 1, 1, st)
+    elif kind == "strided":
+        fn = lambda: nat.call("pfcs_fft_axis_c2c", nat.ptr(a), nat.ptr(a), nh, n, n, 1, 1, st)
+    else:
+        raise SystemExit(f"unknown kind {kind}")
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    for i in range(reps):
+        if i == reps - 1:
+            ev[0].record()
+        fn()
+    ev[1].record()
+    torch.cuda.synchronize()
+    print(kind, n, "last launch ms", round(ev[0].elapsed_time(ev[1]), 4), "variant env",
+          {k: v for k, v in os.environ.items() if k.startswith("PFCS_VARIANT")})
+
+
+if __name__ == "__main__":
+    main()

@@ -38,7 +38,14 @@ def main():
     if "--build" in sys.argv:
         build_tune()
         return
-    os.environ["PFCS_LIB_PATH"] = str(TUNE_LIB)
+    os.environ.setdefault("PFCS_LIB_PATH", str(TUNE_LIB))
+    kinds = None
+    sizes = (512, 1024)
+    for a in sys.argv[1:]:
+        if a.startswith("--kinds="):
+            kinds = {int(k) for k in a.split("=", 1)[1].split(",")}
+        if a.startswith("--sizes="):
+            sizes = tuple(int(k) for k in a.split("=", 1)[1].split(","))
     import torch
     from paper_2603_26818_b200 import _native as nat
 
@@ -61,6 +68,8 @@ def main():
     C = torch.complex128
 
     def sweep(kind, n, fn, nbytes):
+        if kinds is not None and kind not in kinds:
+            return
         row = {}
         for s in range(8):
             os.environ[f"PFCS_VARIANT_{kind}_{n}"] = str(s)
@@ -74,7 +83,7 @@ def main():
         results[f"{kind}_{n}"] = row
         print(kind, n, row, flush=True)
 
-    for n in (512, 1024):
+    for n in sizes:
         nh = n // 2 + 1
         # LINES (z pass, plain)
         a = torch.empty(nh * n * n, dtype=C, device="cuda")
@@ -88,6 +97,18 @@ def main():
         r = torch.randn(n * n * n, dtype=torch.float64, device="cuda")
         sweep(2, n // 2, lambda: nat.call("pfcs_rfft_x", nat.ptr(r), nat.ptr(a), n, n * n, st),
               8 * r.numel() + 16 * a.numel())
+        # C2R along x shares the REALX variant key; reported as kind 6
+        if kinds is None or 6 in kinds:
+            kinds_save = kinds
+            kinds = None
+            row_key = f"2_{n // 2}"
+            prev = results.pop(row_key, None)
+            sweep(2, n // 2, lambda: nat.call("pfcs_irfft_x", nat.ptr(a), nat.ptr(r), n, n * n, st),
+                  8 * r.numel() + 16 * a.numel())
+            results[f"6_{n // 2}"] = results.pop(row_key)
+            if prev is not None:
+                results[row_key] = prev
+            kinds = kinds_save
         del r
         diag = torch.zeros(nat.DIAG_SLOTS * 4, dtype=torch.float64, device="cuda")
         # fused cube pass (KIND_CUBER = 5, keyed by M)
@@ -103,7 +124,7 @@ def main():
               4 * 16 * a.numel())
         del a, psi
         torch.cuda.empty_cache()
-    print(json.dumps(results))
+    print(json.dumps({"lib": os.environ["PFCS_LIB_PATH"].rsplit("/", 1)[-1], "results": results}))
 
 
 if __name__ == "__main__":
