@@ -305,6 +305,10 @@ static int strided_n(const double2* in, double2* out, i64 outer, i64 inner, Slab
   if (!tw) return PFCS_E_CUDA;
   SlabSplit a{si.G, si.base, si.extra}, b{so.G, so.base, so.extra};
   const bool bin = si.G > 1, bout = so.G > 1;
+  if (!bin && !bout && inner > 1 && tma_enabled()) {
+    const int rc = launch_strided_tma(in, out, outer, N, inner, FWD, st);
+    if (rc != 1) return rc;
+  }
   return with_variant<KIND_STRIDED, N>([&](auto var) -> int {
     constexpr int V = decltype(var)::value;
     constexpr int T = TileCfg<N>::T_MIN << (V & 3);

@@ -28,6 +28,12 @@ inline int ilog2(long long n) {
   return l;
 }
 
+// TMA-staged strided pass (pfcs_tma.cu): default on, PFCS_TMA=0 disables; returns 1
+// when it does not apply to the call.
+bool tma_enabled();
+int launch_strided_tma(const double2* in, double2* out, long long outer, int n, long long inner, bool forward,
+                       cudaStream_t st);
+
 // Opt a kernel in to > 48 KB dynamic shared memory once.
 int ensure_smem(const void* func, size_t bytes);
 

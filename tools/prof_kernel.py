@@ -4,8 +4,8 @@
 
 kind: cube_x | update_z | rfft_x | irfft_x | zlines | strided
 The kernel runs `reps` times (default 2: one warm launch + one to capture with
-`ncu -k regex:<kernel> -s 1 -c 1`).  Prints the CUDA-event time per launch
-(never a bench number when run under ncu).
+`ncu -k regex:<kernel> -s 1 -c 1`).  Prints the average CUDA-event time of
+launches 2..reps (never a bench number when run under ncu).
 """
 import os
 import sys
@@ -51,14 +51,15 @@ def main():
     else:
         raise SystemExit(f"unknown kind {kind}")
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
-    for i in range(reps):
-        if i == reps - 1:
-            ev[0].record()
+    fn()
+    ev[0].record()
+    for i in range(reps - 1):
         fn()
     ev[1].record()
     torch.cuda.synchronize()
-    print(kind, n, "last launch ms", round(ev[0].elapsed_time(ev[1]), 4), "variant env",
-          {k: v for k, v in os.environ.items() if k.startswith("PFCS_VARIANT")})
+    ms = ev[0].elapsed_time(ev[1]) / max(reps - 1, 1)
+    print(kind, n, "avg launch ms", round(ms, 4), "env",
+          {k: v for k, v in os.environ.items() if k.startswith("PFCS_")})
 
 
 if __name__ == "__main__":
