@@ -1,6 +1,7 @@
 // pfcs_internal.h — host-side helpers shared by the libpfcs translation units.
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -31,6 +32,8 @@ inline int ilog2(long long n) {
 // TMA-staged strided pass (pfcs_tma.cu): default on, PFCS_TMA=0 disables; returns 1
 // when it does not apply to the call.
 bool tma_enabled();
+bool make_tmap(CUtensorMap* map, int rank, const void* base, const unsigned long long* dims,
+               const unsigned long long* strides_bytes, const unsigned* box);
 int launch_strided_tma(const double2* in, double2* out, long long outer, int n, long long inner, bool forward,
                        cudaStream_t st);
 

@@ -11,47 +11,10 @@
 // the in-flight HBM data costs no registers and no load instructions.  The
 // stage is read into registers in the exact order k_strided loads them and
 // the FFT code is shared, so results are bit-identical to k_strided.
-#include <cuda.h>
-
-#include "pfcs_fft.cuh"
 #include "pfcs_internal.h"
+#include "pfcs_tma.cuh"
 
 namespace pfcs {
-
-__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_fence_init() {
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
-  asm volatile(
-      "{\n"
-      " .reg .pred p;\n"
-      " PFCS_WAIT:\n"
-      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      " @!p bra PFCS_WAIT;\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-// order this thread's (and, after a CTA barrier, the CTA's) generic-proxy
-// shared-memory accesses before subsequent async-proxy (TMA) writes
-__device__ __forceinline__ void fence_proxy_async() {
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
-__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, unsigned long long* bar, int c0,
-                                            int c1, int c2) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
-      "l"((unsigned long long)map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
-      : "memory");
-}
 
 template <int N, int T>
 struct TmaCfg {
@@ -138,6 +101,26 @@ __global__ void __launch_bounds__(T*(N / radix_R(N)), 1)
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn();
+
+// Tiled FLOAT64 tensor map (rank <= 3); false when the driver rejects it or
+// the entry point is unavailable (callers then take the non-TMA kernels).
+bool make_tmap(CUtensorMap* map, int rank, const void* base, const unsigned long long* dims,
+               const unsigned long long* strides_bytes, const unsigned* box) {
+  EncodeTiledFn enc = encode_fn();
+  if (!enc || ((uintptr_t)base & 15)) return false;
+  cuuint64_t d[3], s[2];
+  cuuint32_t b[3], e[3] = {1, 1, 1};
+  for (int k = 0; k < rank; ++k) {
+    d[k] = dims[k];
+    b[k] = box[k];
+    if (k + 1 < rank) s[k] = strides_bytes[k];
+  }
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, (cuuint32_t)rank, (void*)base, d, s, b, e,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
 
 static EncodeTiledFn encode_fn() {
   static EncodeTiledFn fn = [] {

@@ -25,6 +25,7 @@
 #include "pfcs_diag.cuh"
 #include "pfcs_fft.cuh"
 #include "pfcs_internal.h"
+#include "pfcs_tma.cuh"
 
 namespace pfcs {
 
@@ -106,17 +107,38 @@ __host__ __device__ constexpr int real_ls(int m, int t) {
   return tile_ls(m, t, true) + (tile_ls(m, t, true) == pad_idx(m) ? 8 : 0);
 }
 
+// ST == 3: TMA-staged tiles.  Stage = the tile's input rows as TMA lands
+// them, [row][t]: 2M real rows (R2C) or M+1 complex rows (C2R / cube), each
+// T values wide; two stages (1024-byte aligned) + the FFT workspace + bars.
+template <int M, int T, int MODE>
+struct XStage {
+  static constexpr size_t BYTES = MODE == 0 ? (size_t)2 * M * T * 8 : (size_t)(M + 1) * T * 16;
+  static constexpr size_t PADDED = (BYTES + 1023) / 1024 * 1024;
+  static constexpr int ROWS = MODE == 0 ? 2 * M : M;          // rows moved by the tiled map
+  static constexpr int BR = ROWS < 256 ? ROWS : 256;          // rows per box
+  static constexpr int NB = ROWS / BR;
+  static constexpr size_t SMEM = 2 * PADDED + (size_t)T * real_ls(M, T) * 16 + 16 + 1024;
+};
+
 template <int M, int T, int ST, int MODE>
 __global__ void __launch_bounds__(T*(M / real_R(M, MODE)),
-                                  min_blocks(T*(M / real_R(M, MODE)), MODE == 2 ? PFCS_CUBE_TARGET : (ST == 2 ? 640 : 768)))
+                                  min_blocks(T*(M / real_R(M, MODE)), ST == 3 ? 512 : (MODE == 2 ? PFCS_CUBE_TARGET : (ST == 2 ? 640 : 768))))
     k_real_x(const void* in_, void* out_, i64 inner, const double2* __restrict__ twN, double scale,
-             double* diag) {
+             double* diag, const __grid_constant__ TmaPair tm) {
   constexpr int R = real_R(M, MODE);
   constexpr int P = M / R;
   constexpr int LS = real_ls(M, T);
-  constexpr bool MIR = use_mirror(MODE);
-  constexpr bool LMIR = late_mirror(MODE);
-  extern __shared__ double2 smem[];
+  constexpr bool TMA = ST == 3;
+  constexpr bool SMIR = TMA && MODE != MODE_R2C;  // mirror rows read from the TMA stage
+  constexpr bool MIR = !TMA && use_mirror(MODE);
+  constexpr bool LMIR = !TMA && late_mirror(MODE);
+  using XS = XStage<M, T, MODE>;
+  extern __shared__ unsigned char xraw[];
+  unsigned char* xbase = TMA ? xraw + ((1024u - (smem_u32(xraw) & 1023u)) & 1023u) : xraw;
+  double2* stage0 = (double2*)xbase;
+  double2* stage1 = (double2*)(xbase + XS::PADDED);
+  double2* smem = TMA ? (double2*)(xbase + 2 * XS::PADDED) : (double2*)xraw;  // FFT workspace
+  const double2* cur = stage0;  // TMA stage holding the current tile
   const int tid = threadIdx.x;
   const int t = tid % T;
   const int j = tid / T;
@@ -174,7 +196,7 @@ __global__ void __launch_bounds__(T*(M / real_R(M, MODE)),
           wl[e] = ok ? in[km * inner + i] : make_double2(0.0, 0.0);
         }
       }
-      if constexpr (!MIR && !LMIR) {
+      if constexpr (!MIR && !LMIR && !SMIR) {
         stash_line<M, R>(r.v, jj, sl);
         if (jj == 0) sl[pad_idx(M)] = r.xm;
         __syncthreads();
@@ -189,6 +211,8 @@ __global__ void __launch_bounds__(T*(M / real_R(M, MODE)),
           bm = r.w[e];
         } else if constexpr (LMIR) {
           bm = wl[e];
+        } else if constexpr (SMIR) {
+          bm = cur[(M - k) * T + t];  // row M for k = 0
         } else {
           bm = sl[pad_idx(M - k)];
         }
@@ -262,7 +286,55 @@ __global__ void __launch_bounds__(T*(M / real_R(M, MODE)),
     }
   };
 
-  reg_tile_loop<ST, RegsX<R, MIR>>(ntiles, load, comp);
+  if constexpr (!TMA) {
+    reg_tile_loop<ST, RegsX<R, MIR>>(ntiles, load, comp);
+  } else {
+    unsigned long long* bars = (unsigned long long*)(smem + (size_t)T * LS);
+    auto issue = [&](i64 tile, int sidx) {
+      const int i0 = (int)(tile * T);
+      unsigned char* dst = (unsigned char*)(sidx ? stage1 : stage0);
+      mbar_expect_tx(&bars[sidx], (unsigned)XS::BYTES);
+      constexpr int W = MODE == MODE_R2C ? 8 : 16;  // bytes per stage element
+#pragma unroll
+      for (int b = 0; b < XS::NB; ++b)
+        tma_load_2d(dst + (size_t)b * XS::BR * T * W, &tm.a, &bars[sidx], (MODE == MODE_R2C ? 1 : 2) * i0, b * XS::BR);
+      if (MODE != MODE_R2C) tma_load_2d(dst + (size_t)M * T * W, &tm.b, &bars[sidx], 2 * i0, M);
+    };
+    if (tid == 0) {
+      mbar_init(&bars[0], 1);
+      mbar_init(&bars[1], 1);
+      mbar_fence_init();
+    }
+    __syncthreads();
+    i64 tile = blockIdx.x;
+    if (tid == 0 && tile < ntiles) issue(tile, 0);
+    for (int it = 0; tile < ntiles; ++it, tile += gridDim.x) {
+      const int sidx = it & 1;
+      if (tid == 0) {
+        const i64 nx = tile + gridDim.x;
+        if (nx < ntiles) {
+          fence_proxy_async();
+          issue(nx, sidx ^ 1);
+        }
+      }
+      mbar_wait(&bars[sidx], (unsigned)((it >> 1) & 1));
+      cur = sidx ? stage1 : stage0;
+      RegsX<R, false> r;
+      if (MODE == MODE_R2C) {
+        const double* sd = (const double*)cur;
+#pragma unroll
+        for (int e = 0; e < R; ++e) {
+          const int m = j + P * e;
+          r.v[e] = make_double2(sd[(2 * m) * T + t], sd[(2 * m + 1) * T + t]);
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < R; ++e) r.v[e] = cur[(j + P * e) * T + t];
+      }
+      comp(tile, r);
+      __syncthreads();
+    }
+  }
   if (MODE == MODE_CUBE) diag_block_max(diag, m_abs, 0.0, m_abs);
 }
 
@@ -323,6 +395,25 @@ __global__ void __launch_bounds__(T*(N / radix_R(N)), min_blocks(T*(N / radix_R(
 
 // ---------------------------------------------------------------- dispatch --
 
+// tensor maps of the x-pass input: rows of `inner` contiguous values
+template <int M, int T, int MODE>
+static bool x_tmaps(TmaPair* tm, const void* in, i64 inner) {
+  if (2 * inner >= (1LL << 31)) return false;
+  using XS = XStage<M, T, MODE>;
+  if (MODE == MODE_R2C) {
+    if (inner % 2) return false;  // row stride must be a multiple of 16 bytes
+    const unsigned long long dims[2] = {(unsigned long long)inner, (unsigned long long)(2 * M)};
+    const unsigned long long str[1] = {(unsigned long long)inner * 8};
+    const unsigned box[2] = {(unsigned)T, (unsigned)XS::BR};
+    return make_tmap(&tm->a, 2, in, dims, str, box);
+  }
+  const unsigned long long dims[2] = {(unsigned long long)(2 * inner), (unsigned long long)(M + 1)};
+  const unsigned long long str[1] = {(unsigned long long)inner * 16};
+  const unsigned box[2] = {(unsigned)(2 * T), (unsigned)XS::BR};
+  const unsigned box1[2] = {(unsigned)(2 * T), 1u};
+  return make_tmap(&tm->a, 2, in, dims, str, box) && make_tmap(&tm->b, 2, in, dims, str, box1);
+}
+
 template <int M, int MODE>
 static int real_x_m(const void* in, void* out, i64 inner, double* diag, cudaStream_t st) {
   const double2* twN = twiddles(2 * M);
@@ -335,11 +426,25 @@ static int real_x_m(const void* in, void* out, i64 inner, double* diag, cudaStre
     if constexpr (T * P > 1024) {
       return fail(PFCS_E_UNSUPPORTED, "tile too large");
     } else {
-      const size_t smem = (size_t)T * real_ls(M, T) * sizeof(double2);
       const i64 ntiles = (inner + T - 1) / T;
+      TmaPair tm;
+      // TMA staging (B200 A/B, ms per launch, off -> on): cube 1024^3 7.02 -> 5.85,
+      // 512^3 0.79 -> 0.67; C2R 1024^3 4.96 -> 4.75; R2C 512^3 0.57 -> 0.50 but
+      // 1024^3 4.94 -> 5.58 (64-byte real rows, one CTA per SM), so R2C keeps
+      // the register pipeline from M = 512 up.
+      if constexpr (XStage<M, T, MODE>::SMEM <= 227 * 1024 && (MODE != MODE_R2C || (T >= 2 && M <= 256))) {
+        if (tma_enabled() && x_tmaps<M, T, MODE>(&tm, in, inner)) {
+          constexpr size_t smem = XStage<M, T, MODE>::SMEM;
+          int grid = 0;
+          if (int rc = persistent_grid((const void*)k_real_x<M, T, 3, MODE>, T * P, smem, ntiles, &grid)) return rc;
+          k_real_x<M, T, 3, MODE><<<grid, T * P, smem, st>>>(in, out, inner, twN, 1.0 / (double)(2 * M), diag, tm);
+          return check_launch("k_real_x(tma)");
+        }
+      }
+      const size_t smem = (size_t)T * real_ls(M, T) * sizeof(double2);
       int grid = 0;
       if (int rc = persistent_grid((const void*)k_real_x<M, T, ST, MODE>, T * P, smem, ntiles, &grid)) return rc;
-      k_real_x<M, T, ST, MODE><<<grid, T * P, smem, st>>>(in, out, inner, twN, 1.0 / (double)(2 * M), diag);
+      k_real_x<M, T, ST, MODE><<<grid, T * P, smem, st>>>(in, out, inner, twN, 1.0 / (double)(2 * M), diag, tm);
       return check_launch("k_real_x");
     }
   });

@@ -1,6 +1,8 @@
-"""The TMA-staged strided pass (csrc/pfcs_tma.cu, PFCS_TMA=1) must be
-bit-identical to the register-pipelined k_strided it replaces, for every tile
-width, ragged inner extents (OOB-filled boxes) and both directions.
+"""The TMA-staged passes (csrc/pfcs_tma.cu k_strided_tma; csrc/pfcs_x.cu
+k_real_x with ST == 3) must be bit-identical to the register-pipelined kernels
+they replace (PFCS_TMA=0): every tile width, ragged inner extents (OOB-filled
+boxes), both directions, the real x transforms and the fused cube pass with
+its diagnostics.
 
 The switch is read once per process, so each configuration runs in a child
 process that writes its outputs for comparison."""
@@ -35,15 +37,32 @@ for (outer, n, inner) in {cases!r}:
         torch.cuda.synchronize()
         out[f"{{outer}}_{{n}}_{{inner}}_{{fwd}}"] = b.cpu().numpy()
         out[f"{{outer}}_{{n}}_{{inner}}_{{fwd}}_ip"] = ip.cpu().numpy()
+for (n, inner) in {xcases!r}:
+    rng = np.random.default_rng(n + inner)
+    nh = n // 2 + 1
+    r = torch.from_numpy(rng.standard_normal((n, inner))).cuda()
+    h = torch.empty((nh, inner), dtype=torch.complex128, device="cuda")
+    nat.call("pfcs_rfft_x", nat.ptr(r), nat.ptr(h), n, inner, nat.stream_ptr())
+    r2 = torch.empty_like(r)
+    nat.call("pfcs_irfft_x", nat.ptr(h), nat.ptr(r2), n, inner, nat.stream_ptr())
+    c = h.clone()
+    diag = torch.zeros(nat.DIAG_SLOTS * 4, dtype=torch.float64, device="cuda")
+    nat.call("pfcs_pfc_cube_x", nat.ptr(c), n, inner, 1, nat.ptr(diag), nat.stream_ptr())
+    torch.cuda.synchronize()
+    out[f"x{{n}}_{{inner}}_r2c"] = h.cpu().numpy()
+    out[f"x{{n}}_{{inner}}_c2r"] = r2.cpu().numpy()
+    out[f"x{{n}}_{{inner}}_cube"] = c.cpu().numpy()
+    out[f"x{{n}}_{{inner}}_diag"] = diag.cpu().numpy()
 np.savez({path!r}, **out)
 """
 
+XCASES = [(128, 96), (256, 1000), (512, 1030), (1024, 520), (1024, 64)]
 CASES = [(3, 64, 40), (2, 128, 33), (2, 256, 16), (2, 512, 9), (3, 1024, 12), (1, 2048, 5), (2, 1024, 1000)]
 
 
 def _run(tmp_path, name, env):
     path = str(tmp_path / f"{name}.npz")
-    code = CHILD.format(root=str(ROOT), cases=CASES, path=path)
+    code = CHILD.format(root=str(ROOT), cases=CASES, xcases=XCASES, path=path)
     e = dict(os.environ)
     e.update(env)
     subprocess.run([sys.executable, "-c", code], check=True, env=e, timeout=300)
