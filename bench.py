@@ -538,7 +538,8 @@ def main():
     out["roofline"] = roofline_of(table, hbm, peak_kind, measured_traffic(workload))
     out["roofline"]["whole_step_frac"] = round(out["value"] / (hbm * ctx.world), 4)
     if pfc_res is not None:
-        pr = roofline_of(pfc_res["kernels"], hbm, peak_kind)
+        pr = roofline_of(pfc_res["kernels"], hbm, peak_kind,
+                         measured_traffic(f"pfc{args.pfc_n}") if ctx.world == 1 else None)
         pfc_res["roofline"] = pr
         t_roof = pfc_res["alg_hbm_bytes_per_step"] / (hbm * 1e9)
         pfc_res["roofline_step_frac"] = round(t_roof / (pfc_res["ms_per_step"] * 1e-3), 4)

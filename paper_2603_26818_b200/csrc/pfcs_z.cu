@@ -22,6 +22,7 @@
 #include "pfcs_diag.cuh"
 #include "pfcs_fft.cuh"
 #include "pfcs_internal.h"
+#include "pfcs_tma.cuh"
 
 namespace pfcs {
 
@@ -61,7 +62,11 @@ __global__ void __launch_bounds__(T*(N / radix_R(N)), min_blocks(T*(N / radix_R(
   constexpr int R = radix_R(N);
   constexpr int P = N / R;
   constexpr int LS = tile_ls(N, T, false);
-  extern __shared__ double2 smem[];
+  constexpr bool TMA = ST == 3;  // N-hat lines staged by TMA (two stages)
+  extern __shared__ unsigned char zraw[];
+  unsigned char* zbase = TMA ? zraw + ((1024u - (smem_u32(zraw) & 1023u)) & 1023u) : zraw;
+  double2* stage = (double2*)zbase;  // [stage 0: T x N][stage 1: T x N]
+  double2* smem = TMA ? stage + 2 * (size_t)T * N : (double2*)zraw;  // FFT workspace
   const int tid = threadIdx.x;
   const int t = tid / P;
   const int j = tid - t * P;
@@ -128,7 +133,50 @@ __global__ void __launch_bounds__(T*(N / radix_R(N)), min_blocks(T*(N / radix_R(
       }
     }
   };
-  reg_tile_loop<ST, RegsZ<R>>(ntiles, load, comp);
+  if constexpr (!TMA) {
+    reg_tile_loop<ST, RegsZ<R>>(ntiles, load, comp);
+  } else {
+    // N-hat lines double-buffered through TMA bulk copies (issued one tile
+    // ahead); psi_hat goes straight to registers, its latency hidden by the
+    // forward FFT.
+    unsigned long long* bars = (unsigned long long*)(smem + (size_t)T * LS);
+    auto issue = [&](i64 tile, int sidx) {
+      const i64 l0 = tile * T;
+      const i64 nl_lines = (nlines - l0) < T ? (nlines - l0) : T;
+      const unsigned bytes = (unsigned)(nl_lines * N * 16);
+      mbar_expect_tx(&bars[sidx], bytes);
+      bulk_load(stage + (size_t)sidx * T * N, nl + l0 * N, bytes, &bars[sidx]);
+    };
+    if (tid == 0) {
+      mbar_init(&bars[0], 1);
+      mbar_init(&bars[1], 1);
+      mbar_fence_init();
+    }
+    __syncthreads();
+    i64 tile = blockIdx.x;
+    if (tid == 0 && tile < ntiles) issue(tile, 0);
+    for (int it = 0; tile < ntiles; ++it, tile += gridDim.x) {
+      const int sidx = it & 1;
+      if (tid == 0) {
+        const i64 nx = tile + gridDim.x;
+        if (nx < ntiles) {
+          fence_proxy_async();
+          issue(nx, sidx ^ 1);
+        }
+      }
+      RegsZ<R> r;
+      const i64 l = tile * T + t;
+      const bool ok = l < nlines;
+#pragma unroll
+      for (int e = 0; e < R; ++e) r.p[e] = ok ? psi_hat[l * N + j + P * e] : make_double2(0.0, 0.0);
+      mbar_wait(&bars[sidx], (unsigned)((it >> 1) & 1));
+      const double2* sv = stage + (size_t)sidx * T * N + (size_t)t * N;
+#pragma unroll
+      for (int e = 0; e < R; ++e) r.v[e] = sv[j + P * e];
+      comp(tile, r);
+      __syncthreads();
+    }
+  }
   diag_flag_nonfinite(diag, bad);
 }
 
@@ -154,9 +202,37 @@ static int pfc_z_n(const double2* nl, double2* psi_hat, double2* next, i64 cx, i
     if constexpr (T * P > 1024) {
       return fail(PFCS_E_UNSUPPORTED, "tile too large");
     } else {
-      const size_t smem = (size_t)T * tile_ls(N, T, false) * sizeof(double2);
+      // TMA staging for an unblocked input (B200: see DESIGN.md); the
+      // partial last tile copies only its valid lines
+      constexpr size_t tsmem = 2 * (size_t)T * N * 16 + (size_t)T * tile_ls(N, T, false) * 16 + 16 + 1024;
+      // Opt-in only (PFCS_TMA_Z=1): on B200 the contiguous z lines already
+      // stream well through LDG, and staging N-hat costs more than it hides
+      // (1024^3: 6.78 ms register-pipelined vs 7.57 ms TMA-staged).
+      static const bool z_tma = [] {
+        const char* v = getenv("PFCS_TMA_Z");
+        return v && *v && atoi(v) != 0;
+      }();
+      const bool use_tma = z_tma && !bin && tma_enabled() && tsmem <= 227 * 1024 && N >= 64 &&
+                           !(((uintptr_t)nl | (uintptr_t)psi_hat) & 15);
+      const size_t smem = use_tma ? tsmem : (size_t)T * tile_ls(N, T, false) * sizeof(double2);
       const i64 ntiles = (nlines + T - 1) / T;
       int grid = 0;
+      if (use_tma) {
+#define PFCS_ZK(BI, BO, NX) k_pfc_z<N, T, 3, BI, BO, NX>
+#define PFCS_ZL(BI, BO, NX)                                                                       \
+  do {                                                                                            \
+    if (int rc = persistent_grid((const void*)PFCS_ZK(BI, BO, NX), T * P, smem, ntiles, &grid))   \
+      return rc;                                                                                  \
+    PFCS_ZK(BI, BO, NX)<<<grid, T * P, smem, st>>>(nl, psi_hat, next, nlines, (int)ny, a, b, kx, \
+                                                   ky, kz, p, tw, scale, diag, tab);              \
+  } while (0)
+        if (!nx) PFCS_ZL(false, false, false);
+        else if (bout) PFCS_ZL(false, true, true);
+        else PFCS_ZL(false, false, true);
+#undef PFCS_ZL
+#undef PFCS_ZK
+        return check_launch("k_pfc_z(tma)");
+      }
 #define PFCS_ZK(BI, BO, NX) k_pfc_z<N, T, ST, BI, BO, NX>
 #define PFCS_ZL(BI, BO, NX)                                                                       \
   do {                                                                                            \

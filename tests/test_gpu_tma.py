@@ -1,8 +1,8 @@
 """The TMA-staged passes (csrc/pfcs_tma.cu k_strided_tma; csrc/pfcs_x.cu
 k_real_x with ST == 3) must be bit-identical to the register-pipelined kernels
 they replace (PFCS_TMA=0): every tile width, ragged inner extents (OOB-filled
-boxes), both directions, the real x transforms and the fused cube pass with
-its diagnostics.
+boxes), both directions, the real x transforms, the fused cube pass and the
+fused z update (k_pfc_z, bulk copies) with their diagnostics.
 
 The switch is read once per process, so each configuration runs in a child
 process that writes its outputs for comparison."""
@@ -53,16 +53,33 @@ for (n, inner) in {xcases!r}:
     out[f"x{{n}}_{{inner}}_c2r"] = r2.cpu().numpy()
     out[f"x{{n}}_{{inner}}_cube"] = c.cpu().numpy()
     out[f"x{{n}}_{{inner}}_diag"] = diag.cpu().numpy()
+for (cx, ny, nz) in {zcases!r}:
+    rng = np.random.default_rng(cx * ny + nz)
+    shp = (cx, ny, nz)
+    nl = torch.from_numpy(rng.standard_normal(shp) + 1j * rng.standard_normal(shp)).cuda()
+    psi = torch.from_numpy(rng.standard_normal(shp) + 1j * rng.standard_normal(shp)).cuda()
+    nxt = torch.empty_like(nl)
+    kx = torch.linspace(0, 1, cx, dtype=torch.float64, device="cuda")
+    ky = torch.linspace(0, 1, ny, dtype=torch.float64, device="cuda")
+    kz = torch.linspace(0, 1, nz, dtype=torch.float64, device="cuda")
+    diag = torch.zeros(nat.DIAG_SLOTS * 4, dtype=torch.float64, device="cuda")
+    nat.call("pfcs_pfc_update_z", nat.ptr(nl), nat.ptr(psi), nat.ptr(nxt), cx, ny, nz, 1, 1,
+             nat.ptr(kx), nat.ptr(ky), nat.ptr(kz), -0.3, 0.1, nat.ptr(diag), nat.stream_ptr())
+    torch.cuda.synchronize()
+    out[f"z{{cx}}_{{ny}}_{{nz}}_psi"] = psi.cpu().numpy()
+    out[f"z{{cx}}_{{ny}}_{{nz}}_next"] = nxt.cpu().numpy()
+    out[f"z{{cx}}_{{ny}}_{{nz}}_diag"] = diag.cpu().numpy()
 np.savez({path!r}, **out)
 """
 
+ZCASES = [(3, 5, 256), (2, 7, 1024), (5, 3, 64), (4, 4, 512)]
 XCASES = [(128, 96), (256, 1000), (512, 1030), (1024, 520), (1024, 64)]
 CASES = [(3, 64, 40), (2, 128, 33), (2, 256, 16), (2, 512, 9), (3, 1024, 12), (1, 2048, 5), (2, 1024, 1000)]
 
 
 def _run(tmp_path, name, env):
     path = str(tmp_path / f"{name}.npz")
-    code = CHILD.format(root=str(ROOT), cases=CASES, xcases=XCASES, path=path)
+    code = CHILD.format(root=str(ROOT), cases=CASES, xcases=XCASES, zcases=ZCASES, path=path)
     e = dict(os.environ)
     e.update(env)
     subprocess.run([sys.executable, "-c", code], check=True, env=e, timeout=300)
@@ -76,6 +93,6 @@ def test_tma_strided_bit_identical(tmp_path, t):
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     base = _run(tmp_path, "base", {"PFCS_TMA": "0"})
-    tma = _run(tmp_path, f"tma{t}", {"PFCS_TMA": "1", "PFCS_TMA_T": str(t)})
+    tma = _run(tmp_path, f"tma{t}", {"PFCS_TMA": "1", "PFCS_TMA_T": str(t), "PFCS_TMA_Z": "1"})
     for k in base.files:
         assert np.array_equal(base[k], tma[k]), k
