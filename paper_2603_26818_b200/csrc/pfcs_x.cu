@@ -427,7 +427,7 @@ static int real_x_m(const void* in, void* out, i64 inner, double* diag, cudaStre
       return fail(PFCS_E_UNSUPPORTED, "tile too large");
     } else {
       const i64 ntiles = (inner + T - 1) / T;
-      TmaPair tm;
+      TmaPair tm{};  // unused (zero) unless the TMA path is taken
       // TMA staging (B200 A/B, ms per launch, off -> on): cube 1024^3 7.02 -> 5.85,
       // 512^3 0.79 -> 0.67; C2R 1024^3 4.96 -> 4.75; R2C 512^3 0.57 -> 0.50 but
       // 1024^3 4.94 -> 5.58 (64-byte real rows, one CTA per SM), so R2C keeps
