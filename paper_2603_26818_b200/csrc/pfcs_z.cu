@@ -53,8 +53,12 @@ struct RegsZ {
   double2 p[R];  // psi_hat z line
 };
 
+#ifndef PFCS_Z_TMA_TARGET
+#define PFCS_Z_TMA_TARGET 512
+#endif
 template <int N, int T, int ST, bool BIN, bool BOUT, bool NEXT>
-__global__ void __launch_bounds__(T*(N / radix_R(N)), min_blocks(T*(N / radix_R(N)), 512))
+__global__ void __launch_bounds__(T*(N / radix_R(N)),
+                                  min_blocks(T*(N / radix_R(N)), ST == 3 ? PFCS_Z_TMA_TARGET : 512))
     k_pfc_z(const double2* nl, double2* psi_hat, double2* next, i64 nlines, int ny, SlabSplit sin,
             SlabSplit sout, const double* __restrict__ kx, const double* __restrict__ ky,
             const double* __restrict__ kz, PfcSym p, const double2* __restrict__ tw, double scale,
@@ -62,11 +66,16 @@ __global__ void __launch_bounds__(T*(N / radix_R(N)), min_blocks(T*(N / radix_R(
   constexpr int R = radix_R(N);
   constexpr int P = N / R;
   constexpr int LS = tile_ls(N, T, false);
-  constexpr bool TMA = ST == 3;  // N-hat lines staged by TMA (two stages)
+  // TMA: psi_hat lines are bulk-copied into a shared stage (needed only after
+  // the forward FFT of N-hat, so they cost no registers across it); N-hat is
+  // loaded straight into registers.
+  constexpr bool TMA = ST == 3;
   extern __shared__ unsigned char zraw[];
   unsigned char* zbase = TMA ? zraw + ((1024u - (smem_u32(zraw) & 1023u)) & 1023u) : zraw;
-  double2* stage = (double2*)zbase;  // [stage 0: T x N][stage 1: T x N]
-  double2* smem = TMA ? stage + 2 * (size_t)T * N : (double2*)zraw;  // FFT workspace
+  double2* stage = (double2*)zbase;  // psi_hat stage: T x N
+  double2* smem = TMA ? stage + (size_t)T * N : (double2*)zraw;  // FFT workspace
+  unsigned long long* bar = (unsigned long long*)(smem + (size_t)T * LS);
+  int it_cur = 0;
   const int tid = threadIdx.x;
   const int t = tid / P;
   const int j = tid - t * P;
@@ -88,8 +97,15 @@ __global__ void __launch_bounds__(T*(N / radix_R(N)), min_blocks(T*(N / radix_R(
         a = l * N + z;
       }
       r.v[e] = ok ? nl[a] : make_double2(0.0, 0.0);
-      r.p[e] = ok ? psi_hat[l * N + z] : make_double2(0.0, 0.0);
+      if constexpr (!TMA) r.p[e] = ok ? psi_hat[l * N + z] : make_double2(0.0, 0.0);
     }
+  };
+  auto issue = [&](i64 tile) {  // thread 0: psi_hat lines of `tile` -> stage
+    const i64 l0 = tile * T;
+    const i64 lines = (nlines - l0) < T ? (nlines - l0) : T;
+    const unsigned bytes = (unsigned)(lines * N * 16);
+    mbar_expect_tx(bar, bytes);
+    bulk_load(stage, psi_hat + l0 * N, bytes, bar);
   };
   auto comp = [&](i64 tile, RegsZ<R>& r) {
     const i64 l = tile * T + t;
@@ -100,19 +116,27 @@ __global__ void __launch_bounds__(T*(N / radix_R(N)), min_blocks(T*(N / radix_R(
     const int ly = ok ? (int)(l - lx * ny) : 0;
     const double kxx = __ldg(&kx[lx]);
     const double kyy = __ldg(&ky[ly]);
+    if constexpr (TMA) mbar_wait(bar, (unsigned)(it_cur & 1));
 #pragma unroll
     for (int e = 0; e < R; ++e) {
       const int z = jj + P * e;
       const double k2 = k2_of(kxx, kyy, __ldg(&kz[z]));
       double lap, rden;
       pfc_symbols(k2, p.eps, p.dt, lap, rden);
-      const double2 ph = r.p[e];
+      const double2 ph = TMA ? stage[(size_t)t * N + z] : r.p[e];
       const double nr = __dadd_rn(ph.x, __dmul_rn(p.dt, __dmul_rn(lap, r.v[e].x)));
       const double ni = __dadd_rn(ph.y, __dmul_rn(p.dt, __dmul_rn(lap, r.v[e].y)));
       const double2 nw = make_double2(__dmul_rn(nr, rden), __dmul_rn(ni, rden));
       bad |= ok && !(isfinite(nw.x) && isfinite(nw.y));
       if (ok) psi_hat[l * N + z] = nw;
       r.v[e] = nw;
+    }
+    if constexpr (TMA) {  // stage read by every thread: refill with the next tile
+      __syncthreads();
+      if (threadIdx.x == 0 && tile + gridDim.x < ntiles) {
+        fence_proxy_async();
+        issue(tile + gridDim.x);
+      }
     }
     if (NEXT) {
       const int j2 = opaque(jj);
@@ -136,45 +160,17 @@ __global__ void __launch_bounds__(T*(N / radix_R(N)), min_blocks(T*(N / radix_R(
   if constexpr (!TMA) {
     reg_tile_loop<ST, RegsZ<R>>(ntiles, load, comp);
   } else {
-    // N-hat lines double-buffered through TMA bulk copies (issued one tile
-    // ahead); psi_hat goes straight to registers, its latency hidden by the
-    // forward FFT.
-    unsigned long long* bars = (unsigned long long*)(smem + (size_t)T * LS);
-    auto issue = [&](i64 tile, int sidx) {
-      const i64 l0 = tile * T;
-      const i64 nl_lines = (nlines - l0) < T ? (nlines - l0) : T;
-      const unsigned bytes = (unsigned)(nl_lines * N * 16);
-      mbar_expect_tx(&bars[sidx], bytes);
-      bulk_load(stage + (size_t)sidx * T * N, nl + l0 * N, bytes, &bars[sidx]);
-    };
     if (tid == 0) {
-      mbar_init(&bars[0], 1);
-      mbar_init(&bars[1], 1);
+      mbar_init(bar, 1);
       mbar_fence_init();
     }
     __syncthreads();
     i64 tile = blockIdx.x;
-    if (tid == 0 && tile < ntiles) issue(tile, 0);
-    for (int it = 0; tile < ntiles; ++it, tile += gridDim.x) {
-      const int sidx = it & 1;
-      if (tid == 0) {
-        const i64 nx = tile + gridDim.x;
-        if (nx < ntiles) {
-          fence_proxy_async();
-          issue(nx, sidx ^ 1);
-        }
-      }
+    if (tid == 0 && tile < ntiles) issue(tile);
+    for (; tile < ntiles; ++it_cur, tile += gridDim.x) {
       RegsZ<R> r;
-      const i64 l = tile * T + t;
-      const bool ok = l < nlines;
-#pragma unroll
-      for (int e = 0; e < R; ++e) r.p[e] = ok ? psi_hat[l * N + j + P * e] : make_double2(0.0, 0.0);
-      mbar_wait(&bars[sidx], (unsigned)((it >> 1) & 1));
-      const double2* sv = stage + (size_t)sidx * T * N + (size_t)t * N;
-#pragma unroll
-      for (int e = 0; e < R; ++e) r.v[e] = sv[j + P * e];
+      load(tile, r);
       comp(tile, r);
-      __syncthreads();
     }
   }
   diag_flag_nonfinite(diag, bad);
@@ -204,15 +200,15 @@ static int pfc_z_n(const double2* nl, double2* psi_hat, double2* next, i64 cx, i
     } else {
       // TMA staging for an unblocked input (B200: see DESIGN.md); the
       // partial last tile copies only its valid lines
-      constexpr size_t tsmem = 2 * (size_t)T * N * 16 + (size_t)T * tile_ls(N, T, false) * 16 + 16 + 1024;
-      // Opt-in only (PFCS_TMA_Z=1): on B200 the contiguous z lines already
-      // stream well through LDG, and staging N-hat costs more than it hides
-      // (1024^3: 6.78 ms register-pipelined vs 7.57 ms TMA-staged).
+      constexpr size_t tsmem = (size_t)T * N * 16 + (size_t)T * tile_ls(N, T, false) * 16 + 16 + 1024;
+      // psi_hat staged by TMA bulk copies: opt-in (PFCS_TMA_Z=1).  On the B200
+      // the contiguous z lines stream best through LDG (1024^3: 6.80 ms
+      // register-loaded vs 7.09 ms psi-staged vs 7.57 ms N-hat-staged).
       static const bool z_tma = [] {
         const char* v = getenv("PFCS_TMA_Z");
         return v && *v && atoi(v) != 0;
       }();
-      const bool use_tma = z_tma && !bin && tma_enabled() && tsmem <= 227 * 1024 && N >= 64 &&
+      const bool use_tma = z_tma && tma_enabled() && tsmem <= 227 * 1024 && N >= 64 &&
                            !(((uintptr_t)nl | (uintptr_t)psi_hat) & 15);
       const size_t smem = use_tma ? tsmem : (size_t)T * tile_ls(N, T, false) * sizeof(double2);
       const i64 ntiles = (nlines + T - 1) / T;
@@ -226,7 +222,11 @@ static int pfc_z_n(const double2* nl, double2* psi_hat, double2* next, i64 cx, i
     PFCS_ZK(BI, BO, NX)<<<grid, T * P, smem, st>>>(nl, psi_hat, next, nlines, (int)ny, a, b, kx, \
                                                    ky, kz, p, tw, scale, diag, tab);              \
   } while (0)
-        if (!nx) PFCS_ZL(false, false, false);
+        if (!nx) {
+          if (bin) PFCS_ZL(true, false, false);
+          else PFCS_ZL(false, false, false);
+        } else if (bin && bout) PFCS_ZL(true, true, true);
+        else if (bin) PFCS_ZL(true, false, true);
         else if (bout) PFCS_ZL(false, true, true);
         else PFCS_ZL(false, false, true);
 #undef PFCS_ZL
