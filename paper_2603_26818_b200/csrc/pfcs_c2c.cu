@@ -384,6 +384,10 @@ static int strided_to_n(const double2* in, i64 outer, i64 inner, SlabSplitH si, 
   if (!tw) return PFCS_E_CUDA;
   SlabSplit a{si.G, si.base, si.extra}, so{souter.G, souter.base, souter.extra};
   const bool bin = si.G > 1;
+  if (!bin && inner > 1 && tma_enabled()) {
+    const int rc = launch_strided_tma(in, nullptr, outer, N, inner, FWD, st, &souter, &dst);
+    if (rc != 1) return rc;
+  }
   return with_variant<KIND_STRIDED, N>([&](auto var) -> int {
     constexpr int V = decltype(var)::value;
     constexpr int T = TileCfg<N>::T_MIN << (V & 3);

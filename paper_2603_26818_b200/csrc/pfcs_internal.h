@@ -34,8 +34,10 @@ inline int ilog2(long long n) {
 bool tma_enabled();
 bool make_tmap(CUtensorMap* map, int rank, const void* base, const unsigned long long* dims,
                const unsigned long long* strides_bytes, const unsigned* box);
+struct SlabSplitH;
+struct PeerTable;
 int launch_strided_tma(const double2* in, double2* out, long long outer, int n, long long inner, bool forward,
-                       cudaStream_t st);
+                       cudaStream_t st, const SlabSplitH* souter = nullptr, const PeerTable* dst = nullptr);
 
 // Opt a kernel in to > 48 KB dynamic shared memory once.
 int ensure_smem(const void* func, size_t bytes);

@@ -28,10 +28,13 @@ struct TmaCfg {
   static constexpr size_t SMEM = 2 * (size_t)STAGE + (size_t)T * LS * 16 + 16 + 1024;
 };
 
-template <int N, int T, bool FWD>
+// OPEER: outer row o goes to tout.p[h][(o - ooff_h) ...] (the fused
+// transpose of the slab pipeline: souter splits the outer axis over ranks).
+template <int N, int T, bool FWD, bool OPEER = false>
 __global__ void __launch_bounds__(T*(N / radix_R(N)), 1)
     k_strided_tma(const __grid_constant__ CUtensorMap map, double2* out, i64 outer, i64 inner, i64 tpo,
-                  const double2* __restrict__ tw, double scale) {
+                  const double2* __restrict__ tw, double scale, SlabSplit souter = SlabSplit{},
+                  PeerTable tout = PeerTable{}) {
   using C = TmaCfg<N, T>;
   constexpr int R = C::R;
   constexpr int P = C::P;
@@ -85,7 +88,14 @@ __global__ void __launch_bounds__(T*(N / radix_R(N)), 1)
     const int jj = opaque(j);
     fft_line<N, FWD>(v, jj, sl, tw);
     if (i < inner) {
-      double2* dst = out + o * (i64)N * inner + i;
+      double2* dst;
+      if constexpr (OPEER) {
+        int h, ooff, co;
+        souter.locate3((int)o, h, ooff, co);
+        dst = tout.p[h] + (o - ooff) * (i64)N * inner + i;
+      } else {
+        dst = out + o * (i64)N * inner + i;
+      }
 #pragma unroll
       for (int e = 0; e < R; ++e) {
         double2 x = v[e];
@@ -152,7 +162,8 @@ static int tma_tile_width(int dflt) {
 }
 
 template <int N, int T, bool FWD>
-static int strided_tma_nt(const double2* in, double2* out, i64 outer, i64 inner, cudaStream_t st) {
+static int strided_tma_nt(const double2* in, double2* out, i64 outer, i64 inner, cudaStream_t st,
+                          const SlabSplitH* souter = nullptr, const PeerTable* dst = nullptr) {
   using C = TmaCfg<N, T>;
   if constexpr (C::SMEM > 227 * 1024 || T * C::P > 1024) {
     return 1;  // not applicable
@@ -172,6 +183,14 @@ static int strided_tma_nt(const double2* in, double2* out, i64 outer, i64 inner,
     if (!tw) return PFCS_E_CUDA;
     const i64 tpo = (inner + T - 1) / T;
     int grid = 0;
+    if (dst) {
+      const SlabSplit so{souter->G, souter->base, souter->extra};
+      if (int rc = persistent_grid((const void*)k_strided_tma<N, T, FWD, true>, T * C::P, C::SMEM, outer * tpo, &grid))
+        return rc;
+      k_strided_tma<N, T, FWD, true><<<grid, T * C::P, C::SMEM, st>>>(map, nullptr, outer, inner, tpo, tw,
+                                                                      1.0 / (double)N, so, *dst);
+      return check_launch("k_strided_tma(peer)");
+    }
     if (int rc = persistent_grid((const void*)k_strided_tma<N, T, FWD>, T * C::P, C::SMEM, outer * tpo, &grid))
       return rc;
     k_strided_tma<N, T, FWD><<<grid, T * C::P, C::SMEM, st>>>(map, out, outer, inner, tpo, tw, 1.0 / (double)N);
@@ -180,24 +199,26 @@ static int strided_tma_nt(const double2* in, double2* out, i64 outer, i64 inner,
 }
 
 template <int N, bool FWD>
-static int strided_tma_n(const double2* in, double2* out, i64 outer, i64 inner, cudaStream_t st) {
+static int strided_tma_n(const double2* in, double2* out, i64 outer, i64 inner, cudaStream_t st,
+                         const SlabSplitH* so = nullptr, const PeerTable* dst = nullptr) {
   switch (tma_tile_width(N >= 1024 ? 4 : 8)) {
-    case 1: return strided_tma_nt<N, 1, FWD>(in, out, outer, inner, st);
-    case 2: return strided_tma_nt<N, 2, FWD>(in, out, outer, inner, st);
-    case 4: return strided_tma_nt<N, 4, FWD>(in, out, outer, inner, st);
-    default: return strided_tma_nt<N, 8, FWD>(in, out, outer, inner, st);
+    case 1: return strided_tma_nt<N, 1, FWD>(in, out, outer, inner, st, so, dst);
+    case 2: return strided_tma_nt<N, 2, FWD>(in, out, outer, inner, st, so, dst);
+    case 4: return strided_tma_nt<N, 4, FWD>(in, out, outer, inner, st, so, dst);
+    default: return strided_tma_nt<N, 8, FWD>(in, out, outer, inner, st, so, dst);
   }
 }
 
 // Returns PFCS_OK / an error code, or 1 when the TMA path does not apply
 // (the caller then runs k_strided).
 int launch_strided_tma(const double2* in, double2* out, long long outer, int n, long long inner, bool forward,
-                       cudaStream_t st) {
+                       cudaStream_t st, const SlabSplitH* souter, const PeerTable* dst) {
   if (((uintptr_t)in & 15) || inner < 1 || 2 * inner >= (1LL << 31) || outer >= (1LL << 31)) return 1;
   switch (n) {
-#define PFCS_TMA_CASE(NN) \
-  case NN:                \
-    return forward ? strided_tma_n<NN, true>(in, out, outer, inner, st) : strided_tma_n<NN, false>(in, out, outer, inner, st);
+#define PFCS_TMA_CASE(NN)                                                            \
+  case NN:                                                                           \
+    return forward ? strided_tma_n<NN, true>(in, out, outer, inner, st, souter, dst) \
+                   : strided_tma_n<NN, false>(in, out, outer, inner, st, souter, dst);
     PFCS_TMA_CASE(64)
     PFCS_TMA_CASE(128)
     PFCS_TMA_CASE(256)
