@@ -321,11 +321,18 @@ __global__ void __launch_bounds__(T*(M / real_R(M, MODE)),
       cur = sidx ? stage1 : stage0;
       RegsX<R, false> r;
       if (MODE == MODE_R2C) {
+        // rows 2m and 2m+1 of a T-double stage row pair sit in opposite
+        // halves of the 32 banks when T = 8: odd-j threads read their odd
+        // row first, so each load instruction touches both halves (2
+        // wavefronts per warp instead of 4)
         const double* sd = (const double*)cur;
+        const int sw = j & 1;
 #pragma unroll
         for (int e = 0; e < R; ++e) {
           const int m = j + P * e;
-          r.v[e] = make_double2(sd[(2 * m) * T + t], sd[(2 * m + 1) * T + t]);
+          const double a = sd[(2 * m + sw) * T + t];
+          const double b = sd[(2 * m + 1 - sw) * T + t];
+          r.v[e] = sw ? make_double2(b, a) : make_double2(a, b);
         }
       } else {
 #pragma unroll
