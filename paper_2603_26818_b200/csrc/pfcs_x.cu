@@ -259,15 +259,25 @@ __global__ void __launch_bounds__(T*(M / real_R(M, MODE)),
     const int j2 = opaque(jj);  // keep the forward FFT's index math out of the inverse's live range
     fft_line<M, true, 2, PFCS_TW_LOADS, R>(r.v, j2, sl, twN);
     const double2 wj = __ldg(&twN[jj]);
-    __syncthreads();
-    stash_line<M, R>(r.v, jj, sl);
+    // Pairing Z_k with Z_{M-k}.  TMA mode exchanges through the current stage
+    // ([k][t] rows, conflict-free for t-fastest lanes): it was last read
+    // before the FFT's barriers and is refilled only after the end-of-tile
+    // barrier, so no barrier is needed in front of the stash.
+    double2* stg = const_cast<double2*>(cur);
+    if constexpr (TMA) {
+#pragma unroll
+      for (int e = 0; e < R; ++e) stg[(jj + P * e) * T + t] = v[e];
+    } else {
+      __syncthreads();
+      stash_line<M, R>(r.v, jj, sl);
+    }
     __syncthreads();
     double2* out = (double2*)out_;
 #pragma unroll
     for (int e = 0; e < R; ++e) {
       const int k = jj + P * e;
       const double2 zk = v[e];
-      const double2 zm = sl[pad_idx((M - k) & (M - 1))];
+      const double2 zm = TMA ? stg[((M - k) & (M - 1)) * T + t] : sl[pad_idx((M - k) & (M - 1))];
       double2 x;
       if (k == 0) {
         x = make_double2(zk.x + zk.y, 0.0);
