@@ -53,6 +53,7 @@ __all__ = [
     "TRIANGULAR_Q",
     "FCC_Q1",
     "INIT_KINDS",
+    "initial_field_slab",
 ]
 
 # lattice wavenumbers on the zeros of the two-ring symbol (pfc.py:43-46)
@@ -314,11 +315,14 @@ def _spectral_geometry(state: PfcState):
     return g.cx, g.ny, g.nz, g.xoff == 0, slab_kvectors(state.grid, state.symbols, g, dev)
 
 
-def _finish(state: PfcState, params: PfcParams, d: np.ndarray, first_index: int) -> None:
+def _finish(state: PfcState, params: PfcParams, d: np.ndarray, first_index: int,
+            realness: list | None = None) -> None:
     m_re, m_im, m_abs, bad = _StepEngine.reduce_diag(d)
     for s in range(len(m_re)):
         if state.psi_hat.dev.numel():
             state.last_max_imag_ratio = float(m_im[s] / m_re[s]) if m_re[s] > 0 else 0.0
+        if realness is not None:
+            realness.append(state.last_max_imag_ratio)
         if bad[s]:
             state.step_index = first_index + s
             raise DivergenceError(first_index + s, float(m_abs[s]))
@@ -338,10 +342,11 @@ def pfc_step(state: PfcState, params: PfcParams) -> PfcState:
     return state
 
 
-def pfc_run(state: PfcState, params: PfcParams, n_steps: int) -> PfcState:
+def pfc_run(state: PfcState, params: PfcParams, n_steps: int, realness: list | None = None) -> PfcState:
     """``n_steps`` steps enqueued back to back without host round trips (the
     hot loop): per-step diagnostics land in a device array that is read once
-    at the end.  Divergence is still reported with the index of the first
+    at the end (``realness`` collects each step's max|Im psi|/max|Re psi|).
+    Divergence is still reported with the index of the first
     non-finite step (the state has then advanced past it)."""
     n_steps = int(n_steps)
     if n_steps <= 0:
@@ -367,7 +372,7 @@ def pfc_run(state: PfcState, params: PfcParams, n_steps: int) -> PfcState:
     while s < n_steps:
         eng.launch(state, params, diag[s * per:(s + 1) * per])
         s += 1
-    _finish(state, params, diag.cpu().numpy(), first)
+    _finish(state, params, diag.cpu().numpy(), first, realness)
     return state
 
 
@@ -566,9 +571,101 @@ def initial_field(kind: str, grid: GridSpec, *, psi_bar: float = -0.3, seed: int
     return psi
 
 
+NOISE_CHUNK_BYTES = 1 << 27  # x-chunk of the streamed noise draw (128 MiB)
+
+
+def initial_field_slab(kind: str, grid: GridSpec, axis: int, start: int, stop: int, *,
+                       psi_bar: float = -0.3, seed: int = 0, noise_amplitude: float = 0.01,
+                       amplitude: float = 0.1, amplitude2: float | None = None, n_seeds: int = 5,
+                       seed_radius: float | None = None, on_incommensurate: str = "warn") -> np.ndarray:
+    """``initial_field(...)[slab]`` for planes [start, stop) of ``axis``,
+    bit-identical, without materialising the full grid:
+    the per-axis coordinate / cosine vectors are built over the whole axis
+    exactly as in ``initial_field`` and then sliced, the pointwise formulas
+    are elementwise, and the noise generator is streamed in x-chunks of the
+    full grid (the slowest axis, so the draw sequence is the one-shot
+    sequence) keeping only the slab's columns.  Memory: the slab plus one
+    ~128 MiB chunk, so a 2048^3 run never holds the 64 GiB field on a rank."""
+    kind = kind.lower()
+    if kind not in INIT_KINDS:
+        raise ValueError(f"unknown init kind {kind!r}; expected one of {INIT_KINDS}")
+    nx, ny, nz = grid.shape
+    sel = [slice(None)] * 3
+    sel[axis] = slice(start, stop)
+    sel = tuple(sel)
+    shape = list(grid.shape)
+    shape[axis] = stop - start
+    psi = np.full(tuple(shape), psi_bar, dtype=np.float64)
+    if kind == "constant_plus_noise":
+        gen = np.random.default_rng(seed)
+        if axis == 0:
+            # draws before the slab's x rows are consumed and discarded in chunks
+            row = ny * nz
+            x0 = 0
+            xc = max(1, NOISE_CHUNK_BYTES // (8 * row))
+            while x0 < start:
+                m = min(xc, start - x0)
+                gen.uniform(-noise_amplitude, noise_amplitude, (m, ny, nz))
+                x0 += m
+            return psi + gen.uniform(-noise_amplitude, noise_amplitude, tuple(shape))
+        noise = np.empty(tuple(shape), dtype=np.float64)
+        xc = max(1, NOISE_CHUNK_BYTES // (8 * ny * nz))
+        for x0 in range(0, nx, xc):
+            x1 = min(nx, x0 + xc)
+            blk = gen.uniform(-noise_amplitude, noise_amplitude, (x1 - x0, ny, nz))
+            noise[x0:x1] = blk[(slice(None),) + sel[1:]]
+        return psi + noise
+    x, y, z = _axes(grid)
+    cut = lambda v, a: v[sel] if a == axis else v  # noqa: E731
+    x, y, z = cut(x, 0), cut(y, 1), cut(z, 2)
+    a2 = amplitude if amplitude2 is None else amplitude2
+    if kind == "single_mode_triangular_2d":
+        if not grid.is_2d:
+            raise ValueError("single_mode_triangular_2d requires nz == 1")
+        _check_commensurate(grid, TRIANGULAR_Q, 0, on_incommensurate)
+        _check_commensurate(grid, TRIANGULAR_Q / math.sqrt(3.0), 1, on_incommensurate)
+        return psi + _triangular(x, y, amplitude)
+    if kind == "two_mode_fcc_3d":
+        if grid.is_2d:
+            raise ValueError("two_mode_fcc_3d requires nz > 1")
+        for ax in range(3):
+            _check_commensurate(grid, FCC_Q1, ax, on_incommensurate)
+        return psi + _fcc(x, y, z, amplitude, a2)
+    # seeded_crystallites: scalar draws per seed, elementwise envelopes
+    gen = np.random.default_rng(seed)
+    radius = seed_radius if seed_radius is not None else 0.15 * min(
+        grid.length[:2] if grid.is_2d else grid.length)
+    for _ in range(n_seeds):
+        c = [gen.uniform(0, grid.length[i]) for i in range(3)]
+        if grid.is_2d:
+            c[2] = 0.0
+            th = gen.uniform(0, 2 * math.pi)
+            cs, sn = math.cos(th), math.sin(th)
+            dx, dy = x - c[0], y - c[1]
+            prof = _triangular(cs * dx - sn * dy, sn * dx + cs * dy, amplitude)
+            r2 = dx**2 + dy**2
+        else:
+            rot = np.linalg.qr(gen.standard_normal((3, 3)))[0]
+            dx, dy, dz = x - c[0], y - c[1], z - c[2]
+            xr = rot[0, 0] * dx + rot[0, 1] * dy + rot[0, 2] * dz
+            yr = rot[1, 0] * dx + rot[1, 1] * dy + rot[1, 2] * dz
+            zr = rot[2, 0] * dx + rot[2, 1] * dy + rot[2, 2] * dz
+            prof = _fcc(xr, yr, zr, amplitude, a2)
+            r2 = dx**2 + dy**2 + dz**2
+        env = 0.5 * (1.0 - np.tanh((np.sqrt(r2) - radius) / max(radius * 0.2, 1e-12)))
+        psi = psi + env * np.broadcast_to(prof, tuple(shape))
+    return psi
+
+
 def init_condition(kind: str, grid: GridSpec, worker, *, real: bool = False, **kwargs) -> DistField:
-    """Initial density in the physical layout (pfc.py:301-310).  ``real=True``
-    keeps the slab float64 (R2C/C2R path)."""
-    full = initial_field(kind, grid, **kwargs)
-    return distfft.scatter(full, worker, grid, distfft.physical_layout(grid), Space.PHYSICAL,
-                           real=real)
+    """Initial density in the physical layout (pfc.py:301-310).  Each rank
+    builds only its own slab (``initial_field_slab``; bit-identical to the
+    reference's scatter of the replicated full field).  ``real=True`` keeps
+    the slab float64 (R2C/C2R path)."""
+    layout = distfft.physical_layout(grid)
+    lay = distfft.layout_for(grid, layout, worker.size)
+    r = worker.rank
+    part = initial_field_slab(kind, grid, lay.axis, lay.offsets[r], lay.offsets[r] + lay.counts[r], **kwargs)
+    dtype = np.float64 if real else np.complex128
+    return DistField(grid, layout, Space.PHYSICAL, np.ascontiguousarray(part, dtype=dtype),
+                     device=distfft._device_of(worker))
