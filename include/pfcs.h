@@ -47,6 +47,20 @@ int pfcs_device_count(int* count);
 int pfcs_fft_axis_c2c(const void* in, void* out, int64_t n0, int64_t n1, int64_t n2, int axis,
                       int forward, void* stream);
 
+/* ---- pfcs_fft_axis_c2c with a pointwise prologue fused into the pass: the
+ * products of hydro.hydro_psi_step / hydro_velocity_step (hydro.py:83-86,
+ * 100-103) that feed fftcore.fft_nd.  The pass reads `in`, applies
+ *   pro = 0: nothing (plain pfcs_fft_axis_c2c)
+ *   pro = 1: x*(x*x), complex, numpy order (psi**3, pfc.py:109 / hydro.py:86)
+ *   pro = 2: aux[idx] * x, aux complex128 of the same (n0, n1, n2) shape
+ *   pro = 3: i * d[k] * x, aux = float64 vector indexed by coordinate aux_axis
+ * and writes the transformed result to `out` (out != aux).  Bit-identical to
+ * pfcs_pfc_cube / pfcs_cmul / pfcs_mul_deriv into `out` followed by
+ * pfcs_fft_axis_c2c(out, out, ...); that two-kernel form is also what runs
+ * when no fused kernel applies (non-power-of-two lengths). */
+int pfcs_fft_axis_c2c_pro(const void* in, void* out, int64_t n0, int64_t n1, int64_t n2, int axis,
+                          int forward, int pro, const void* aux, int aux_axis, void* stream);
+
 /* ---- slab-pipeline z-line transforms: distfft.dist_fft_forward/inverse
  * (distfft.py:150-173) fused with distfft._exchange's concatenate/slice
  * (distfft.py:110-124).  `nlines` contiguous-z lines of length nz.  When

@@ -36,6 +36,7 @@ _SIGS = {
     "pfcs_last_error": [],
     "pfcs_device_count": [ctypes.POINTER(_c_int)],
     "pfcs_fft_axis_c2c": [_c_p, _c_p, _c_i64, _c_i64, _c_i64, _c_int, _c_int, _c_p],
+    "pfcs_fft_axis_c2c_pro": [_c_p, _c_p, _c_i64, _c_i64, _c_i64, _c_int, _c_int, _c_int, _c_p, _c_int, _c_p],
     "pfcs_fft_zlines": [_c_p, _c_p, _c_i64, _c_i64, _c_int, _c_int, _c_int, _c_p],
     "pfcs_fft_lines": [_c_p, _c_p, _c_i64, _c_i64, _c_i64, _c_int, _c_int, _c_int, _c_p],
     "pfcs_fft_zlines_to": [_c_p, _c_p, _c_i64, _c_i64, _c_int, _c_int, _c_int, _c_p],

@@ -19,6 +19,7 @@
 //                 accepts any N, SPEC sizes 1..16 and primes).
 #include "pfcs_fft.cuh"
 #include "pfcs_internal.h"
+#include "pfcs_pro.cuh"
 
 namespace pfcs {
 
@@ -27,10 +28,12 @@ struct Regs1 {
   double2 v[R];
 };
 
-template <int N, int T, int ST, bool FWD, bool BIN, bool BOUT>
+// PRO: a pointwise prologue (pfcs_pro.cuh) applied to each loaded element
+// before the transform (plain layouts only).
+template <int N, int T, int ST, bool FWD, bool BIN, bool BOUT, bool PRO = false>
 __global__ void __launch_bounds__(T*(N / radix_R(N)), min_blocks(T*(N / radix_R(N)), ST == 2 ? 640 : 1024))
     k_lines(const double2* in, double2* out, i64 nlines, SlabSplit sin, SlabSplit sout, PeerTable tout,
-            const double2* __restrict__ tw, double scale) {
+            const double2* __restrict__ tw, double scale, Pro pro = Pro{}) {
   constexpr int R = radix_R(N);
   constexpr int P = N / R;
   constexpr int LS = tile_ls(N, T, false);
@@ -60,6 +63,14 @@ __global__ void __launch_bounds__(T*(N / radix_R(N)), min_blocks(T*(N / radix_R(
   auto comp = [&](i64 tile, Regs1<R>& r) {
     const i64 l = tile * T + t;
     const int jj = opaque(j);
+    if constexpr (PRO) {  // lines run along z: (x, y) = (l / n1, l % n1)
+      const i64 lx = l / pro.n1;
+      const i64 ly = l - lx * pro.n1;
+      const i64 cl = pro.axis == 0 ? lx : ly;
+#pragma unroll
+      for (int e = 0; e < R; ++e)
+        r.v[e] = apply_pro(pro, r.v[e], l * N + jj + P * e, pro.axis == 2 ? (i64)(jj + P * e) : cl);
+    }
     fft_line<N, FWD>(r.v, jj, sl, tw);
     if (l < nlines) {
 #pragma unroll
@@ -264,7 +275,7 @@ static int blocked_dft(const double2* in, double2* out, i64 outer, int n, i64 in
 
 template <int N, bool FWD>
 static int lines_n(const double2* in, double2* out, i64 nlines, SlabSplitH si, SlabSplitH so,
-                   const PeerTable* dst, cudaStream_t st) {
+                   const PeerTable* dst, cudaStream_t st, const Pro* pro = nullptr) {
   const double2* tw = twiddles(N);
   if (!tw) return PFCS_E_CUDA;
   SlabSplit a{si.G, si.base, si.extra}, b{so.G, so.base, so.extra};
@@ -282,6 +293,16 @@ static int lines_n(const double2* in, double2* out, i64 nlines, SlabSplitH si, S
     } else {
     const size_t smem = (size_t)T * tile_ls(N, T, false) * sizeof(double2);
     const i64 ntiles = (nlines + T - 1) / T;
+    if (pro) {
+      if (bin || bout) return fail(PFCS_E_UNSUPPORTED, "prologue on a blocked line pass");
+      int grid = 0;
+      if (int rc = persistent_grid((const void*)k_lines<N, T, ST, FWD, false, false, true>, T * P, smem, ntiles,
+                                   &grid))
+        return rc;
+      k_lines<N, T, ST, FWD, false, false, true><<<grid, T * P, smem, st>>>(in, out, nlines, a, b, tab, tw, scale,
+                                                                           *pro);
+      return check_launch("k_lines(pro)");
+    }
     const void* f;
     if (bin && bout) f = (const void*)k_lines<N, T, ST, FWD, true, true>;
     else if (bin) f = (const void*)k_lines<N, T, ST, FWD, true, false>;
@@ -370,6 +391,26 @@ int launch_lines_to(const double2* in, double2* out, long long nlines, int n, in
       break;
   }
   return fail(PFCS_E_UNSUPPORTED, "unsupported line length");
+}
+
+// Plain contiguous lines with a fused prologue; returns 1 when not
+// applicable (non-power-of-two length).
+int launch_lines_pro(const double2* in, double2* out, long long nlines, int n, const Pro& pro, bool forward,
+                     cudaStream_t st) {
+  if (nlines <= 0) return PFCS_OK;
+  if (!is_pow2(n) || n > 4096 || n < 2) return 1;
+  const SlabSplitH one = slab_split(n, 1);
+  switch (n) {
+#define PFCS_CASE(NN) \
+  case NN:            \
+    return forward ? lines_n<NN, true>(in, out, nlines, one, one, nullptr, st, &pro)  \
+                   : lines_n<NN, false>(in, out, nlines, one, one, nullptr, st, &pro);
+    PFCS_POW2_CASES(PFCS_CASE)
+#undef PFCS_CASE
+    default:
+      break;
+  }
+  return 1;
 }
 
 int launch_strided_c2c(const double2* in, double2* out, long long outer, int n, long long inner,

@@ -36,8 +36,12 @@ bool make_tmap(CUtensorMap* map, int rank, const void* base, const unsigned long
                const unsigned long long* strides_bytes, const unsigned* box);
 struct SlabSplitH;
 struct PeerTable;
+struct Pro;
 int launch_strided_tma(const double2* in, double2* out, long long outer, int n, long long inner, bool forward,
-                       cudaStream_t st, const SlabSplitH* souter = nullptr, const PeerTable* dst = nullptr);
+                       cudaStream_t st, const SlabSplitH* souter = nullptr, const PeerTable* dst = nullptr,
+                       const Pro* pro = nullptr);
+int launch_lines_pro(const double2* in, double2* out, long long nlines, int n, const Pro& pro, bool forward,
+                     cudaStream_t st);
 
 // Opt a kernel in to > 48 KB dynamic shared memory once.
 int ensure_smem(const void* func, size_t bytes);

@@ -12,6 +12,7 @@
 // stage is read into registers in the exact order k_strided loads them and
 // the FFT code is shared, so results are bit-identical to k_strided.
 #include "pfcs_internal.h"
+#include "pfcs_pro.cuh"
 #include "pfcs_tma.cuh"
 
 namespace pfcs {
@@ -30,11 +31,12 @@ struct TmaCfg {
 
 // OPEER: outer row o goes to tout.p[h][(o - ooff_h) ...] (the fused
 // transpose of the slab pipeline: souter splits the outer axis over ranks).
-template <int N, int T, bool FWD, bool OPEER = false>
+// PRO: pointwise prologue (pfcs_pro.cuh) on each element read from the stage.
+template <int N, int T, bool FWD, bool OPEER = false, bool PRO = false>
 __global__ void __launch_bounds__(T*(N / radix_R(N)), 1)
     k_strided_tma(const __grid_constant__ CUtensorMap map, double2* out, i64 outer, i64 inner, i64 tpo,
                   const double2* __restrict__ tw, double scale, SlabSplit souter = SlabSplit{},
-                  PeerTable tout = PeerTable{}) {
+                  PeerTable tout = PeerTable{}, Pro pro = Pro{}) {
   using C = TmaCfg<N, T>;
   constexpr int R = C::R;
   constexpr int P = C::P;
@@ -86,6 +88,22 @@ __global__ void __launch_bounds__(T*(N / radix_R(N)), 1)
     const i64 o = tile / tpo;
     const i64 i = (tile - o * tpo) * T + t;
     const int jj = opaque(j);
+    if constexpr (PRO) {
+      if (i < inner) {
+        // element (o, n, i) of the (outer, N, inner) view of the (n0, n1, n2)
+        // grid; PRO_DERIV (not on the hydro hot path here) decodes its
+        // coordinate from the flat index
+#pragma unroll
+        for (int e = 0; e < R; ++e) {
+          const i64 idx = (o * N + jj + P * e) * inner + i;
+          i64 c = 0;
+          if (pro.kind == PRO_DERIV)
+            c = pro.axis == 2 ? idx % pro.n2
+                              : (pro.axis == 1 ? (idx / pro.n2) % pro.n1 : idx / ((i64)pro.n2 * pro.n1));
+          v[e] = apply_pro(pro, v[e], idx, c);
+        }
+      }
+    }
     fft_line<N, FWD>(v, jj, sl, tw);
     if (i < inner) {
       double2* dst;
@@ -163,7 +181,8 @@ static int tma_tile_width(int dflt) {
 
 template <int N, int T, bool FWD>
 static int strided_tma_nt(const double2* in, double2* out, i64 outer, i64 inner, cudaStream_t st,
-                          const SlabSplitH* souter = nullptr, const PeerTable* dst = nullptr) {
+                          const SlabSplitH* souter = nullptr, const PeerTable* dst = nullptr,
+                          const Pro* pro = nullptr) {
   using C = TmaCfg<N, T>;
   if constexpr (C::SMEM > 227 * 1024 || T * C::P > 1024) {
     return 1;  // not applicable
@@ -183,6 +202,14 @@ static int strided_tma_nt(const double2* in, double2* out, i64 outer, i64 inner,
     if (!tw) return PFCS_E_CUDA;
     const i64 tpo = (inner + T - 1) / T;
     int grid = 0;
+    if (pro) {
+      if (int rc = persistent_grid((const void*)k_strided_tma<N, T, FWD, false, true>, T * C::P, C::SMEM,
+                                   outer * tpo, &grid))
+        return rc;
+      k_strided_tma<N, T, FWD, false, true><<<grid, T * C::P, C::SMEM, st>>>(
+          map, out, outer, inner, tpo, tw, 1.0 / (double)N, SlabSplit{}, PeerTable{}, *pro);
+      return check_launch("k_strided_tma(pro)");
+    }
     if (dst) {
       const SlabSplit so{souter->G, souter->base, souter->extra};
       if (int rc = persistent_grid((const void*)k_strided_tma<N, T, FWD, true>, T * C::P, C::SMEM, outer * tpo, &grid))
@@ -200,25 +227,25 @@ static int strided_tma_nt(const double2* in, double2* out, i64 outer, i64 inner,
 
 template <int N, bool FWD>
 static int strided_tma_n(const double2* in, double2* out, i64 outer, i64 inner, cudaStream_t st,
-                         const SlabSplitH* so = nullptr, const PeerTable* dst = nullptr) {
+                         const SlabSplitH* so = nullptr, const PeerTable* dst = nullptr, const Pro* pro = nullptr) {
   switch (tma_tile_width(N >= 1024 ? 4 : 8)) {
-    case 1: return strided_tma_nt<N, 1, FWD>(in, out, outer, inner, st, so, dst);
-    case 2: return strided_tma_nt<N, 2, FWD>(in, out, outer, inner, st, so, dst);
-    case 4: return strided_tma_nt<N, 4, FWD>(in, out, outer, inner, st, so, dst);
-    default: return strided_tma_nt<N, 8, FWD>(in, out, outer, inner, st, so, dst);
+    case 1: return strided_tma_nt<N, 1, FWD>(in, out, outer, inner, st, so, dst, pro);
+    case 2: return strided_tma_nt<N, 2, FWD>(in, out, outer, inner, st, so, dst, pro);
+    case 4: return strided_tma_nt<N, 4, FWD>(in, out, outer, inner, st, so, dst, pro);
+    default: return strided_tma_nt<N, 8, FWD>(in, out, outer, inner, st, so, dst, pro);
   }
 }
 
 // Returns PFCS_OK / an error code, or 1 when the TMA path does not apply
 // (the caller then runs k_strided).
 int launch_strided_tma(const double2* in, double2* out, long long outer, int n, long long inner, bool forward,
-                       cudaStream_t st, const SlabSplitH* souter, const PeerTable* dst) {
+                       cudaStream_t st, const SlabSplitH* souter, const PeerTable* dst, const Pro* pro) {
   if (((uintptr_t)in & 15) || inner < 1 || 2 * inner >= (1LL << 31) || outer >= (1LL << 31)) return 1;
   switch (n) {
 #define PFCS_TMA_CASE(NN)                                                            \
   case NN:                                                                           \
-    return forward ? strided_tma_n<NN, true>(in, out, outer, inner, st, souter, dst) \
-                   : strided_tma_n<NN, false>(in, out, outer, inner, st, souter, dst);
+    return forward ? strided_tma_n<NN, true>(in, out, outer, inner, st, souter, dst, pro) \
+                   : strided_tma_n<NN, false>(in, out, outer, inner, st, souter, dst, pro);
     PFCS_TMA_CASE(64)
     PFCS_TMA_CASE(128)
     PFCS_TMA_CASE(256)

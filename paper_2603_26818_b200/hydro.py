@@ -89,18 +89,41 @@ def _out(t: torch.Tensor, host: bool):
     return t.cpu().numpy() if host else t
 
 
-def _fft(t: torch.Tensor, forward: bool) -> torch.Tensor:
+PRO_CUBE, PRO_CMUL, PRO_DERIV = 1, 2, 3  # fused prologues (include/pfcs.h pfcs_fft_axis_c2c_pro)
+
+
+def _fft(t: torch.Tensor, forward: bool, pro: int = 0, aux=None, aux_axis: int = 0) -> torch.Tensor:
     """Full-grid 3D transform, one libpfcs pass per axis (orders as
-    fftcore.fft_nd: forward 0,1,2; inverse 2,1,0)."""
+    fftcore.fft_nd: forward 0,1,2; inverse 2,1,0).  ``pro`` fuses a pointwise
+    product into the first pass: F(t^3), F(aux * t), F^-1(i d_axis t)."""
     out = torch.empty_like(t)
     n0, n1, n2 = t.shape
     st = nat.stream_ptr()
     order = (0, 1, 2) if forward else (2, 1, 0)
     src = t
-    for ax in order:
-        nat.call("pfcs_fft_axis_c2c", nat.ptr(src), nat.ptr(out), n0, n1, n2, ax, 1 if forward else 0, st)
+    for k, ax in enumerate(order):
+        if k == 0 and pro:
+            nat.call("pfcs_fft_axis_c2c_pro", nat.ptr(src), nat.ptr(out), n0, n1, n2, ax, 1 if forward else 0,
+                     pro, nat.ptr(aux) if aux is not None else None, aux_axis, st)
+        else:
+            nat.call("pfcs_fft_axis_c2c", nat.ptr(src), nat.ptr(out), n0, n1, n2, ax, 1 if forward else 0, st)
         src = out
     return out
+
+
+def _fft_cube(ps: torch.Tensor) -> torch.Tensor:
+    """F(psi**3) with the cube fused into the first (x) pass."""
+    return _fft(ps, True, PRO_CUBE)
+
+
+def _fft_cmul(a: torch.Tensor, g: torch.Tensor) -> torch.Tensor:
+    """F(a * g) with the product fused into the first (x) pass."""
+    return _fft(g, True, PRO_CMUL, a)
+
+
+def _ifft_deriv(x_hat: torch.Tensor, axis: int, sym) -> torch.Tensor:
+    """F^-1(i k_axis x_hat) with the multiplier fused into the first (z) pass."""
+    return _fft(x_hat, False, PRO_DERIV, _vectors(sym, x_hat.device)[3 + axis], axis)
 
 
 def _cube(t: torch.Tensor) -> torch.Tensor:
@@ -164,12 +187,12 @@ def hydro_psi_step(psi_hat, psi, v1, v2, v3, sym: SymbolTable, params: HydroPara
     kx, ky, kz = _vectors(sym, dev)[:3]
     n0, n1, n2 = ph.shape
     st = nat.stream_ptr()
-    xs = [_fft(_mul_deriv(ph, ax, None, sym), False) for ax in range(3)]
+    xs = [_ifft_deriv(ph, ax, sym) for ax in range(3)]
     adv = torch.empty_like(ph)
     nat.call("pfcs_hydro_advect", nat.ptr(vs[0]), nat.ptr(xs[0]), nat.ptr(vs[1]), nat.ptr(xs[1]),
              nat.ptr(vs[2]), nat.ptr(xs[2]), nat.ptr(adv), adv.numel(), st)
     del xs
-    nl_hat = _fft(_cube(ps), True)
+    nl_hat = _fft_cube(ps)
     adv_hat = _fft(adv, True)
     new = ph.clone()
     diag = _Diag(dev)
@@ -194,16 +217,17 @@ def hydro_velocity_step(v_hat, psi, d_axis, sym: SymbolTable, params: HydroParam
     n0, n1, n2 = vh.shape
     st = nat.stream_ptr()
     axis = _deriv_axis(d_axis, sym)
-    nl_hat = _fft(_cube(ps), True)
+    nl_hat = _fft_cube(ps)
     f_hat = _fft(ps, True)
     mu_hat = torch.empty_like(vh)
     nat.call("pfcs_hydro_mu", nat.ptr(nl_hat), nat.ptr(f_hat), nat.ptr(mu_hat), n0, n1, n2,
              nat.ptr(kx), nat.ptr(ky), nat.ptr(kz), float(sym.eps), st)
     del nl_hat, f_hat
-    g = _fft(_mul_deriv(mu_hat, axis, d_axis, sym), False)
-    prod = torch.empty_like(vh)
-    nat.call("pfcs_cmul", nat.ptr(ps), nat.ptr(g), nat.ptr(prod), prod.numel(), st)
-    force = _fft(prod, True)
+    if axis is not None:
+        g = _ifft_deriv(mu_hat, axis, sym)
+    else:
+        g = _fft(_mul_deriv(mu_hat, axis, d_axis, sym), False)
+    force = _fft_cmul(ps, g)  # F(psi * g), product fused into the first pass
     dt, rho = float(params.pfc.dt), float(params.rho)
     new = vh.clone()
     diag = _Diag(dev)

@@ -38,7 +38,7 @@ import torch
 
 from . import _native as nat
 from .grid import SymbolTable
-from .hydro import (HydroParams, TAG_PSI, V_TAGS, _cube, _dev, _Diag, _fft, _mul_deriv, _out,
+from .hydro import (HydroParams, TAG_PSI, V_TAGS, _dev, _Diag, _fft, _fft_cmul, _fft_cube, _ifft_deriv, _out,
                     _raise_divergence, _vectors)
 
 __all__ = [
@@ -96,7 +96,7 @@ def _st():
 
 def _adv_product(x_hat: torch.Tensor, axis: int, v: torch.Tensor, sym) -> torch.Tensor:
     """v_axis * F^-1(d_axis * x_hat) (one term of v . grad x)."""
-    g = _fft(_mul_deriv(x_hat, axis, None, sym), False)
+    g = _ifft_deriv(x_hat, axis, sym)
     p = torch.empty_like(g)
     nat.call("pfcs_cmul", nat.ptr(v), nat.ptr(g), nat.ptr(p), p.numel(), _st())
     return p
@@ -115,7 +115,7 @@ def density_step(psi_hat, psi, products, sym: SymbolTable, params: MultiParams, 
     dev = ph.device
     kx, ky, kz = _vectors(sym, dev)[:3]
     n0, n1, n2 = ph.shape
-    nl_hat = _fft(_cube(ps), True)
+    nl_hat = _fft_cube(ps)
     adv_hat = _fft(_sum3(*products), True)
     new = ph.clone()
     diag = _Diag(dev)
@@ -158,13 +158,13 @@ def velocity_step(v_hat, psi, axis: int, sym: SymbolTable, params: MultiParams, 
     kx, ky, kz = _vectors(sym, dev)[:3]
     n0, n1, n2 = vh.shape
     st = _st()
-    nl_hat = _fft(_cube(ps), True)
+    nl_hat = _fft_cube(ps)
     f_hat = _fft(ps, True)
     mu_hat = torch.empty_like(vh)
     nat.call("pfcs_hydro_mu", nat.ptr(nl_hat), nat.ptr(f_hat), nat.ptr(mu_hat), n0, n1, n2, nat.ptr(kx),
              nat.ptr(ky), nat.ptr(kz), float(sym.eps), st)
     del nl_hat, f_hat
-    force = _fft(_adv_product(mu_hat, axis, ps, sym), True)
+    force = _fft_cmul(ps, _ifft_deriv(mu_hat, axis, sym))  # F(psi * F^-1(i k mu_hat)), both fused
     if params.beta != 0.0:
         cc, chh = _dev(c), _dev(c_hat)
         fc = torch.empty_like(cc)
@@ -173,7 +173,7 @@ def velocity_step(v_hat, psi, axis: int, sym: SymbolTable, params: MultiParams, 
         muc = torch.empty_like(fc_hat)
         nat.call("pfcs_ch_mu", nat.ptr(fc_hat), nat.ptr(chh), nat.ptr(muc), n0, n1, n2, nat.ptr(kx), nat.ptr(ky),
                  nat.ptr(kz), float(params.kappa), st)
-        force_c = _fft(_adv_product(muc, axis, cc, sym), True)
+        force_c = _fft_cmul(cc, _ifft_deriv(muc, axis, sym))
         total = torch.empty_like(force)
         nat.call("pfcs_axpy", nat.ptr(force), nat.ptr(force_c), nat.ptr(total), total.numel(),
                  float(params.beta), st)
