@@ -224,6 +224,31 @@ int pfcs_apply_op(const void* in, void* out, int64_t cx, int64_t ny, int64_t nz,
 /* Scratch bytes pfcs_energy_sum needs for n elements. */
 int64_t pfcs_energy_scratch_bytes(int64_t n);
 
+/* ---- single-GPU plan API: the whole hot path from C without Python.
+ * A plan describes one real (nx, ny, nz) C-order fp64 grid on the current
+ * device (2D grids: pass (nx, 1, ny)); the spectrum is the R2C half
+ * spectrum (nx/2+1, ny, nz) complex128, C order, numpy's rfftn layout
+ * along x.  Same arithmetic and launch sequence as distfft.forward/inverse
+ * and pfc.pfc_run at one rank (distfft.py:150-173, pfc.py:96-128), so the
+ * results are bit-identical to the Python path.  Needs power-of-two nx >= 4
+ * and nz <= 4096 (else PFCS_E_UNSUPPORTED at create).
+ *   fwd:  in (real, read only) -> out (spectrum)
+ *   inv:  in (spectrum, read only) -> out (real); work >= spectral_elems
+ *   pfc_steps: nsteps fused semi-implicit PFC steps on psi_hat in place;
+ *         kx (nx/2+1), ky (ny), kz (nz) are the 1D wavenumbers
+ *         (grid.wavenumbers), diag (nullable) receives nsteps x
+ *         PFCS_DIAG_SLOTS x 4 per-step diagnostics (zeroed here), work >=
+ *         spectral_elems complex128. */
+typedef struct pfcs_plan pfcs_plan;
+int pfcs_plan_create(int64_t nx, int64_t ny, int64_t nz, pfcs_plan** plan);
+int pfcs_plan_destroy(pfcs_plan* plan);
+int64_t pfcs_plan_spectral_elems(const pfcs_plan* plan);
+int pfcs_plan_fwd(const pfcs_plan* plan, const double* in, void* out, void* stream);
+int pfcs_plan_inv(const pfcs_plan* plan, const void* in, double* out, void* work, void* stream);
+int pfcs_plan_pfc_steps(const pfcs_plan* plan, void* psi_hat, const double* kx, const double* ky,
+                        const double* kz, double eps, double dt, int64_t nsteps, double* diag, void* work,
+                        void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -37,6 +37,12 @@ _SIGS = {
     "pfcs_device_count": [ctypes.POINTER(_c_int)],
     "pfcs_fft_axis_c2c": [_c_p, _c_p, _c_i64, _c_i64, _c_i64, _c_int, _c_int, _c_p],
     "pfcs_fft_axis_c2c_pro": [_c_p, _c_p, _c_i64, _c_i64, _c_i64, _c_int, _c_int, _c_int, _c_p, _c_int, _c_p],
+    "pfcs_plan_create": [_c_i64, _c_i64, _c_i64, _c_p],
+    "pfcs_plan_destroy": [_c_p],
+    "pfcs_plan_fwd": [_c_p, _c_p, _c_p, _c_p],
+    "pfcs_plan_inv": [_c_p, _c_p, _c_p, _c_p, _c_p],
+    "pfcs_plan_pfc_steps": [_c_p, _c_p, _c_p, _c_p, _c_p, _c_d, _c_d, _c_i64, _c_p, _c_p, _c_p],
+    "pfcs_plan_spectral_elems": [_c_p],
     "pfcs_fft_zlines": [_c_p, _c_p, _c_i64, _c_i64, _c_int, _c_int, _c_int, _c_p],
     "pfcs_fft_lines": [_c_p, _c_p, _c_i64, _c_i64, _c_i64, _c_int, _c_int, _c_int, _c_p],
     "pfcs_fft_zlines_to": [_c_p, _c_p, _c_i64, _c_i64, _c_int, _c_int, _c_int, _c_p],
@@ -76,7 +82,8 @@ _SIGS = {
     "pfcs_absmax": [_c_p, _c_i64, _c_i64, _c_p, _c_p],
     "pfcs_apply_op": [_c_p, _c_p, _c_i64, _c_i64, _c_i64, _c_p, _c_p, _c_p, _c_d, _c_p],
 }
-_RESTYPE = {"pfcs_last_error": ctypes.c_char_p, "pfcs_energy_scratch_bytes": _c_i64}
+_RESTYPE = {"pfcs_last_error": ctypes.c_char_p, "pfcs_energy_scratch_bytes": _c_i64,
+            "pfcs_plan_spectral_elems": _c_i64}
 
 _lib = None
 _lock = threading.Lock()
@@ -131,7 +138,8 @@ def check(rc: int, what: str) -> None:
 # events recorded on the current stream around the launch.
 launches = 0
 trace: list | None = None
-_NO_LAUNCH = {"pfcs_version", "pfcs_last_error", "pfcs_device_count", "pfcs_energy_scratch_bytes"}
+_NO_LAUNCH = {"pfcs_version", "pfcs_last_error", "pfcs_device_count", "pfcs_energy_scratch_bytes",
+              "pfcs_plan_create", "pfcs_plan_destroy", "pfcs_plan_spectral_elems"}
 
 
 def call(name: str, *args) -> None:

@@ -419,3 +419,74 @@ int pfcs_apply_op(const void* in, void* out, int64_t cx, int64_t ny, int64_t nz,
 }
 
 }  // extern "C"
+
+// ------------------------------------------------------------ plan API ----
+struct pfcs_plan {
+  int64_t nx, ny, nz, nh;
+};
+
+extern "C" {
+
+int pfcs_plan_create(int64_t nx, int64_t ny, int64_t nz, pfcs_plan** plan) {
+  if (!plan) return fail(PFCS_E_ARG, "plan out-pointer is null");
+  *plan = nullptr;
+  if (nx < 4 || ny < 1 || nz < 1) return fail(PFCS_E_ARG, "bad grid");
+  if (!is_pow2(nx) || nx > 8192) return fail(PFCS_E_UNSUPPORTED, "plan needs a power-of-two nx in [4, 8192]");
+  if (!is_pow2(nz) || nz > 4096) return fail(PFCS_E_UNSUPPORTED, "plan needs a power-of-two nz <= 4096");
+  *plan = new pfcs_plan{nx, ny, nz, nx / 2 + 1};
+  return PFCS_OK;
+}
+
+int pfcs_plan_destroy(pfcs_plan* plan) {
+  delete plan;
+  return PFCS_OK;
+}
+
+int64_t pfcs_plan_spectral_elems(const pfcs_plan* p) { return p ? p->nh * p->ny * p->nz : -1; }
+
+int pfcs_plan_fwd(const pfcs_plan* p, const double* in, void* out, void* stream) {
+  if (!p || !in || !out) return fail(PFCS_E_ARG, "null argument");
+  // x (R2C), y in place, z in place: distfft._forward_core at G = 1
+  if (int rc = pfcs_rfft_x(in, out, p->nx, p->ny * p->nz, stream)) return rc;
+  if (p->ny > 1)
+    if (int rc = pfcs_fft_axis_c2c(out, out, p->nh, p->ny, p->nz, 1, 1, stream)) return rc;
+  return pfcs_fft_zlines(out, out, p->nh * p->ny, p->nz, 1, 1, 1, stream);
+}
+
+int pfcs_plan_inv(const pfcs_plan* p, const void* in, double* out, void* work, void* stream) {
+  if (!p || !in || !out || !work) return fail(PFCS_E_ARG, "null argument");
+  // z (into work), y in place, x (C2R): distfft._inverse_core at G = 1
+  if (int rc = pfcs_fft_zlines(in, work, p->nh * p->ny, p->nz, 1, 1, 0, stream)) return rc;
+  if (p->ny > 1)
+    if (int rc = pfcs_fft_axis_c2c(work, work, p->nh, p->ny, p->nz, 1, 0, stream)) return rc;
+  return pfcs_irfft_x(work, out, p->nx, p->ny * p->nz, stream);
+}
+
+int pfcs_plan_pfc_steps(const pfcs_plan* p, void* psi_hat, const double* kx, const double* ky, const double* kz,
+                        double eps, double dt, int64_t nsteps, double* diag, void* work, void* stream) {
+  if (!p || !psi_hat || !kx || !ky || !kz || !work) return fail(PFCS_E_ARG, "null argument");
+  if (nsteps < 0) return fail(PFCS_E_ARG, "negative step count");
+  if (nsteps == 0) return PFCS_OK;
+  const size_t per = (size_t)PFCS_DIAG_SLOTS * 4;
+  if (diag)
+    if (int rc = check_cuda(cudaMemsetAsync(diag, 0, (size_t)nsteps * per * sizeof(double), S(stream)), "memset"))
+      return rc;
+  // pfc._StepEngine.launch, fused G = 1: work holds the z-inverse of psi_hat
+  // (the update kernel leaves the next step's in it)
+  const int64_t lines = p->nh * p->ny;
+  if (int rc = pfcs_fft_zlines(psi_hat, work, lines, p->nz, 1, 1, 0, stream)) return rc;
+  for (int64_t s = 0; s < nsteps; ++s) {
+    double* d = diag ? diag + s * per : nullptr;
+    if (p->ny > 1)
+      if (int rc = pfcs_fft_axis_c2c(work, work, p->nh, p->ny, p->nz, 1, 0, stream)) return rc;
+    if (int rc = pfcs_pfc_cube_x(work, p->nx, p->ny * p->nz, 1, d, stream)) return rc;
+    if (p->ny > 1)
+      if (int rc = pfcs_fft_axis_c2c(work, work, p->nh, p->ny, p->nz, 1, 1, stream)) return rc;
+    if (int rc = pfcs_pfc_update_z(work, psi_hat, work, p->nh, p->ny, p->nz, 1, 1, kx, ky, kz, eps, dt, d, stream))
+      return rc;
+  }
+  return PFCS_OK;
+}
+
+}  // extern "C"
+
