@@ -205,8 +205,20 @@ def hydro_psi_step(psi_hat, psi, v1, v2, v3, sym: SymbolTable, params: HydroPara
     return _out(new, host), _out(new_psi, host)
 
 
+def _mu_hat(ps: torch.Tensor, sym: SymbolTable) -> torch.Tensor:
+    """mu_hat = F[psi^3] + op F[psi] (hydro.py:96-97)."""
+    kx, ky, kz = _vectors(sym, ps.device)[:3]
+    n0, n1, n2 = ps.shape
+    nl_hat = _fft_cube(ps)
+    f_hat = _fft(ps, True)
+    mu_hat = torch.empty_like(ps)
+    nat.call("pfcs_hydro_mu", nat.ptr(nl_hat), nat.ptr(f_hat), nat.ptr(mu_hat), n0, n1, n2,
+             nat.ptr(kx), nat.ptr(ky), nat.ptr(kz), float(sym.eps), nat.stream_ptr())
+    return mu_hat
+
+
 def hydro_velocity_step(v_hat, psi, d_axis, sym: SymbolTable, params: HydroParams,
-                        step_index: int = 0):
+                        step_index: int = 0, *, mu_hat=None):
     """Viscous decay plus Gaussian-smoothed thermodynamic force on one
     velocity component (hydro.py:93-107); ``d_axis`` is sym.d1/d2/d3 (or
     the axis index).  Returns (v_hat, v) as new arrays."""
@@ -217,12 +229,8 @@ def hydro_velocity_step(v_hat, psi, d_axis, sym: SymbolTable, params: HydroParam
     n0, n1, n2 = vh.shape
     st = nat.stream_ptr()
     axis = _deriv_axis(d_axis, sym)
-    nl_hat = _fft_cube(ps)
-    f_hat = _fft(ps, True)
-    mu_hat = torch.empty_like(vh)
-    nat.call("pfcs_hydro_mu", nat.ptr(nl_hat), nat.ptr(f_hat), nat.ptr(mu_hat), n0, n1, n2,
-             nat.ptr(kx), nat.ptr(ky), nat.ptr(kz), float(sym.eps), st)
-    del nl_hat, f_hat
+    if mu_hat is None:  # shared by the three components in serial mode
+        mu_hat = _mu_hat(ps, sym)
     if axis is not None:
         g = _ifft_deriv(mu_hat, axis, sym)
     else:
@@ -245,9 +253,11 @@ def serial_hydro_step(fields: HydroFields, sym: SymbolTable, params: HydroParams
     first with the previous velocities, then v1..v3 with the fresh density."""
     fields.psi_hat, fields.psi = hydro_psi_step(fields.psi_hat, fields.psi, *fields.v, sym, params,
                                                 step_index=fields.step_index)
+    ps = _dev(fields.psi)
+    mu_hat = _mu_hat(ps, sym)  # the three components share it
     for i in range(3):
-        fields.v_hat[i], fields.v[i] = hydro_velocity_step(fields.v_hat[i], fields.psi, i, sym, params,
-                                                           step_index=fields.step_index)
+        fields.v_hat[i], fields.v[i] = hydro_velocity_step(fields.v_hat[i], ps, i, sym, params,
+                                                           step_index=fields.step_index, mu_hat=mu_hat)
     fields.step_index += 1
     fields.sim_time += params.pfc.dt
     return fields

@@ -150,29 +150,52 @@ def composition_step(c_hat, c, v, sym: SymbolTable, params: MultiParams, step_in
     return new, _fft(new, False)
 
 
+def density_mu(psi, sym: SymbolTable) -> torch.Tensor:
+    """mu_hat = F[psi^3] + op F[psi] (hydro.py:96-97): the chemical potential
+    every velocity component's force is built from."""
+    ps = _dev(psi)
+    kx, ky, kz = _vectors(sym, ps.device)[:3]
+    n0, n1, n2 = ps.shape
+    nl_hat = _fft_cube(ps)
+    f_hat = _fft(ps, True)
+    mu_hat = torch.empty_like(ps)
+    nat.call("pfcs_hydro_mu", nat.ptr(nl_hat), nat.ptr(f_hat), nat.ptr(mu_hat), n0, n1, n2, nat.ptr(kx),
+             nat.ptr(ky), nat.ptr(kz), float(sym.eps), _st())
+    return mu_hat
+
+
+def composition_mu(c, c_hat, sym: SymbolTable, params: MultiParams) -> torch.Tensor:
+    """mu_c = F[f'(c)] + kappa k^2 c_hat, the composition force's potential."""
+    cc, chh = _dev(c), _dev(c_hat)
+    kx, ky, kz = _vectors(sym, cc.device)[:3]
+    n0, n1, n2 = cc.shape
+    st = _st()
+    fc = torch.empty_like(cc)
+    nat.call("pfcs_ch_nonlin", nat.ptr(cc), nat.ptr(fc), fc.numel(), float(params.alpha), st)
+    fc_hat = _fft(fc, True)
+    muc = torch.empty_like(fc_hat)
+    nat.call("pfcs_ch_mu", nat.ptr(fc_hat), nat.ptr(chh), nat.ptr(muc), n0, n1, n2, nat.ptr(kx), nat.ptr(ky),
+             nat.ptr(kz), float(params.kappa), st)
+    return muc
+
+
 def velocity_step(v_hat, psi, axis: int, sym: SymbolTable, params: MultiParams, c=None, c_hat=None,
-                  step_index=0):
-    """hydro_velocity_step (hydro.py:93-107) plus beta * F[c d_axis mu_c]."""
+                  step_index=0, *, mu_hat=None, mu_c=None):
+    """hydro_velocity_step (hydro.py:93-107) plus beta * F[c d_axis mu_c].
+    ``mu_hat`` / ``mu_c`` (from density_mu / composition_mu) may be passed in
+    when several components are advanced from the same fields (serial mode
+    computes them once per step instead of once per component)."""
     vh, ps = _dev(v_hat), _dev(psi)
     dev = vh.device
     kx, ky, kz = _vectors(sym, dev)[:3]
     n0, n1, n2 = vh.shape
     st = _st()
-    nl_hat = _fft_cube(ps)
-    f_hat = _fft(ps, True)
-    mu_hat = torch.empty_like(vh)
-    nat.call("pfcs_hydro_mu", nat.ptr(nl_hat), nat.ptr(f_hat), nat.ptr(mu_hat), n0, n1, n2, nat.ptr(kx),
-             nat.ptr(ky), nat.ptr(kz), float(sym.eps), st)
-    del nl_hat, f_hat
+    if mu_hat is None:
+        mu_hat = density_mu(ps, sym)
     force = _fft_cmul(ps, _ifft_deriv(mu_hat, axis, sym))  # F(psi * F^-1(i k mu_hat)), both fused
     if params.beta != 0.0:
-        cc, chh = _dev(c), _dev(c_hat)
-        fc = torch.empty_like(cc)
-        nat.call("pfcs_ch_nonlin", nat.ptr(cc), nat.ptr(fc), fc.numel(), float(params.alpha), st)
-        fc_hat = _fft(fc, True)
-        muc = torch.empty_like(fc_hat)
-        nat.call("pfcs_ch_mu", nat.ptr(fc_hat), nat.ptr(chh), nat.ptr(muc), n0, n1, n2, nat.ptr(kx), nat.ptr(ky),
-                 nat.ptr(kz), float(params.kappa), st)
+        cc = _dev(c)
+        muc = mu_c if mu_c is not None else composition_mu(cc, c_hat, sym, params)
         force_c = _fft_cmul(cc, _ifft_deriv(muc, axis, sym))
         total = torch.empty_like(force)
         nat.call("pfcs_axpy", nat.ptr(force), nat.ptr(force_c), nat.ptr(total), total.numel(),
@@ -200,9 +223,12 @@ def serial_multi_step(fields: MultiFields, sym: SymbolTable, params: MultiParams
     psi_hat, psi = density_step(ph, fields.psi, prods, sym, params, fields.step_index)
     del prods
     c_hat, c = composition_step(fields.c_hat, fields.c, vs, sym, params, fields.step_index)
+    # the three components share mu_hat (and mu_c): computed once
+    mu_hat = density_mu(psi, sym)
+    mu_c = composition_mu(c, c_hat, sym, params) if params.beta != 0.0 else None
     for i in range(3):
         vh, v = velocity_step(fields.v_hat[i], psi, i, sym, params, c=c, c_hat=c_hat,
-                              step_index=fields.step_index)
+                              step_index=fields.step_index, mu_hat=mu_hat, mu_c=mu_c)
         fields.v_hat[i], fields.v[i] = _out(vh, host), _out(v, host)
     fields.psi_hat, fields.psi = _out(psi_hat, host), _out(psi, host)
     fields.c_hat, fields.c = _out(c_hat, host), _out(c, host)
