@@ -233,62 +233,9 @@ __device__ __forceinline__ void stash_line(const double2 (&v)[R], int j, double2
   for (int e = 0; e < R; ++e) sl[pad_idx(j + P * e)] = v[e];
 }
 
-// ------------------------------------------------ asynchronous tile loads --
-// Every pass kernel is persistent and double-buffered: while a CTA runs the
-// FFT of tile i out of shared buffer i&1, the cp.async (LDGSTS) copies of
-// tile i+1 are already in flight into the other buffer, so the HBM pipe
-// never idles during the butterflies.  Each thread lands its own R elements
-// at their padded positions, which is exactly where the first Stockham pass
-// reads them.
+// ------------------------------------------------------ tile pipelines --
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
   return (unsigned)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void cp_async16(void* dst, const void* src, bool valid) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(dst)), "l"(src),
-               "r"(valid ? 16 : 0));
-}
-__device__ __forceinline__ void cp_async8(void* dst, const void* src, bool valid) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(smem_u32(dst)), "l"(src),
-               "r"(valid ? 8 : 0));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int K>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;\n" ::"n"(K));
-}
-
-// Persistent loop over `ntiles` tiles (grid-stride).
-//   pre(tile, stage)  issues the cp.async copies of `tile` into buffer `stage`
-//   comp(tile, stage) consumes buffer `stage` (may use it as FFT scratch)
-// STAGES == 2 double-buffers (tile i+1 in flight while tile i computes);
-// STAGES == 1 relies on the other resident CTAs of the SM for overlap.
-template <int STAGES, class Pre, class Comp>
-__device__ __forceinline__ void tile_loop(long long ntiles, Pre&& pre, Comp&& comp) {
-  if constexpr (STAGES == 1) {
-    for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-      pre(tile, 0);
-      cp_async_commit();
-      cp_async_wait<0>();
-      __syncthreads();
-      comp(tile, 0);
-      __syncthreads();
-    }
-  } else {
-    long long tile = blockIdx.x;
-    if (tile < ntiles) pre(tile, 0);
-    cp_async_commit();
-    int it = 0;
-    for (; tile < ntiles; tile += gridDim.x, ++it) {
-      const long long next = tile + gridDim.x;
-      if (next < ntiles) pre(next, (it + 1) & 1);
-      cp_async_commit();
-      cp_async_wait<1>();
-      __syncthreads();
-      comp(tile, it & 1);
-      __syncthreads();
-    }
-    cp_async_wait<0>();
-  }
 }
 
 // Register-pipelined persistent loop: `Regs` is the per-thread register set

@@ -71,18 +71,16 @@ __host__ __device__ constexpr int real_R(int m, int mode) {
 }
 
 // Mirrored pre-step: the C2R pre-twiddle pairs X_k with X_{M-k}.  With
-// MIRROR the tile load fetches both rows straight from global memory (the
-// mirror rows are the same tile's rows, so they hit L1/L2) instead of
-// exchanging them through shared memory, saving one smem round trip and one
-// CTA barrier per tile.
-// PFCS_MIRROR=2 issues the mirror loads at the start of the tile's compute
-// rather than with the (possibly prefetched) tile load: the rows were just
-// fetched by the partner threads, so they come from L1 and cost no registers
-// across the prefetch window.
+// PFCS_MIRROR=2 (default) the cube pass loads the mirror rows straight from
+// global memory at the start of the tile's compute (the rows were just
+// fetched by the partner threads, so they come from L1/L2) instead of
+// exchanging them through shared memory: one smem round trip and one CTA
+// barrier less per tile, no registers held across the prefetch window.
+// PFCS_MIRROR=0 restores the shared-memory pairing (A/B).  The TMA-staged
+// form reads the mirror rows from the stage instead (SMIR below).
 #ifndef PFCS_MIRROR
 #define PFCS_MIRROR 2
 #endif
-__host__ __device__ constexpr bool use_mirror(int mode) { return PFCS_MIRROR == 1 && mode == 2; }
 #ifndef PFCS_MIRROR_C2R
 #define PFCS_MIRROR_C2R 0
 #endif
@@ -90,15 +88,10 @@ __host__ __device__ constexpr bool late_mirror(int mode) {
   return PFCS_MIRROR == 2 && (mode == 2 || (PFCS_MIRROR_C2R && mode == 1));
 }
 
-template <int R, bool MIR>
+template <int R>
 struct RegsX {
   double2 v[R];
   double2 xm;  // row M (half-spectrum Nyquist mode), used by thread j == 0
-};
-template <int R>
-struct RegsX<R, true> {
-  double2 v[R];
-  double2 w[R];  // X_{M-k} for k = j + P e (row M for k = 0)
 };
 
 // Extra +8 keeps row M (index PAD(M)) inside the line when the bank rule
@@ -130,7 +123,6 @@ __global__ void __launch_bounds__(T*(M / real_R(M, MODE)),
   constexpr int LS = real_ls(M, T);
   constexpr bool TMA = ST == 3;
   constexpr bool SMIR = TMA && MODE != MODE_R2C;  // mirror rows read from the TMA stage
-  constexpr bool MIR = !TMA && use_mirror(MODE);
   constexpr bool LMIR = !TMA && late_mirror(MODE);
   using XS = XStage<M, T, MODE>;
   extern __shared__ unsigned char xraw[];
@@ -146,7 +138,7 @@ __global__ void __launch_bounds__(T*(M / real_R(M, MODE)),
   const i64 ntiles = (inner + T - 1) / T;
   double m_abs = 0.0;
 
-  auto load = [&](i64 tile, RegsX<R, MIR>& r) {
+  auto load = [&](i64 tile, RegsX<R>& r) {
     const i64 i = tile * T + t;
     const bool ok = i < inner;
     if (MODE == MODE_R2C) {
@@ -164,19 +156,11 @@ __global__ void __launch_bounds__(T*(M / real_R(M, MODE)),
         const i64 k = j + P * e;
         r.v[e] = ok ? in[k * inner + i] : make_double2(0.0, 0.0);
       }
-      if constexpr (MIR) {
-#pragma unroll
-        for (int e = 0; e < R; ++e) {
-          const i64 km = M - (j + P * e);  // in [1, M]
-          r.w[e] = ok ? in[km * inner + i] : make_double2(0.0, 0.0);
-        }
-      } else {
-        r.xm = (ok && j == 0) ? in[(i64)M * inner + i] : make_double2(0.0, 0.0);
-      }
+      r.xm = (ok && j == 0) ? in[(i64)M * inner + i] : make_double2(0.0, 0.0);
     }
   };
 
-  auto comp = [&](i64 tile, RegsX<R, MIR>& r) {
+  auto comp = [&](i64 tile, RegsX<R>& r) {
     const unsigned tid_ = opaque_tid();
     const int t = tid_ % T;
     const int jj = tid_ / T;
@@ -196,7 +180,7 @@ __global__ void __launch_bounds__(T*(M / real_R(M, MODE)),
           wl[e] = ok ? in[km * inner + i] : make_double2(0.0, 0.0);
         }
       }
-      if constexpr (!MIR && !LMIR && !SMIR) {
+      if constexpr (!LMIR && !SMIR) {
         stash_line<M, R>(r.v, jj, sl);
         if (jj == 0) sl[pad_idx(M)] = r.xm;
         __syncthreads();
@@ -207,9 +191,7 @@ __global__ void __launch_bounds__(T*(M / real_R(M, MODE)),
         const int k = jj + P * e;
         double2 a = v[e];
         double2 bm;
-        if constexpr (MIR) {
-          bm = r.w[e];
-        } else if constexpr (LMIR) {
+        if constexpr (LMIR) {
           bm = wl[e];
         } else if constexpr (SMIR) {
           bm = cur[(M - k) * T + t];  // row M for k = 0
@@ -297,7 +279,7 @@ __global__ void __launch_bounds__(T*(M / real_R(M, MODE)),
   };
 
   if constexpr (!TMA) {
-    reg_tile_loop<ST, RegsX<R, MIR>>(ntiles, load, comp);
+    reg_tile_loop<ST, RegsX<R>>(ntiles, load, comp);
   } else {
     unsigned long long* bars = (unsigned long long*)(smem + (size_t)T * LS);
     auto issue = [&](i64 tile, int sidx) {
@@ -329,7 +311,7 @@ __global__ void __launch_bounds__(T*(M / real_R(M, MODE)),
       }
       mbar_wait(&bars[sidx], (unsigned)((it >> 1) & 1));
       cur = sidx ? stage1 : stage0;
-      RegsX<R, false> r;
+      RegsX<R> r;
       if (MODE == MODE_R2C) {
         // rows 2m and 2m+1 of a T-double stage row pair sit in opposite
         // halves of the 32 banks when T = 8: odd-j threads read their odd
@@ -370,13 +352,13 @@ __global__ void __launch_bounds__(T*(N / radix_R(N)), min_blocks(T*(N / radix_R(
   double2* sl = smem + t * LS;
   const i64 ntiles = (inner + T - 1) / T;
   double m_re = 0.0, m_im = 0.0, m_abs = 0.0;
-  auto load = [&](i64 tile, RegsX<R, false>& r) {
+  auto load = [&](i64 tile, RegsX<R>& r) {
     const i64 i = tile * T + t;
     const bool ok = i < inner;
 #pragma unroll
     for (int e = 0; e < R; ++e) r.v[e] = ok ? data[(i64)(j + P * e) * inner + i] : make_double2(0.0, 0.0);
   };
-  auto comp = [&](i64 tile, RegsX<R, false>& r) {
+  auto comp = [&](i64 tile, RegsX<R>& r) {
     const unsigned tid_ = opaque_tid();
     const int t = tid_ % T;
     const int jj = tid_ / T;
@@ -406,7 +388,7 @@ __global__ void __launch_bounds__(T*(N / radix_R(N)), min_blocks(T*(N / radix_R(
       for (int e = 0; e < R; ++e) data[(i64)(j2 + P * e) * inner + i] = v[e];
     }
   };
-  reg_tile_loop<ST, RegsX<R, false>>(ntiles, load, comp);
+  reg_tile_loop<ST, RegsX<R>>(ntiles, load, comp);
   diag_block_max(diag, m_re, m_im, m_abs);
 }
 
