@@ -1,0 +1,47 @@
+"""Time the serial multiphysics step (5 fields, 512^3 default) in isolation:
+    python tools/time_multi.py [n] [steps]"""
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+
+
+def main():
+    import numpy as np
+    import torch
+
+    from paper_2603_26818_b200 import hydro, multiphysics as mpx
+    from paper_2603_26818_b200.grid import GridSpec, make_symbols
+    from paper_2603_26818_b200.pfc import PfcParams
+
+    n = int(sys.argv[1]) if len(sys.argv) > 1 else 512
+    steps = int(sys.argv[2]) if len(sys.argv) > 2 else 6
+    dev = torch.device("cuda", 0)
+    grid = GridSpec((n,) * 3, (2 * np.pi * np.sqrt(3) * (n // 8),) * 3)
+    hp = hydro.HydroParams(pfc=PfcParams(eps=-0.3, dt=0.1), rho=1.0, gamma=1.0, a0=2.0)
+    mp = mpx.MultiParams(hydro=hp, mobility=1.0, kappa=1.0, alpha=1.0, beta=0.0)
+    sym = make_symbols(grid, -0.3, a0=2.0)
+    gen = torch.Generator(device=dev).manual_seed(11)
+
+    def field(scale, base=0.0):
+        x = torch.rand((n,) * 3, dtype=torch.float64, device=dev, generator=gen)
+        return (base + scale * (x - 0.5)).to(torch.complex128)
+
+    psi, c = field(0.02, -0.3), field(0.2)
+    zeros = torch.zeros((n,) * 3, dtype=torch.complex128, device=dev)
+    f = mpx.MultiFields(psi_hat=hydro._fft(psi, True), psi=psi, c_hat=hydro._fft(c, True), c=c,
+                        v_hat=[zeros.clone() for _ in range(3)], v=[zeros.clone() for _ in range(3)])
+    for _ in range(2):
+        mpx.serial_multi_step(f, sym, mp)
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(steps):
+        mpx.serial_multi_step(f, sym, mp)
+    b.record()
+    torch.cuda.synchronize()
+    print(f"multiphysics {n}^3 serial: {a.elapsed_time(b) / steps:.2f} ms/step")
+
+
+if __name__ == "__main__":
+    main()
