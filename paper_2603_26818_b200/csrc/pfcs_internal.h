@@ -93,6 +93,26 @@ int with_variant(F&& f) {
 #endif
 }
 
+// As with_variant, for launches whose default tile is too coarse for the
+// problem: when the default tile width would give fewer tiles than SMs
+// (`tiles_at_tmin` = tiles at the minimum width), the narrowest,
+// single-stage variant 0 runs instead, so small grids (the 2D 256^2 step)
+// spread over the whole GPU.
+constexpr long long SMALL_TILE_THRESHOLD = 148;
+template <int KIND, int N, class F>
+int with_variant_n(long long tiles_at_tmin, F&& f) {
+#ifdef PFCS_TUNE
+  (void)tiles_at_tmin;
+  return with_variant<KIND, N>(f);
+#else
+  constexpr int d = default_variant(KIND, N);
+  if constexpr ((d & 3) != 0) {
+    if ((tiles_at_tmin >> (d & 3)) < SMALL_TILE_THRESHOLD) return f(std::integral_constant<int, 0>{});
+  }
+  return f(std::integral_constant<int, d>{});
+#endif
+}
+
 // Balanced-slab split descriptor for a line of length n over g ranks.
 struct SlabSplitH {
   int G, base, extra;

@@ -417,7 +417,9 @@ template <int M, int MODE>
 static int real_x_m(const void* in, void* out, i64 inner, double* diag, cudaStream_t st) {
   const double2* twN = twiddles(2 * M);
   if (!twN) return PFCS_E_CUDA;
-  return with_variant<MODE == MODE_CUBE ? KIND_CUBER : KIND_REALX, M>([&](auto var) -> int {
+  constexpr int PM = M / real_R(M, MODE);
+  const long long tiles_min = (inner + (PM >= 32 ? 1 : 32 / PM) - 1) / (PM >= 32 ? 1 : 32 / PM);
+  return with_variant_n<MODE == MODE_CUBE ? KIND_CUBER : KIND_REALX, M>(tiles_min, [&](auto var) -> int {
     constexpr int V = decltype(var)::value;
     constexpr int P = M / real_R(M, MODE);
     // R2C/C2R at M = 256 (the 512^3 round trip) take 16 lines per tile:

@@ -190,7 +190,7 @@ static int pfc_z_n(const double2* nl, double2* psi_hat, double2* next, i64 cx, i
   const bool bin = si.G > 1, bout = so.G > 1 || dst != nullptr, nx = next != nullptr || dst != nullptr;
   const PeerTable tab = dst ? *dst : local_table(next, nlines, so.G, so.base, so.extra);
   const double scale = 1.0 / (double)N;
-  return with_variant<KIND_PFCZ, N>([&](auto var) -> int {
+  return with_variant_n<KIND_PFCZ, N>((nlines + TileCfg<N>::T_MIN - 1) / TileCfg<N>::T_MIN, [&](auto var) -> int {
     constexpr int V = decltype(var)::value;
     constexpr int T = TileCfg<N>::T_MIN << (V & 3);
     constexpr int ST = 1 + (V >> 2);
