@@ -30,8 +30,11 @@ struct Regs1 {
 
 // PRO: a pointwise prologue (pfcs_pro.cuh) applied to each loaded element
 // before the transform (plain layouts only).
+#ifndef PFCS_LINES_TARGET2
+#define PFCS_LINES_TARGET2 768  // register target of the 2-stage z-line kernel (B200 512^3: 0.360 -> 0.357 ms)
+#endif
 template <int N, int T, int ST, bool FWD, bool BIN, bool BOUT, bool PRO = false>
-__global__ void __launch_bounds__(T*(N / radix_R(N)), min_blocks(T*(N / radix_R(N)), ST == 2 ? 640 : 1024))
+__global__ void __launch_bounds__(T*(N / radix_R(N)), min_blocks(T*(N / radix_R(N)), ST == 2 ? PFCS_LINES_TARGET2 : 1024))
     k_lines(const double2* in, double2* out, i64 nlines, SlabSplit sin, SlabSplit sout, PeerTable tout,
             const double2* __restrict__ tw, double scale, Pro pro = Pro{}) {
   constexpr int R = radix_R(N);

@@ -32,7 +32,10 @@ namespace pfcs {
 typedef long long i64;
 
 #ifndef PFCS_TW_LOADS
-#define PFCS_TW_LOADS 3  // twiddle-table loads per radix-8 butterfly (3 or 1)
+#define PFCS_TW_LOADS 3  // twiddle-table loads per radix-8 butterfly (7, 3 or 1)
+#endif
+#ifndef PFCS_DFT8_FMA
+#define PFCS_DFT8_FMA 0  // A/B: fold the radix-8 1/sqrt(2) rotations into FMAs
 #endif
 
 __host__ __device__ constexpr int pad_idx(int n) { return n + (n >> 3); }
@@ -125,6 +128,27 @@ __device__ __forceinline__ void dft8(double2 (&y)[8]) {
   double2 o0 = y[1], o1 = y[3], o2 = y[5], o3 = y[7];
   dft4<FWD>(e0, e1, e2, e3);
   dft4<FWD>(o0, o1, o2, o3);
+#if PFCS_DFT8_FMA
+  // the 1/sqrt(2) rotations folded into the final add/sub as FMAs (4 fewer
+  // fp64 instructions per dft8)
+  double2 u1, u3;
+  if (FWD) {
+    u1 = make_double2(o1.x + o1.y, o1.y - o1.x);
+    u3 = make_double2(o3.y - o3.x, -(o3.x + o3.y));
+  } else {
+    u1 = make_double2(o1.x - o1.y, o1.x + o1.y);
+    u3 = make_double2(-(o3.x + o3.y), o3.x - o3.y);
+  }
+  const double2 t2 = mul_j<FWD>(o2);
+  y[0] = cadd(e0, o0);
+  y[4] = csub(e0, o0);
+  y[1] = make_double2(fma(s, u1.x, e1.x), fma(s, u1.y, e1.y));
+  y[5] = make_double2(fma(-s, u1.x, e1.x), fma(-s, u1.y, e1.y));
+  y[2] = cadd(e2, t2);
+  y[6] = csub(e2, t2);
+  y[3] = make_double2(fma(s, u3.x, e3.x), fma(s, u3.y, e3.y));
+  y[7] = make_double2(fma(-s, u3.x, e3.x), fma(-s, u3.y, e3.y));
+#else
   double2 t1, t2, t3;
   if (FWD) {
     t1 = make_double2((o1.x + o1.y) * s, (o1.y - o1.x) * s);
@@ -142,6 +166,7 @@ __device__ __forceinline__ void dft8(double2 (&y)[8]) {
   y[6] = csub(e2, t2);
   y[3] = cadd(e3, t3);
   y[7] = csub(e3, t3);
+#endif
 }
 
 template <int r, bool FWD>
@@ -185,13 +210,20 @@ __device__ __forceinline__ void fft_pass(double2 (&v)[R], int j, double2* sl,
       double2 w[r];
       w[1] = ldg_tw(&tw[t1]);
       if constexpr (r >= 4) w[2] = (TWL >= 3) ? ldg_tw(&tw[2 * t1]) : cmul(w[1], w[1]);
-      if constexpr (r == 4) w[3] = cmul(w[1], w[2]);
+      if constexpr (r == 4) w[3] = (TWL >= 7) ? ldg_tw(&tw[3 * t1]) : cmul(w[1], w[2]);
       if constexpr (r == 8) {
         w[4] = (TWL >= 3) ? ldg_tw(&tw[4 * t1]) : cmul(w[2], w[2]);
-        w[3] = cmul(w[1], w[2]);
-        w[5] = cmul(w[1], w[4]);
-        w[6] = cmul(w[2], w[4]);
-        w[7] = cmul(w[3], w[4]);
+        if constexpr (TWL >= 7) {  // every power from the table: no fp64 products
+          w[3] = ldg_tw(&tw[3 * t1]);
+          w[5] = ldg_tw(&tw[5 * t1]);
+          w[6] = ldg_tw(&tw[6 * t1]);
+          w[7] = ldg_tw(&tw[7 * t1]);
+        } else {
+          w[3] = cmul(w[1], w[2]);
+          w[5] = cmul(w[1], w[4]);
+          w[6] = cmul(w[2], w[4]);
+          w[7] = cmul(w[3], w[4]);
+        }
       }
 #pragma unroll
       for (int q = 1; q < r; ++q) y[q] = twmul<FWD>(y[q], w[q]);

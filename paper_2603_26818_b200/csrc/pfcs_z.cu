@@ -53,12 +53,15 @@ struct RegsZ {
   double2 p[R];  // psi_hat z line
 };
 
+#ifndef PFCS_Z_TARGET
+#define PFCS_Z_TARGET 640  // resident threads per SM the register cap of k_pfc_z aims for (B200: 640 -> 96 regs, 5 CTAs; 1024^3 6.80 -> 6.46 ms)
+#endif
 #ifndef PFCS_Z_TMA_TARGET
 #define PFCS_Z_TMA_TARGET 512
 #endif
 template <int N, int T, int ST, bool BIN, bool BOUT, bool NEXT>
 __global__ void __launch_bounds__(T*(N / radix_R(N)),
-                                  min_blocks(T*(N / radix_R(N)), ST == 3 ? PFCS_Z_TMA_TARGET : 512))
+                                  min_blocks(T*(N / radix_R(N)), ST == 3 ? PFCS_Z_TMA_TARGET : PFCS_Z_TARGET))
     k_pfc_z(const double2* nl, double2* psi_hat, double2* next, i64 nlines, int ny, SlabSplit sin,
             SlabSplit sout, const double* __restrict__ kx, const double* __restrict__ ky,
             const double* __restrict__ kz, PfcSym p, const double2* __restrict__ tw, double scale,
