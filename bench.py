@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--fft-n", type=int, default=FFT_N)
     ap.add_argument("--pfc-n", type=int, default=PFC_N)
     ap.add_argument("--no-pfc", action="store_true")
+    ap.add_argument("--pfc-big", action="store_true", help="also run the 2048^3 PFC step on one GPU")
+    ap.add_argument("--pfc-big-n", type=int, default=2048)
     ap.add_argument("--multi-n", type=int, default=512)
     ap.add_argument("--no-multi", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -87,8 +89,12 @@ def kernel_bytes(name: str, args) -> float:
     if name == "pfcs_pfc_cube_x":
         nx, inner, real = args[1], args[2], args[3]
         return 2.0 * 16.0 * (nx // 2 + 1 if real else nx) * inner
-    if name == "pfcs_pfc_update_z":
+    if name in ("pfcs_pfc_update_z", "pfcs_pfc_update_z_to"):
         return 4.0 * 16.0 * args[3] * args[4] * args[5]
+    if name == "pfcs_fft_zlines_to":  # fused-exchange forms: same HBM bytes, stores go to peers
+        return 2.0 * 16.0 * args[2] * args[3]
+    if name == "pfcs_fft_lines_scatter":
+        return 2.0 * 16.0 * args[2] * args[3] * args[4]
     return 0.0
 
 
@@ -468,14 +474,16 @@ def run_multi(ctx, args):
             "config": f"{n}^3 complex128 full-grid fields, density+composition+v1..v3; {mode}"}
 
 
-def run_pfc(ctx, args):
+def run_pfc(ctx, args, n=None, steps=None, warmup=None):
     import torch
 
     from paper_2603_26818_b200 import _native as nat
     from paper_2603_26818_b200 import distfft, pfc
     from paper_2603_26818_b200.grid import GridSpec, make_symbols, slab_layout
 
-    n = args.pfc_n
+    n = args.pfc_n if n is None else n
+    steps = args.steps if steps is None else steps
+    warmup = args.warmup if warmup is None else warmup
     w = ctx.worker()
     grid = GridSpec((n, n, n), pfc.default_domain_length((n, n, n)))
     cz = slab_layout(n, ctx.world).counts[ctx.rank]
@@ -493,22 +501,22 @@ def run_pfc(ctx, args):
     if ctx.rank == 0:
         mean0 = float(st.psi_hat.dev.reshape(-1)[0].real.item())
 
-    for _ in range(max(1, args.warmup)):
+    for _ in range(max(1, warmup)):
         pfc.pfc_run(st, params, 1)
     torch.cuda.synchronize()
     ctx.barrier()
     a = torch.cuda.Event(enable_timing=True)
     b = torch.cuda.Event(enable_timing=True)
     a.record()
-    pfc.pfc_run(st, params, args.steps)  # K steps enqueued back to back, one read-back
+    pfc.pfc_run(st, params, steps)  # K steps enqueued back to back, one read-back
     b.record()
     torch.cuda.synchronize()
     ctx.barrier()
-    ms = ctx.max_over_ranks(a.elapsed_time(b) / args.steps)
+    ms = ctx.max_over_ranks(a.elapsed_time(b) / steps)
     nat.trace = []
-    pfc.pfc_run(st, params, max(2, args.steps // 4))
+    pfc.pfc_run(st, params, max(2, steps // 4))
     torch.cuda.synchronize()
-    table = kernel_table(nat.trace, max(2, args.steps // 4))
+    table = kernel_table(nat.trace, max(2, steps // 4))
     nat.trace = None
     mass_ok = True
     if ctx.rank == 0:
@@ -571,6 +579,21 @@ def main():
     with ClockSampler(ctx.device.index) as clk:
         table = run_fft(ctx, args, out)
         pfc_res = None if args.no_pfc else run_pfc(ctx, args)
+        # configs[3] grid (2048^3) when it is in this run's reach: at N >= 2
+        # GPUs (slab; <= 69 GB per rank) or with --pfc-big on one GPU (R2C
+        # state 2 x 68.8 GB); a failure is reported, not fatal
+        pfc_big = None
+        if not args.no_pfc and (ctx.world >= 2 or args.pfc_big):
+            import torch
+
+            pfc_res_keep = pfc_res
+            torch.cuda.empty_cache()
+            try:
+                pfc_big = run_pfc(ctx, args, n=args.pfc_big_n, steps=max(3, args.steps // 4), warmup=2)
+            except Exception as exc:  # noqa: BLE001 - keep the rest of the line
+                pfc_big = {"error": f"{type(exc).__name__}: {str(exc)[:200]}"}
+            torch.cuda.empty_cache()
+            pfc_res = pfc_res_keep
         pfc2d = None if args.no_pfc else run_pfc2d(ctx, args)
         multi = None if args.no_multi else run_multi(ctx, args)
     out["clocks"] = clk.summary()
@@ -584,6 +607,12 @@ def main():
         t_roof = pfc_res["alg_hbm_bytes_per_step"] / (hbm * 1e9)
         pfc_res["roofline_step_frac"] = round(t_roof / (pfc_res["ms_per_step"] * 1e-3), 4)
         out["pfc"] = pfc_res
+    if pfc_big is not None:
+        if "error" not in pfc_big:
+            t_roof = pfc_big["alg_hbm_bytes_per_step"] / (hbm * 1e9)
+            pfc_big["roofline_step_frac"] = round(t_roof / (pfc_big["ms_per_step"] * 1e-3), 4)
+            pfc_big["config"] += " (configs[3] grid; slab decomposition)" if args.pfc_big_n == 2048 else ""
+        out["pfc2048"] = pfc_big
     if pfc2d is not None:
         out["pfc2d"] = pfc2d
     if multi is not None:
