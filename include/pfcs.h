@@ -190,6 +190,18 @@ int pfcs_hydro_mu(const void* nl_hat, const void* f_hat, void* out, int64_t n0, 
 int pfcs_hydro_vel_update(void* v_hat, const void* force, int64_t n0, int64_t n1, int64_t n2,
                           const double* kx, const double* ky, const double* kz, double c_cg, double c_den,
                           double c_exp, double* diag, void* stream);
+/* Out-of-place forms of the three spectral updates (state_in read, state_out
+ * written; in == out is the in-place form above): the Python steps return
+ * new arrays without copying the state first. */
+int pfcs_hydro_psi_update_to(const void* psi_in, void* psi_out, const void* nl_hat, const void* adv_hat, int64_t n0,
+                             int64_t n1, int64_t n2, const double* kx, const double* ky, const double* kz,
+                             double eps, double dt, double* diag, void* stream);
+int pfcs_hydro_vel_update_to(const void* v_in, void* v_out, const void* force, int64_t n0, int64_t n1, int64_t n2,
+                             const double* kx, const double* ky, const double* kz, double c_cg, double c_den,
+                             double c_exp, double* diag, void* stream);
+int pfcs_ch_update_to(const void* c_in, void* c_out, const void* f_hat, const void* adv_hat, int64_t n0, int64_t n1,
+                      int64_t n2, const double* kx, const double* ky, const double* kz, double mobility,
+                      double kappa, double dt, double* diag, void* stream);
 
 /* ---- composition field of the multiphysics mode (new; no reference
  * counterpart — restated in oracle/ref_numpy.py): Cahn-Hilliard c advected

@@ -75,6 +75,12 @@ _SIGS = {
     "pfcs_ch_update": [_c_p, _c_p, _c_p, _c_i64, _c_i64, _c_i64, _c_p, _c_p, _c_p, _c_d, _c_d, _c_d,
                        _c_p, _c_p],
     "pfcs_ch_mu": [_c_p, _c_p, _c_p, _c_i64, _c_i64, _c_i64, _c_p, _c_p, _c_p, _c_d, _c_p],
+    "pfcs_hydro_psi_update_to": [_c_p, _c_p, _c_p, _c_p, _c_i64, _c_i64, _c_i64, _c_p, _c_p, _c_p, _c_d, _c_d,
+                                 _c_p, _c_p],
+    "pfcs_hydro_vel_update_to": [_c_p, _c_p, _c_p, _c_i64, _c_i64, _c_i64, _c_p, _c_p, _c_p, _c_d, _c_d, _c_d,
+                                 _c_p, _c_p],
+    "pfcs_ch_update_to": [_c_p, _c_p, _c_p, _c_p, _c_i64, _c_i64, _c_i64, _c_p, _c_p, _c_p, _c_d, _c_d, _c_d,
+                          _c_p, _c_p],
     "pfcs_add3": [_c_p, _c_p, _c_p, _c_p, _c_i64, _c_p],
     "pfcs_axpy": [_c_p, _c_p, _c_p, _c_i64, _c_d, _c_p],
     "pfcs_energy_sum": [_c_p, _c_i64, _c_p, _c_i64, _c_i64, _c_p, _c_p, _c_p],

@@ -77,7 +77,8 @@ __global__ void k_advect(const double2* v1, const double2* x1, const double2* v2
 }
 
 // psi_hat <- (psi_hat + dt*(lap*nl_hat - adv_hat)) / (1 - dt*linear)   (hydro.py:86-87)
-__global__ void k_hydro_psi_update(double2* psi_hat, const double2* nl_hat, const double2* adv_hat, i64 n,
+// psi_in may equal psi_hat (in place); distinct = out of place (no state copy)
+__global__ void k_hydro_psi_update(const double2* psi_in, double2* psi_hat, const double2* nl_hat, const double2* adv_hat, i64 n,
                                    int n1, int n2, const double* __restrict__ kx,
                                    const double* __restrict__ ky, const double* __restrict__ kz,
                                    double eps, double dt, double* diag) {
@@ -93,7 +94,7 @@ __global__ void k_hydro_psi_update(double2* psi_hat, const double2* nl_hat, cons
     const double2 ad = adv_hat ? adv_hat[i] : make_double2(0.0, 0.0);
     const double tr = __dsub_rn(__dmul_rn(lap, nl.x), ad.x);
     const double ti = __dsub_rn(__dmul_rn(lap, nl.y), ad.y);
-    const double2 ph = psi_hat[i];
+    const double2 ph = psi_in[i];
     const double2 nw = make_double2(__dmul_rn(__dadd_rn(ph.x, __dmul_rn(dt, tr)), rden),
                                     __dmul_rn(__dadd_rn(ph.y, __dmul_rn(dt, ti)), rden));
     bad |= !isfinite(nw.x);  // hydro._check_finite looks at the real part (hydro.py:72-74)
@@ -118,7 +119,7 @@ __global__ void k_hydro_mu(const double2* nl_hat, const double2* f_hat, double2*
 
 // v_hat <- (v_hat - ((dt/rho)*cg)*force) / (1 - ((dt/rho)*gamma)*lap)  (hydro.py:103-104)
 // c_cg = dt/rho, c_den = (dt/rho)*gamma, c_exp = -0.5*a0**2 (host-evaluated)
-__global__ void k_hydro_vel_update(double2* v_hat, const double2* force, i64 n, int n1, int n2,
+__global__ void k_hydro_vel_update(const double2* v_in, double2* v_hat, const double2* force, i64 n, int n1, int n2,
                                    const double* __restrict__ kx, const double* __restrict__ ky,
                                    const double* __restrict__ kz, double c_cg, double c_den,
                                    double c_exp, double* diag) {
@@ -130,7 +131,7 @@ __global__ void k_hydro_vel_update(double2* v_hat, const double2* force, i64 n, 
     const double w = __dmul_rn(c_cg, cg);
     const double rden = __drcp_rn(__dsub_rn(1.0, __dmul_rn(c_den, lap)));
     const double2 f = force ? force[i] : make_double2(0.0, 0.0);
-    const double2 v = v_hat[i];
+    const double2 v = v_in[i];
     const double2 nw = make_double2(__dmul_rn(__dsub_rn(v.x, __dmul_rn(w, f.x)), rden),
                                     __dmul_rn(__dsub_rn(v.y, __dmul_rn(w, f.y)), rden));
     bad |= !isfinite(nw.x);
@@ -154,7 +155,8 @@ __global__ void k_ch_nonlin(const double2* c, double2* out, i64 n, double alpha)
   }
 }
 
-__global__ void k_ch_update(double2* c_hat, const double2* f_hat, const double2* adv_hat, i64 n, int n1, int n2,
+__global__ void k_ch_update(const double2* c_in, double2* c_hat, const double2* f_hat, const double2* adv_hat, i64 n,
+                            int n1, int n2,
                             const double* __restrict__ kx, const double* __restrict__ ky,
                             const double* __restrict__ kz, double mob, double kappa, double dt, double* diag) {
   bool bad = false;
@@ -164,7 +166,7 @@ __global__ void k_ch_update(double2* c_hat, const double2* f_hat, const double2*
     const double rden = __drcp_rn(__dadd_rn(1.0, __dmul_rn(__dmul_rn(dt, __dmul_rn(mob, kappa)), __dmul_rn(lap, lap))));
     const double2 f = f_hat[i];
     const double2 ad = adv_hat ? adv_hat[i] : make_double2(0.0, 0.0);
-    const double2 ch = c_hat[i];
+    const double2 ch = c_in[i];
     const double tr = __dsub_rn(__dmul_rn(ml, f.x), ad.x);
     const double ti = __dsub_rn(__dmul_rn(ml, f.y), ad.y);
     const double2 nw = make_double2(__dmul_rn(__dadd_rn(ch.x, __dmul_rn(dt, tr)), rden),
@@ -233,15 +235,21 @@ int pfcs_hydro_advect(const void* v1, const void* x1, const void* v2, const void
   return check_launch("k_advect");
 }
 
-int pfcs_hydro_psi_update(void* psi_hat, const void* nl_hat, const void* adv_hat, int64_t n0, int64_t n1,
-                          int64_t n2, const double* kx, const double* ky, const double* kz, double eps,
-                          double dt, double* diag, void* stream) {
+int pfcs_hydro_psi_update_to(const void* psi_in, void* psi_out, const void* nl_hat, const void* adv_hat, int64_t n0,
+                             int64_t n1, int64_t n2, const double* kx, const double* ky, const double* kz,
+                             double eps, double dt, double* diag, void* stream) {
   const i64 n = n0 * n1 * n2;
   if (n <= 0) return PFCS_OK;
   k_hydro_psi_update<<<grid_for(n), 256, 0, (cudaStream_t)stream>>>(
-      (double2*)psi_hat, (const double2*)nl_hat, (const double2*)adv_hat, n, (int)n1, (int)n2, kx, ky, kz, eps,
-      dt, diag);
+      (const double2*)psi_in, (double2*)psi_out, (const double2*)nl_hat, (const double2*)adv_hat, n, (int)n1,
+      (int)n2, kx, ky, kz, eps, dt, diag);
   return check_launch("k_hydro_psi_update");
+}
+
+int pfcs_hydro_psi_update(void* psi_hat, const void* nl_hat, const void* adv_hat, int64_t n0, int64_t n1,
+                          int64_t n2, const double* kx, const double* ky, const double* kz, double eps,
+                          double dt, double* diag, void* stream) {
+  return pfcs_hydro_psi_update_to(psi_hat, psi_hat, nl_hat, adv_hat, n0, n1, n2, kx, ky, kz, eps, dt, diag, stream);
 }
 
 int pfcs_hydro_mu(const void* nl_hat, const void* f_hat, void* out, int64_t n0, int64_t n1, int64_t n2,
@@ -254,14 +262,21 @@ int pfcs_hydro_mu(const void* nl_hat, const void* f_hat, void* out, int64_t n0, 
   return check_launch("k_hydro_mu");
 }
 
-int pfcs_hydro_vel_update(void* v_hat, const void* force, int64_t n0, int64_t n1, int64_t n2,
-                          const double* kx, const double* ky, const double* kz, double c_cg, double c_den,
-                          double c_exp, double* diag, void* stream) {
+int pfcs_hydro_vel_update_to(const void* v_in, void* v_out, const void* force, int64_t n0, int64_t n1, int64_t n2,
+                             const double* kx, const double* ky, const double* kz, double c_cg, double c_den,
+                             double c_exp, double* diag, void* stream) {
   const i64 n = n0 * n1 * n2;
   if (n <= 0) return PFCS_OK;
   k_hydro_vel_update<<<grid_for(n), 256, 0, (cudaStream_t)stream>>>(
-      (double2*)v_hat, (const double2*)force, n, (int)n1, (int)n2, kx, ky, kz, c_cg, c_den, c_exp, diag);
+      (const double2*)v_in, (double2*)v_out, (const double2*)force, n, (int)n1, (int)n2, kx, ky, kz, c_cg, c_den,
+      c_exp, diag);
   return check_launch("k_hydro_vel_update");
+}
+
+int pfcs_hydro_vel_update(void* v_hat, const void* force, int64_t n0, int64_t n1, int64_t n2,
+                          const double* kx, const double* ky, const double* kz, double c_cg, double c_den,
+                          double c_exp, double* diag, void* stream) {
+  return pfcs_hydro_vel_update_to(v_hat, v_hat, force, n0, n1, n2, kx, ky, kz, c_cg, c_den, c_exp, diag, stream);
 }
 
 int pfcs_ch_nonlin(const void* c, void* out, int64_t n, double alpha, void* stream) {
@@ -270,15 +285,21 @@ int pfcs_ch_nonlin(const void* c, void* out, int64_t n, double alpha, void* stre
   return check_launch("k_ch_nonlin");
 }
 
+int pfcs_ch_update_to(const void* c_in, void* c_out, const void* f_hat, const void* adv_hat, int64_t n0, int64_t n1,
+                      int64_t n2, const double* kx, const double* ky, const double* kz, double mobility,
+                      double kappa, double dt, double* diag, void* stream) {
+  const i64 n = n0 * n1 * n2;
+  if (n <= 0) return PFCS_OK;
+  k_ch_update<<<grid_for(n), 256, 0, (cudaStream_t)stream>>>(
+      (const double2*)c_in, (double2*)c_out, (const double2*)f_hat, (const double2*)adv_hat, n, (int)n1, (int)n2,
+      kx, ky, kz, mobility, kappa, dt, diag);
+  return check_launch("k_ch_update");
+}
+
 int pfcs_ch_update(void* c_hat, const void* f_hat, const void* adv_hat, int64_t n0, int64_t n1, int64_t n2,
                    const double* kx, const double* ky, const double* kz, double mobility, double kappa,
                    double dt, double* diag, void* stream) {
-  const i64 n = n0 * n1 * n2;
-  if (n <= 0) return PFCS_OK;
-  k_ch_update<<<grid_for(n), 256, 0, (cudaStream_t)stream>>>((double2*)c_hat, (const double2*)f_hat,
-                                                            (const double2*)adv_hat, n, (int)n1, (int)n2, kx,
-                                                            ky, kz, mobility, kappa, dt, diag);
-  return check_launch("k_ch_update");
+  return pfcs_ch_update_to(c_hat, c_hat, f_hat, adv_hat, n0, n1, n2, kx, ky, kz, mobility, kappa, dt, diag, stream);
 }
 
 int pfcs_ch_mu(const void* f_hat, const void* c_hat, void* out, int64_t n0, int64_t n1, int64_t n2,

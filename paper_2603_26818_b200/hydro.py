@@ -194,9 +194,9 @@ def hydro_psi_step(psi_hat, psi, v1, v2, v3, sym: SymbolTable, params: HydroPara
     del xs
     nl_hat = _fft_cube(ps)
     adv_hat = _fft(adv, True)
-    new = ph.clone()
+    new = torch.empty_like(ph)
     diag = _Diag(dev)
-    nat.call("pfcs_hydro_psi_update", nat.ptr(new), nat.ptr(nl_hat), nat.ptr(adv_hat), n0, n1, n2,
+    nat.call("pfcs_hydro_psi_update_to", nat.ptr(ph), nat.ptr(new), nat.ptr(nl_hat), nat.ptr(adv_hat), n0, n1, n2,
              nat.ptr(kx), nat.ptr(ky), nat.ptr(kz), float(sym.eps), float(params.pfc.dt),
              nat.ptr(diag.t), st)
     if diag.bad():
@@ -237,9 +237,9 @@ def hydro_velocity_step(v_hat, psi, d_axis, sym: SymbolTable, params: HydroParam
         g = _fft(_mul_deriv(mu_hat, axis, d_axis, sym), False)
     force = _fft_cmul(ps, g)  # F(psi * g), product fused into the first pass
     dt, rho = float(params.pfc.dt), float(params.rho)
-    new = vh.clone()
+    new = torch.empty_like(vh)
     diag = _Diag(dev)
-    nat.call("pfcs_hydro_vel_update", nat.ptr(new), nat.ptr(force), n0, n1, n2, nat.ptr(kx), nat.ptr(ky),
+    nat.call("pfcs_hydro_vel_update_to", nat.ptr(vh), nat.ptr(new), nat.ptr(force), n0, n1, n2, nat.ptr(kx), nat.ptr(ky),
              nat.ptr(kz), dt / rho, (dt / rho) * float(params.gamma), -0.5 * float(sym.a0) ** 2,
              nat.ptr(diag.t), st)
     if diag.bad():

@@ -117,9 +117,9 @@ def density_step(psi_hat, psi, products, sym: SymbolTable, params: MultiParams, 
     n0, n1, n2 = ph.shape
     nl_hat = _fft_cube(ps)
     adv_hat = _fft(_sum3(*products), True)
-    new = ph.clone()
+    new = torch.empty_like(ph)
     diag = _Diag(dev)
-    nat.call("pfcs_hydro_psi_update", nat.ptr(new), nat.ptr(nl_hat), nat.ptr(adv_hat), n0, n1, n2,
+    nat.call("pfcs_hydro_psi_update_to", nat.ptr(ph), nat.ptr(new), nat.ptr(nl_hat), nat.ptr(adv_hat), n0, n1, n2,
              nat.ptr(kx), nat.ptr(ky), nat.ptr(kz), float(sym.eps), float(params.hydro.pfc.dt),
              nat.ptr(diag.t), _st())
     if diag.bad():
@@ -140,9 +140,9 @@ def composition_step(c_hat, c, v, sym: SymbolTable, params: MultiParams, step_in
     f = torch.empty_like(cc)
     nat.call("pfcs_ch_nonlin", nat.ptr(cc), nat.ptr(f), f.numel(), float(params.alpha), _st())
     f_hat = _fft(f, True)
-    new = ch.clone()
+    new = torch.empty_like(ch)
     diag = _Diag(dev)
-    nat.call("pfcs_ch_update", nat.ptr(new), nat.ptr(f_hat), nat.ptr(adv_hat), n0, n1, n2, nat.ptr(kx),
+    nat.call("pfcs_ch_update_to", nat.ptr(ch), nat.ptr(new), nat.ptr(f_hat), nat.ptr(adv_hat), n0, n1, n2, nat.ptr(kx),
              nat.ptr(ky), nat.ptr(kz), float(params.mobility), float(params.kappa),
              float(params.hydro.pfc.dt), nat.ptr(diag.t), _st())
     if diag.bad():
@@ -203,9 +203,9 @@ def velocity_step(v_hat, psi, axis: int, sym: SymbolTable, params: MultiParams, 
         force = total
     hp = params.hydro
     dt, rho = float(hp.pfc.dt), float(hp.rho)
-    new = vh.clone()
+    new = torch.empty_like(vh)
     diag = _Diag(dev)
-    nat.call("pfcs_hydro_vel_update", nat.ptr(new), nat.ptr(force), n0, n1, n2, nat.ptr(kx), nat.ptr(ky),
+    nat.call("pfcs_hydro_vel_update_to", nat.ptr(vh), nat.ptr(new), nat.ptr(force), n0, n1, n2, nat.ptr(kx), nat.ptr(ky),
              nat.ptr(kz), dt / rho, (dt / rho) * float(hp.gamma), -0.5 * float(sym.a0) ** 2,
              nat.ptr(diag.t), st)
     if diag.bad():
