@@ -579,11 +579,12 @@ def main():
     with ClockSampler(ctx.device.index) as clk:
         table = run_fft(ctx, args, out)
         pfc_res = None if args.no_pfc else run_pfc(ctx, args)
-        # configs[3] grid (2048^3) when it is in this run's reach: at N >= 2
-        # GPUs (slab; <= 69 GB per rank) or with --pfc-big on one GPU (R2C
-        # state 2 x 68.8 GB); a failure is reported, not fatal
+        # configs[3] grid (2048^3) when it is comfortably in this run's reach:
+        # at N >= 4 GPUs (slab, <= ~70 GB peak per rank incl. the exchange
+        # buffers) or with --pfc-big on one GPU (R2C state 2 x 68.8 GB); a
+        # failure is reported, not fatal
         pfc_big = None
-        if not args.no_pfc and (ctx.world >= 2 or args.pfc_big):
+        if not args.no_pfc and (ctx.world >= 4 or args.pfc_big):
             import torch
 
             pfc_res_keep = pfc_res
