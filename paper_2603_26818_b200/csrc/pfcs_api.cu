@@ -155,6 +155,14 @@ int persistent_grid(const void* func, int threads, size_t smem, long long ntiles
   return PFCS_OK;
 }
 
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* v = getenv("PFCS_PDL");
+    return !(v && *v && atoi(v) == 0);
+  }();
+  return on;
+}
+
 int tune_variant(int kind, int n, int dflt) {
   char name[64];
   snprintf(name, sizeof(name), "PFCS_VARIANT_%d_%d", kind, n);

@@ -82,6 +82,13 @@ __device__ __forceinline__ int opaque(int x) {
   asm volatile("" : "+r"(x));
   return x;
 }
+// Programmatic dependent launch: wait until the stream predecessor grid has
+// completed and its writes are visible, then let our own dependents launch.
+__device__ __forceinline__ void pdl_wait() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // threadIdx.x read that cannot be hoisted (recomputing a tile's thread
 // coordinates per tile keeps the whole index/pointer family loop-local)
 // (unsigned, so tid % T and tid / T stay single AND/shift instructions)

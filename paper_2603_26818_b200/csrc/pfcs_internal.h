@@ -7,6 +7,7 @@
 
 #include <string>
 #include <type_traits>
+#include <utility>
 
 #include "../../include/pfcs.h"
 
@@ -42,6 +43,28 @@ int launch_strided_tma(const double2* in, double2* out, long long outer, int n, 
                        const Pro* pro = nullptr);
 int launch_lines_pro(const double2* in, double2* out, long long nlines, int n, const Pro& pro, bool forward,
                      cudaStream_t st);
+
+// Programmatic dependent launch (Hopper/Blackwell): the kernel may be
+// scheduled while its stream predecessor drains; it calls pdl_wait() (device)
+// before touching the predecessor's output.  Cuts the launch gap between the
+// small back-to-back passes of launch-bound steps (2D PFC) and is a no-op
+// cost for the large ones.  PFCS_PDL=0 disables it (A/B).
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 // Opt a kernel in to > 48 KB dynamic shared memory once.
 int ensure_smem(const void* func, size_t bytes);

@@ -118,6 +118,7 @@ __global__ void __launch_bounds__(T*(M / real_R(M, MODE)),
                                   min_blocks(T*(M / real_R(M, MODE)), ST == 3 ? 512 : (MODE == 2 ? PFCS_CUBE_TARGET : (ST == 2 ? 640 : 768))))
     k_real_x(const void* in_, void* out_, i64 inner, const double2* __restrict__ twN, double scale,
              double* diag, const __grid_constant__ TmaPair tm) {
+  pdl_wait();
   constexpr int R = real_R(M, MODE);
   constexpr int P = M / R;
   constexpr int LS = real_ls(M, T);
@@ -443,14 +444,16 @@ static int real_x_m(const void* in, void* out, i64 inner, double* diag, cudaStre
           constexpr size_t smem = XStage<M, T, MODE>::SMEM;
           int grid = 0;
           if (int rc = persistent_grid((const void*)k_real_x<M, T, 3, MODE>, T * P, smem, ntiles, &grid)) return rc;
-          k_real_x<M, T, 3, MODE><<<grid, T * P, smem, st>>>(in, out, inner, twN, 1.0 / (double)(2 * M), diag, tm);
+          launch_pdl(k_real_x<M, T, 3, MODE>, dim3(grid), dim3(T * P), smem, st, in, out, inner, twN,
+                     1.0 / (double)(2 * M), diag, tm);
           return check_launch("k_real_x(tma)");
         }
       }
       const size_t smem = (size_t)T * real_ls(M, T) * sizeof(double2);
       int grid = 0;
       if (int rc = persistent_grid((const void*)k_real_x<M, T, ST, MODE>, T * P, smem, ntiles, &grid)) return rc;
-      k_real_x<M, T, ST, MODE><<<grid, T * P, smem, st>>>(in, out, inner, twN, 1.0 / (double)(2 * M), diag, tm);
+      launch_pdl(k_real_x<M, T, ST, MODE>, dim3(grid), dim3(T * P), smem, st, in, out, inner, twN,
+                 1.0 / (double)(2 * M), diag, tm);
       return check_launch("k_real_x");
     }
   });

@@ -66,6 +66,7 @@ __global__ void __launch_bounds__(T*(N / radix_R(N)),
             SlabSplit sout, const double* __restrict__ kx, const double* __restrict__ ky,
             const double* __restrict__ kz, PfcSym p, const double2* __restrict__ tw, double scale,
             double* diag, PeerTable tnext) {
+  pdl_wait();
   constexpr int R = radix_R(N);
   constexpr int P = N / R;
   constexpr int LS = tile_ls(N, T, false);
@@ -222,8 +223,8 @@ static int pfc_z_n(const double2* nl, double2* psi_hat, double2* next, i64 cx, i
   do {                                                                                            \
     if (int rc = persistent_grid((const void*)PFCS_ZK(BI, BO, NX), T * P, smem, ntiles, &grid))   \
       return rc;                                                                                  \
-    PFCS_ZK(BI, BO, NX)<<<grid, T * P, smem, st>>>(nl, psi_hat, next, nlines, (int)ny, a, b, kx, \
-                                                   ky, kz, p, tw, scale, diag, tab);              \
+    launch_pdl(PFCS_ZK(BI, BO, NX), dim3(grid), dim3(T * P), smem, st, nl, psi_hat, next, nlines,     \
+               (int)ny, a, b, kx, ky, kz, p, tw, scale, diag, tab);                               \
   } while (0)
         if (!nx) {
           if (bin) PFCS_ZL(true, false, false);
@@ -241,8 +242,8 @@ static int pfc_z_n(const double2* nl, double2* psi_hat, double2* next, i64 cx, i
   do {                                                                                            \
     if (int rc = persistent_grid((const void*)PFCS_ZK(BI, BO, NX), T * P, smem, ntiles, &grid))   \
       return rc;                                                                                  \
-    PFCS_ZK(BI, BO, NX)<<<grid, T * P, smem, st>>>(nl, psi_hat, next, nlines, (int)ny, a, b, kx, \
-                                                   ky, kz, p, tw, scale, diag, tab);              \
+    launch_pdl(PFCS_ZK(BI, BO, NX), dim3(grid), dim3(T * P), smem, st, nl, psi_hat, next, nlines,     \
+               (int)ny, a, b, kx, ky, kz, p, tw, scale, diag, tab);                               \
   } while (0)
       if (!nx) {
         if (bin) PFCS_ZL(true, false, false);
