@@ -17,7 +17,7 @@
 //   pass on its own rows -> cluster barrier.
 // No HBM traffic and no kernel launches inside the loop: the step is bound
 // by the cluster barriers and the per-CTA FFT latency, not by launches.
-// Measured on the B200 at 256^2: 15.3 us/step, vs 11 us/step for the
+// Measured on the B200 at 256^2: 14.4 us/step, vs 10.5-11 us/step for the
 // CUDA-graph-replayed two-kernel step that spreads each pass over all 148
 // SMs — so the cluster loop is opt-in (pfc.py, PFCS_CLUSTER2D=1).
 #include <cooperative_groups.h>
@@ -65,10 +65,12 @@ struct Pfc2dCfg {
   static constexpr int ZL = (THREADS + PZ - 1) / PZ;  // z lines incl. dummies
   static constexpr int LSX = tile_ls(M, TC, true) + 8;   // x workspace line stride
   static constexpr int LSZ = tile_ls(NY, RC, false);      // z workspace line stride
-  // shared layout (double2): psi rows, work rows, x buffer [NH][TC], x ws, z ws
+  // shared layout (double2): psi rows, work rows (z-inverse), N-hat rows
+  // (x-pass results, double buffer so a step needs two cluster barriers),
+  // x buffer [NH][TC], x ws, z ws
   static constexpr size_t PSI = (size_t)RC * NY, WORK = (size_t)RC * NY, XB = (size_t)NH * TC;
   static constexpr size_t XWS = (size_t)XL * LSX, ZWS = (size_t)ZL * LSZ;
-  static constexpr size_t SMEM = (PSI + WORK + XB + XWS + ZWS) * 16;
+  static constexpr size_t SMEM = (PSI + 2 * WORK + XB + XWS + ZWS) * 16;
 };
 
 template <int NX, int NY, int C>
@@ -83,7 +85,8 @@ __global__ void __cluster_dims__(C, 1, 1) __launch_bounds__(Pfc2dCfg<NX, NY, C>:
   extern __shared__ double2 s2d[];
   double2* psi_s = s2d;
   double2* work_s = psi_s + Cf::PSI;
-  double2* xb = work_s + Cf::WORK;
+  double2* nl_s = work_s + Cf::WORK;  // x-pass results scattered by every CTA
+  double2* xb = nl_s + Cf::WORK;
   double2* xws = xb + Cf::XB;
   double2* zws = xws + Cf::XWS;
   const int tid = threadIdx.x;
@@ -104,10 +107,23 @@ __global__ void __cluster_dims__(C, 1, 1) __launch_bounds__(Pfc2dCfg<NX, NY, C>:
   for (int step = 0; step < nsteps; ++step) {
     double* dstep = diag ? diag + (size_t)step * PFCS_DIAG_SLOTS * PFCS_DIAG_VALS : nullptr;
     // ---- gather this CTA's columns [c*TC, c*TC+TC) of every row into xb[kx][t]
-    for (int idx = tid; idx < NH * TC; idx += blockDim.x) {
-      const int kxi = idx / TC, t = idx - kxi * TC;
-      const double2* src = cluster.map_shared_rank(work_s, (unsigned)(kxi % C));
-      xb[idx] = src[(kxi / C) * NY + c * TC + t];
+    {
+      constexpr int G = (NH * TC + Cf::THREADS - 1) / Cf::THREADS;
+      double2 tmp[G];
+#pragma unroll
+      for (int q = 0; q < G; ++q) {  // all remote loads in flight before the stores
+        const int idx = tid + q * Cf::THREADS;
+        if (idx < NH * TC) {
+          const int kxi = idx / TC, t = idx - kxi * TC;
+          const double2* src = cluster.map_shared_rank(work_s, (unsigned)(kxi % C));
+          tmp[q] = src[(kxi / C) * NY + c * TC + t];
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < G; ++q) {
+        const int idx = tid + q * Cf::THREADS;
+        if (idx < NH * TC) xb[idx] = tmp[q];
+      }
     }
     __syncthreads();
     // ---- x pass (k_real_x MODE_CUBE, mirror rows read from the buffer)
@@ -182,18 +198,18 @@ __global__ void __cluster_dims__(C, 1, 1) __launch_bounds__(Pfc2dCfg<NX, NY, C>:
       }
     }
     diag_block_max(dstep, m_abs, 0.0, m_abs);  // block-wide (contains __syncthreads)
-    cluster.sync();  // every CTA has gathered its columns before any row is overwritten
-    // ---- scatter the finished columns to the row owners' work rows
+    // ---- scatter the finished columns to the row owners' N-hat rows (a
+    // buffer nobody gathers from, so no barrier is needed in front)
     if (xact) {
       const int t = tid % TC, jj = tid / TC;
 #pragma unroll
       for (int e = 0; e < RX; ++e) {
         const int k = jj + PX * e;
-        double2* dst = cluster.map_shared_rank(work_s, (unsigned)(k % C));
+        double2* dst = cluster.map_shared_rank(nl_s, (unsigned)(k % C));
         dst[(k / C) * NY + c * TC + t] = xr[e];
       }
       if (jj == 0) {
-        double2* dst = cluster.map_shared_rank(work_s, (unsigned)(M % C));
+        double2* dst = cluster.map_shared_rank(nl_s, (unsigned)(M % C));
         dst[(M / C) * NY + c * TC + t] = xm_out;
       }
     }
@@ -207,7 +223,7 @@ __global__ void __cluster_dims__(C, 1, 1) __launch_bounds__(Pfc2dCfg<NX, NY, C>:
       double2* sl = zws + line * Cf::LSZ;  // private workspace line, dummies included
       double2 v[RZ];
 #pragma unroll
-      for (int e = 0; e < RZ; ++e) v[e] = work_s[lrow * NY + j + PZ * e];
+      for (int e = 0; e < RZ; ++e) v[e] = nl_s[lrow * NY + j + PZ * e];
       const int jj = opaque(j);
       fft_line<NY, true, 1, 1, RZ>(v, jj, sl, twZ);
       const double kxx = __ldg(&kx[c + C * lrow]);

@@ -384,8 +384,8 @@ def pfc_run(state: PfcState, params: PfcParams, n_steps: int, realness: list | N
 def _cluster2d(eng, state: PfcState) -> bool:
     """Opt-in (PFCS_CLUSTER2D=1): run the 2D 256^2 single-rank R2C time loop
     as one thread-block-cluster kernel (csrc/pfcs_pfc2d.cu; bit-identical).
-    Off by default: on the B200 the 16-SM cluster (15.3 us/step) loses to the
-    graph-replayed two-kernel step spread over all SMs (11 us/step)."""
+    Off by default: on the B200 the 16-SM cluster (14.4 us/step) loses to the
+    graph-replayed two-kernel step spread over all SMs (10.5-11 us/step)."""
     if os.environ.get("PFCS_CLUSTER2D", "0") != "1":
         return False
     g = eng.g
