@@ -53,6 +53,9 @@ struct RegsZ {
   double2 p[R];  // psi_hat z line
 };
 
+#ifndef PFCS_Z_TWL
+#define PFCS_Z_TWL 1  // twiddle loads per butterfly in the fused z update (B200 1024^3: 1 -> 6.46 ms, 3 -> 8.05 ms)
+#endif
 #ifndef PFCS_Z_TARGET
 #define PFCS_Z_TARGET 640  // resident threads per SM the register cap of k_pfc_z aims for (B200: 640 -> 96 regs, 5 CTAs; 1024^3 6.80 -> 6.46 ms)
 #endif
@@ -115,7 +118,7 @@ __global__ void __launch_bounds__(T*(N / radix_R(N)),
     const i64 l = tile * T + t;
     const bool ok = l < nlines;
     const int jj = opaque(j);
-    fft_line<N, true, 1, 1>(r.v, jj, sl, tw);
+    fft_line<N, true, 1, PFCS_Z_TWL>(r.v, jj, sl, tw);
     const i64 lx = ok ? l / ny : 0;
     const int ly = ok ? (int)(l - lx * ny) : 0;
     const double kxx = __ldg(&kx[lx]);
@@ -144,7 +147,7 @@ __global__ void __launch_bounds__(T*(N / radix_R(N)),
     }
     if (NEXT) {
       const int j2 = opaque(jj);
-      fft_line<N, false, 1, 1>(r.v, j2, sl, tw);
+      fft_line<N, false, 1, PFCS_Z_TWL>(r.v, j2, sl, tw);
       if (ok) {
 #pragma unroll
         for (int e = 0; e < R; ++e) {
