@@ -34,6 +34,12 @@ typedef long long i64;
 #ifndef PFCS_TW_LOADS
 #define PFCS_TW_LOADS 3  // twiddle-table loads per radix-8 butterfly (7, 3 or 1)
 #endif
+#ifndef PFCS_X_TWL
+// twiddle loads per butterfly in the x passes (R2C / C2R / fused cube): one
+// table load + products measured faster there on the B200 (cube 1024^3
+// 5.83 -> 5.70 ms, R2C/C2R 512^3 -3 %); the y / z line passes keep 3
+#define PFCS_X_TWL 1
+#endif
 #ifndef PFCS_DFT8_FMA
 #define PFCS_DFT8_FMA 0  // A/B: fold the radix-8 1/sqrt(2) rotations into FMAs
 #endif

@@ -156,7 +156,7 @@ __global__ void __cluster_dims__(C, 1, 1) __launch_bounds__(Pfc2dCfg<NX, NY, C>:
         const double2 wd = make_double2(fma(d.x, w.x, d.y * w.y), fma(d.y, w.x, -d.x * w.y));
         v[e] = make_double2(s.x - wd.y, s.y + wd.x);
       }
-      fft_line<M, false, 2, PFCS_TW_LOADS, RX>(v, jj, sl, twN);
+      fft_line<M, false, 2, PFCS_X_TWL, RX>(v, jj, sl, twN);
 #pragma unroll
       for (int e = 0; e < RX; ++e) v[e] = make_double2(v[e].x * scale_x, v[e].y * scale_x);
 #pragma unroll
@@ -165,7 +165,7 @@ __global__ void __cluster_dims__(C, 1, 1) __launch_bounds__(Pfc2dCfg<NX, NY, C>:
         if (xact) m_abs = dmax_bits(m_abs, dmax_bits(fabs(a), fabs(b)));
         v[e] = make_double2(__dmul_rn(__dmul_rn(a, a), a), __dmul_rn(__dmul_rn(b, b), b));
       }
-      fft_line<M, true, 2, PFCS_TW_LOADS, RX>(v, jj, sl, twN);
+      fft_line<M, true, 2, PFCS_X_TWL, RX>(v, jj, sl, twN);
       // pairing Z_k with Z_{M-k} through xb (its last reads were the pre-step,
       // separated from here by the FFTs' barriers)
       if (xact) {

@@ -210,7 +210,7 @@ __global__ void __launch_bounds__(T*(M / real_R(M, MODE)),
         const double2 wd = make_double2(fma(d.x, w.x, d.y * w.y), fma(d.y, w.x, -d.x * w.y));
         v[e] = make_double2(s.x - wd.y, s.y + wd.x);
       }
-      fft_line<M, false, 2, PFCS_TW_LOADS, R>(r.v, jj, sl, twN);
+      fft_line<M, false, 2, PFCS_X_TWL, R>(r.v, jj, sl, twN);
 #pragma unroll
       for (int e = 0; e < R; ++e) v[e] = make_double2(v[e].x * scale, v[e].y * scale);
     }
@@ -240,7 +240,7 @@ __global__ void __launch_bounds__(T*(M / real_R(M, MODE)),
 
     // forward M-point FFT, then the R2C split
     const int j2 = opaque(jj);  // keep the forward FFT's index math out of the inverse's live range
-    fft_line<M, true, 2, PFCS_TW_LOADS, R>(r.v, j2, sl, twN);
+    fft_line<M, true, 2, PFCS_X_TWL, R>(r.v, j2, sl, twN);
     const double2 wj = __ldg(&twN[jj]);
     // Pairing Z_k with Z_{M-k}.  TMA mode exchanges through the current stage
     // ([k][t] rows, conflict-free for t-fastest lanes): it was last read
