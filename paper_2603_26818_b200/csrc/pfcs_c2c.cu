@@ -74,7 +74,7 @@ __global__ void __launch_bounds__(T*(N / radix_R(N)), min_blocks(T*(N / radix_R(
       for (int e = 0; e < R; ++e)
         r.v[e] = apply_pro(pro, r.v[e], l * N + jj + P * e, pro.axis == 2 ? (i64)(jj + P * e) : cl);
     }
-    fft_line<N, FWD>(r.v, jj, sl, tw);
+    fft_line<N, FWD, 1, PFCS_LINES_TWL>(r.v, jj, sl, tw);
     if (l < nlines) {
 #pragma unroll
       for (int e = 0; e < R; ++e) {
@@ -137,7 +137,7 @@ __global__ void __launch_bounds__(T*(N / radix_R(N)), min_blocks(T*(N / radix_R(
     const i64 o = tile / tpo;
     const i64 i = (tile - o * tpo) * T + t;
     const int jj = opaque(j);
-    fft_line<N, FWD>(r.v, jj, sl, tw);
+    fft_line<N, FWD, 1, PFCS_Y_TWL>(r.v, jj, sl, tw);
     if (i < inner) {
       double2* dst = out;
       i64 orow = o;

@@ -40,6 +40,14 @@ typedef long long i64;
 // 5.83 -> 5.70 ms, R2C/C2R 512^3 -3 %); the y / z line passes keep 3
 #define PFCS_X_TWL 1
 #endif
+#ifndef PFCS_LINES_TWL
+// contiguous z-line passes (k_lines): one load + products measured faster
+// (1024-point lines 3.38 -> 2.85 ms per 1024^3 pass, 512-point unchanged)
+#define PFCS_LINES_TWL 1
+#endif
+#ifndef PFCS_Y_TWL
+#define PFCS_Y_TWL PFCS_TW_LOADS  // strided y passes: 3 (1 measured 2 % slower)
+#endif
 #ifndef PFCS_DFT8_FMA
 #define PFCS_DFT8_FMA 0  // A/B: fold the radix-8 1/sqrt(2) rotations into FMAs
 #endif
@@ -55,7 +63,12 @@ __host__ __device__ constexpr int line_stride(int n) { return pad_idx(n) + 2; }
 __host__ __device__ constexpr int tile_ls(int n, int t, bool strided) {
   return pad_idx(n) + ((!strided || n <= 8) ? 0 : (8 / (t < 8 ? t : 8)) % 8);
 }
-__host__ __device__ constexpr int radix_R(int n) { return n >= 8 ? 8 : n; }
+#ifndef PFCS_R16
+#define PFCS_R16 0  // lines of >= PFCS_R16 points hold 16 values per thread (radix-16 passes); 0 = off
+#endif
+__host__ __device__ constexpr int radix_R(int n) {
+  return (PFCS_R16 > 0 && n >= PFCS_R16) ? 16 : (n >= 8 ? 8 : n);
+}
 // minBlocksPerSM for __launch_bounds__: enough CTAs for `target` resident
 // threads per SM, which caps registers at 65536 / target per thread.
 __host__ __device__ constexpr int min_blocks(int threads, int target) {
@@ -182,6 +195,38 @@ __device__ __forceinline__ void dft8(double2 (&y)[8]) {
 #endif
 }
 
+// 16-point DFT as 4 x 4: dft4 over stride-4 columns, twiddles W16^(n2 k1),
+// dft4 over rows; output index k1 + 4 k2 sits at 4 k1 + k2 before the final
+// (compile-time) transpose.
+template <bool FWD>
+__device__ __forceinline__ void dft16(double2 (&y)[16]) {
+  const double c = 0.92387953251128675613;  // cos(pi/8)
+  const double s = 0.38268343236508977173;  // sin(pi/8)
+  const double h = 0.70710678118654752440;  // 1/sqrt(2)
+#pragma unroll
+  for (int n2 = 0; n2 < 4; ++n2) dft4<FWD>(y[n2], y[4 + n2], y[8 + n2], y[12 + n2]);
+  // element (k1, n2) is y[4 k1 + n2]; multiply by W16^(n2 k1)
+  const double sg = FWD ? -1.0 : 1.0;
+  y[5] = cmul(y[5], make_double2(c, sg * s));            // k1=1 n2=1: W^1
+  y[6] = cmul(y[6], make_double2(h, sg * h));            // W^2
+  y[7] = cmul(y[7], make_double2(s, sg * c));            // W^3
+  y[9] = cmul(y[9], make_double2(h, sg * h));            // k1=2 n2=1: W^2
+  y[10] = mul_j<FWD>(y[10]);                             // W^4
+  y[11] = cmul(y[11], make_double2(-h, sg * h));         // W^6
+  y[13] = cmul(y[13], make_double2(s, sg * c));          // k1=3 n2=1: W^3
+  y[14] = cmul(y[14], make_double2(-h, sg * h));         // W^6
+  y[15] = cmul(y[15], make_double2(-c, -sg * s));        // W^9
+#pragma unroll
+  for (int k1 = 0; k1 < 4; ++k1) dft4<FWD>(y[4 * k1], y[4 * k1 + 1], y[4 * k1 + 2], y[4 * k1 + 3]);
+  double2 z[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) z[i] = y[i];
+#pragma unroll
+  for (int k1 = 0; k1 < 4; ++k1)
+#pragma unroll
+    for (int k2 = 0; k2 < 4; ++k2) y[k1 + 4 * k2] = z[4 * k1 + k2];
+}
+
 template <int r, bool FWD>
 __device__ __forceinline__ void dft_r(double2 (&y)[r]) {
   if constexpr (r == 2) {
@@ -190,6 +235,8 @@ __device__ __forceinline__ void dft_r(double2 (&y)[r]) {
     dft4<FWD>(y[0], y[1], y[2], y[3]);
   } else if constexpr (r == 8) {
     dft8<FWD>(y);
+  } else if constexpr (r == 16) {
+    dft16<FWD>(y);
   }
 }
 
@@ -237,6 +284,16 @@ __device__ __forceinline__ void fft_pass(double2 (&v)[R], int j, double2* sl,
           w[6] = cmul(w[2], w[4]);
           w[7] = cmul(w[3], w[4]);
         }
+      }
+      if constexpr (r == 16) {
+        w[4] = (TWL >= 3) ? ldg_tw(&tw[4 * t1]) : cmul(w[2], w[2]);
+        w[8] = (TWL >= 3) ? ldg_tw(&tw[8 * t1]) : cmul(w[4], w[4]);
+        w[3] = cmul(w[1], w[2]);
+        w[5] = cmul(w[1], w[4]);
+        w[6] = cmul(w[2], w[4]);
+        w[7] = cmul(w[3], w[4]);
+#pragma unroll
+        for (int q = 9; q < 16; ++q) w[q] = cmul(w[q - 8], w[8]);
       }
 #pragma unroll
       for (int q = 1; q < r; ++q) y[q] = twmul<FWD>(y[q], w[q]);

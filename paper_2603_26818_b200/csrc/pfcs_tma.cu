@@ -104,7 +104,7 @@ __global__ void __launch_bounds__(T*(N / radix_R(N)), 1)
         }
       }
     }
-    fft_line<N, FWD>(v, jj, sl, tw);
+    fft_line<N, FWD, 1, PFCS_Y_TWL>(v, jj, sl, tw);
     if (i < inner) {
       double2* dst;
       if constexpr (OPEER) {
