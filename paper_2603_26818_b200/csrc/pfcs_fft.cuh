@@ -48,6 +48,9 @@ typedef long long i64;
 #ifndef PFCS_Y_TWL
 #define PFCS_Y_TWL PFCS_TW_LOADS  // strided y passes: 3 (1 measured 2 % slower)
 #endif
+#ifndef PFCS_Y_TWSMEM
+#define PFCS_Y_TWSMEM 0  // 1: TMA y pass reads twiddles from a smem copy (A/B: 1024^3 3.83 -> 3.98 ms, slower)
+#endif
 #ifndef PFCS_DFT8_FMA
 #define PFCS_DFT8_FMA 0  // A/B: fold the radix-8 1/sqrt(2) rotations into FMAs
 #endif
@@ -128,6 +131,20 @@ __device__ __forceinline__ double2 ldg_tw(const double2* p) {
   asm volatile("ld.global.nc.v2.f64 {%0, %1}, [%2];" : "=d"(w.x), "=d"(w.y) : "l"(p));
   return w;
 #endif
+}
+
+// Twiddle load from a shared-memory copy of the table (kernels that stage it
+// with `TSM`); volatile for the same no-hoisting reason as ldg_tw.
+__device__ __forceinline__ double2 lds_tw(const double2* p) {
+  double2 w;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(w.x), "=d"(w.y)
+               : "r"((unsigned)__cvta_generic_to_shared(p)));
+  return w;
+}
+template <bool TSM>
+__device__ __forceinline__ double2 ld_tw(const double2* p) {
+  if constexpr (TSM) return lds_tw(p);
+  else return ldg_tw(p);
 }
 
 template <bool FWD>
@@ -245,7 +262,7 @@ __device__ __forceinline__ void dft_r(double2 (&y)[r]) {
 // j + P*e of this pass's input; on exit of the last pass v[e] holds output
 // element j + P*e.  `tw` is the size-N table exp(-2 pi i m / N), m < N,
 // read with stride TWS (so a size-2N table serves an N-point transform).
-template <int N, int Ns, bool FWD, int TWS, int TWL = PFCS_TW_LOADS, int R = radix_R(N)>
+template <int N, int Ns, bool FWD, int TWS, int TWL = PFCS_TW_LOADS, int R = radix_R(N), bool TSM = false>
 __device__ __forceinline__ void fft_pass(double2 (&v)[R], int j, double2* sl,
                                          const double2* __restrict__ tw) {
   // R = values per thread (8, or 4 for the register-heavy fused passes);
@@ -268,16 +285,16 @@ __device__ __forceinline__ void fft_pass(double2 (&v)[R], int j, double2* sl,
       // (7 loads -> 3 lifted z-line kernels from 4.3 to 5.9 TB/s on B200)
       const int t1 = TWS * k * (N / (Ns * r));
       double2 w[r];
-      w[1] = ldg_tw(&tw[t1]);
-      if constexpr (r >= 4) w[2] = (TWL >= 3) ? ldg_tw(&tw[2 * t1]) : cmul(w[1], w[1]);
-      if constexpr (r == 4) w[3] = (TWL >= 7) ? ldg_tw(&tw[3 * t1]) : cmul(w[1], w[2]);
+      w[1] = ld_tw<TSM>(&tw[t1]);
+      if constexpr (r >= 4) w[2] = (TWL >= 3) ? ld_tw<TSM>(&tw[2 * t1]) : cmul(w[1], w[1]);
+      if constexpr (r == 4) w[3] = (TWL >= 7) ? ld_tw<TSM>(&tw[3 * t1]) : cmul(w[1], w[2]);
       if constexpr (r == 8) {
-        w[4] = (TWL >= 3) ? ldg_tw(&tw[4 * t1]) : cmul(w[2], w[2]);
+        w[4] = (TWL >= 3) ? ld_tw<TSM>(&tw[4 * t1]) : cmul(w[2], w[2]);
         if constexpr (TWL >= 7) {  // every power from the table: no fp64 products
-          w[3] = ldg_tw(&tw[3 * t1]);
-          w[5] = ldg_tw(&tw[5 * t1]);
-          w[6] = ldg_tw(&tw[6 * t1]);
-          w[7] = ldg_tw(&tw[7 * t1]);
+          w[3] = ld_tw<TSM>(&tw[3 * t1]);
+          w[5] = ld_tw<TSM>(&tw[5 * t1]);
+          w[6] = ld_tw<TSM>(&tw[6 * t1]);
+          w[7] = ld_tw<TSM>(&tw[7 * t1]);
         } else {
           w[3] = cmul(w[1], w[2]);
           w[5] = cmul(w[1], w[4]);
@@ -286,8 +303,8 @@ __device__ __forceinline__ void fft_pass(double2 (&v)[R], int j, double2* sl,
         }
       }
       if constexpr (r == 16) {
-        w[4] = (TWL >= 3) ? ldg_tw(&tw[4 * t1]) : cmul(w[2], w[2]);
-        w[8] = (TWL >= 3) ? ldg_tw(&tw[8 * t1]) : cmul(w[4], w[4]);
+        w[4] = (TWL >= 3) ? ld_tw<TSM>(&tw[4 * t1]) : cmul(w[2], w[2]);
+        w[8] = (TWL >= 3) ? ld_tw<TSM>(&tw[8 * t1]) : cmul(w[4], w[4]);
         w[3] = cmul(w[1], w[2]);
         w[5] = cmul(w[1], w[4]);
         w[6] = cmul(w[2], w[4]);
@@ -315,16 +332,16 @@ __device__ __forceinline__ void fft_pass(double2 (&v)[R], int j, double2* sl,
     __syncthreads();
 #pragma unroll
     for (int e = 0; e < R; ++e) v[e] = sl[pad_idx(j + P * e)];
-    fft_pass<N, Ns * r, FWD, TWS, TWL, R>(v, j, sl, tw);
+    fft_pass<N, Ns * r, FWD, TWS, TWL, R, TSM>(v, j, sl, tw);
   }
 }
 
 // Full N-point transform of the register set (see fft_pass).  All threads of
 // the CTA must call it (it contains __syncthreads when N > 8).
-template <int N, bool FWD, int TWS = 1, int TWL = PFCS_TW_LOADS, int R = radix_R(N)>
+template <int N, bool FWD, int TWS = 1, int TWL = PFCS_TW_LOADS, int R = radix_R(N), bool TSM = false>
 __device__ __forceinline__ void fft_line(double2 (&v)[R], int j, double2* sl,
                                          const double2* __restrict__ tw) {
-  fft_pass<N, 1, FWD, TWS, TWL, R>(v, j, sl, tw);
+  fft_pass<N, 1, FWD, TWS, TWL, R, TSM>(v, j, sl, tw);
 }
 
 // Stash register set (element j + P*e in v[e]) into the padded smem line.

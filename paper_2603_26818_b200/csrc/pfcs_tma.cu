@@ -25,8 +25,11 @@ struct TmaCfg {
   static constexpr int BR = N < 256 ? N : 256;  // rows per TMA box (box dims <= 256)
   static constexpr int NB = N / BR;
   static constexpr unsigned STAGE = (unsigned)N * T * 16u;  // bytes per stage
-  // two stages + FFT workspace + 2 mbarriers, plus alignment slack
-  static constexpr size_t SMEM = 2 * (size_t)STAGE + (size_t)T * LS * 16 + 16 + 1024;
+  // two stages + FFT workspace + 2 mbarriers (+ the twiddle table), plus
+  // alignment slack
+  static constexpr size_t BASE = 2 * (size_t)STAGE + (size_t)T * LS * 16 + 16 + 1024;
+  static constexpr bool TSM = PFCS_Y_TWSMEM && BASE + (size_t)N * 16 <= 227 * 1024;
+  static constexpr size_t SMEM = BASE + (TSM ? (size_t)N * 16 : 0);
 };
 
 // OPEER: outer row o goes to tout.p[h][(o - ooff_h) ...] (the fused
@@ -47,6 +50,15 @@ __global__ void __launch_bounds__(T*(N / radix_R(N)), 1)
   double2* stage1 = stage0 + (size_t)N * T;
   double2* ws = stage1 + (size_t)N * T;
   unsigned long long* bars = (unsigned long long*)(ws + (size_t)T * C::LS);
+  // twiddle table copy (C::TSM, A/B only): L1 holds only what the ~200 KB of
+  // shared memory leave and 1024-point lines miss it on a quarter of the
+  // loads, but the pass is bound by shared-memory instruction issue
+  // (mio_throttle), so moving the loads there made it slower
+  double2* tws = (double2*)(bars + 2);
+  if constexpr (C::TSM) {
+    for (int k = threadIdx.x; k < N; k += blockDim.x) tws[k] = tw[k];
+  }
+  const double2* twp = C::TSM ? (const double2*)tws : tw;
 
   const int tid = threadIdx.x;
   const int t = tid % T;
@@ -104,7 +116,7 @@ __global__ void __launch_bounds__(T*(N / radix_R(N)), 1)
         }
       }
     }
-    fft_line<N, FWD, 1, PFCS_Y_TWL>(v, jj, sl, tw);
+    fft_line<N, FWD, 1, PFCS_Y_TWL, R, C::TSM>(v, jj, sl, twp);
     if (i < inner) {
       double2* dst;
       if constexpr (OPEER) {
