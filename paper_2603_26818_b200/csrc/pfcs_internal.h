@@ -94,10 +94,13 @@ enum { KIND_LINES = 0, KIND_STRIDED = 1, KIND_REALX = 2, KIND_CUBEC = 3, KIND_PF
 #ifndef PFCS_CUBER_1024
 #define PFCS_CUBER_1024 2  // A/B hook: cube pass tile at M = 1024 (2048^3)
 #endif
+#ifndef PFCS_STRIDED_2048
+#define PFCS_STRIDED_2048 2  // A/B hook: strided y pass tile at N = 2048
+#endif
 constexpr int default_variant(int kind, int n) {
   // n: transform length (REALX / CUBER: the half length M)
   return kind == KIND_LINES   ? (n <= 256 ? 5 : (n == 512 ? 4 : 0))
-       : kind == KIND_STRIDED ? (n <= 512 ? 3 : (n == 1024 ? 6 : (n == 2048 ? 2 : 4)))
+       : kind == KIND_STRIDED ? (n <= 512 ? 3 : (n == 1024 ? 6 : (n == 2048 ? PFCS_STRIDED_2048 : 4)))
        : kind == KIND_REALX   ? (n == 256 ? 3 : (n <= 512 ? 7 : (n == 1024 ? 6 : (n == 2048 ? 5 : 4))))
        : kind == KIND_CUBER   ? (n <= 256 ? 3 : (n == 512 ? PFCS_CUBER_512 : (n == 1024 ? PFCS_CUBER_1024 : (n == 2048 ? 1 : 0))))
        : kind == KIND_CUBEC   ? (n <= 512 ? 3 : (n == 1024 ? 2 : (n == 2048 ? 1 : 0)))
