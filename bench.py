@@ -56,6 +56,7 @@ def parse():
     ap.add_argument("--no-multi", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
+    ap.add_argument("--no-cpu-sub", action="store_true", help="skip the sub-lines' CPU baselines")
     return ap.parse_args()
 
 
@@ -387,9 +388,55 @@ def run_fft(ctx, args, out):
     return table
 
 
+def pfc_e2e(ctx, st, params, phys_layout, host_in, steps: int) -> dict:
+    """The PFC metric end to end through the public API with host buffers:
+    pinned host psi -> H2D -> distfft.forward -> (into the state) ->
+    pfc.pfc_run(steps) (diagnostics read back) -> distfft.inverse -> D2H,
+    everything inside the CUDA-event timed region.  One warm-up run first;
+    steps/s = steps / time, copies counted per step."""
+    import torch
+
+    from paper_2603_26818_b200 import distfft, pfc
+
+    w = st.worker
+    dev_in = torch.empty(host_in.shape, dtype=host_in.dtype, device=ctx.device)
+    host_out = torch.empty_like(host_in).pin_memory()
+    diag_bytes = 64 * 4 * 8 * steps  # the per-step diagnostics block pfc_run reads back
+
+    def once():
+        dev_in.copy_(host_in, non_blocking=True)
+        f = distfft.DistField(st.grid, phys_layout, distfft.Space.PHYSICAL, dev_in)
+        spec = distfft.forward(f, w)
+        st.psi_hat.dev.copy_(spec.dev)
+        st.psi_hat.touch()
+        del spec
+        pfc.pfc_run(st, params, steps)
+        back = distfft.inverse(st.psi_hat, w)
+        host_out.copy_(back.dev, non_blocking=True)
+
+    once()
+    torch.cuda.synchronize()
+    ctx.barrier()
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    a.record()
+    once()
+    b.record()
+    torch.cuda.synchronize()
+    ms = ctx.max_over_ranks(a.elapsed_time(b))
+    nb = host_in.numel() * host_in.element_size()
+    return {"value": round(1000.0 * steps / ms, 3), "unit": "steps/s", "ms_per_run": round(ms, 3),
+            "steps_per_run": steps,
+            "h2d_bytes_per_step": int(ctx.sum_over_ranks(nb) / steps),
+            "d2h_bytes_per_step": int(ctx.sum_over_ranks(nb + diag_bytes) / steps),
+            "pipeline": f"host psi in (pinned) -> forward -> pfc_run({steps}) -> inverse -> host psi out; "
+                        f"copies amortised over the run's steps"}
+
+
 def run_pfc2d(ctx, args):
     """configs[0]: 2D PFC 256^2, 100 semi-implicit steps (launch-bound; the
     single-rank path replays CUDA graphs), reference init and domain."""
+    import numpy as np
     import torch
 
     from paper_2603_26818_b200 import distfft, pfc
@@ -416,9 +463,11 @@ def run_pfc2d(ctx, args):
     torch.cuda.synchronize()
     wall = time.perf_counter() - t0
     ms = ctx.max_over_ranks(a.elapsed_time(b) / 100)
+    host = torch.from_numpy(np.ascontiguousarray(f0.local)).pin_memory()
+    e2e = pfc_e2e(ctx, st, params, distfft.Layout.Y_SLAB, host, 100)
     return {"metric": "PFC time-steps/sec", "value": round(1000.0 / ms, 1), "unit": "steps/s",
             "ms_per_step": round(ms, 5), "wall_s_per_100_steps": round(wall, 5),
-            "config": "2D PFC 256x256 fp64 R2C, 100 steps (configs[0]), launch-bound"}
+            "config": "2D PFC 256x256 fp64 R2C, 100 steps (configs[0]), launch-bound", "e2e": e2e}
 
 
 def run_multi(ctx, args):
@@ -474,7 +523,7 @@ def run_multi(ctx, args):
             "config": f"{n}^3 complex128 full-grid fields, density+composition+v1..v3; {mode}"}
 
 
-def run_pfc(ctx, args, n=None, steps=None, warmup=None):
+def run_pfc(ctx, args, n=None, steps=None, warmup=None, e2e=True):
     import torch
 
     from paper_2603_26818_b200 import _native as nat
@@ -490,6 +539,7 @@ def run_pfc(ctx, args, n=None, steps=None, warmup=None):
     gen = torch.Generator(device=ctx.device).manual_seed(7 + ctx.rank)
     psi0 = torch.rand((n, n, cz), dtype=torch.float64, device=ctx.device, generator=gen)
     psi0.mul_(0.02).add_(-0.3 - 0.01)  # psi_bar - eta + 2 eta U(0,1)
+    host = psi0.cpu().pin_memory() if e2e else None
     f0 = distfft.DistField(grid, distfft.Layout.Z_SLAB, distfft.Space.PHYSICAL, psi0)
     spec = distfft.forward(f0, w)
     del f0, psi0
@@ -522,45 +572,307 @@ def run_pfc(ctx, args, n=None, steps=None, warmup=None):
     if ctx.rank == 0:
         mass_ok = float(st.psi_hat.dev.reshape(-1)[0].real.item()) == mean0
     steps_s = 1000.0 / ms
-    return {"metric": "PFC time-steps/sec", "value": round(steps_s, 3), "unit": "steps/s",
-            "ms_per_step": round(ms, 4), "config": f"3D PFC {n}^3 fp64 R2C slab, dt=0.1 eps=-0.3",
-            "kernels": table, "mass_bit_invariant": mass_ok,
-            "alg_hbm_bytes_per_step": pfc_bytes(n) / ctx.world}
+    res = {"metric": "PFC time-steps/sec", "value": round(steps_s, 3), "unit": "steps/s",
+           "ms_per_step": round(ms, 4), "config": f"3D PFC {n}^3 fp64 R2C slab, dt=0.1 eps=-0.3",
+           "kernels": table, "mass_bit_invariant": mass_ok,
+           "alg_hbm_bytes_per_step": pfc_bytes(n) / ctx.world}
+    if e2e:
+        res["e2e"] = pfc_e2e(ctx, st, params, distfft.Layout.Z_SLAB, host, steps)
+    return res
 
 
 # ------------------------------------------------------------ CPU baseline --
+# The reference's CPU path, timed on this box's host cores.  Preferred: the
+# UNMODIFIED reference package staged by oracle/vendor_reference.py under
+# oracle/_ref/pfcspectral (kind "reference"); where it was not staged, the
+# oracle's restatement (kind "port").  Sizes the reference cannot hold in host
+# RAM (1024^3: ~210 B/point) use the oracle's lean R2C restatement, labelled.
 
-def cpu_cores() -> int:
+def cpu_info() -> dict:
     try:
-        return len(os.sched_getaffinity(0))
+        import psutil
+
+        phys, logical = psutil.cpu_count(logical=False), psutil.cpu_count()
     except Exception:
-        return os.cpu_count() or 1
+        phys, logical = None, os.cpu_count()
+    model = None
+    try:
+        for ln in Path("/proc/cpuinfo").read_text().splitlines():
+            if ln.startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except Exception:
+        pass
+    try:
+        usable = len(os.sched_getaffinity(0))
+    except Exception:
+        usable = logical
+    return {"physical_cores": phys, "logical_cpus": logical, "usable_cpus": usable, "model": model}
 
 
-def cpu_fft_baseline(n: int, seconds: float):
-    """The reference's slab-decomposed C2C round trip (distfft.py:150-173 on
-    transport.py's thread group) restated in oracle/ref_numpy.py, with one
-    worker thread per host core; repeated until `seconds` of work."""
+def cpu_threads() -> int:
+    """Worker threads for the CPU reference: every usable logical CPU (numpy's
+    pocketfft releases the GIL, so the reference's thread workers scale)."""
+    return cpu_info()["usable_cpus"] or 1
+
+
+def host_gib() -> float:
+    try:
+        import psutil
+
+        return psutil.virtual_memory().available / 2**30
+    except Exception:
+        return 0.0
+
+
+def ref_package():
+    """The unmodified reference package (oracle/_ref/pfcspectral), or None."""
+    d = ROOT / "oracle" / "_ref"
+    if not (d / "pfcspectral" / "__init__.py").exists():
+        return None
+    if str(d) not in sys.path:
+        sys.path.insert(0, str(d))
+    import pfcspectral
+
+    return pfcspectral
+
+
+def _oracle():
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import ref_numpy
+
+    return ref_numpy
+
+
+def ref_fft_roundtrips(n: int, threads: int, steps: int, budget_s: float):
+    """distfft.forward + inverse (distfft.py:150-173) of a real n^3 field over
+    spawn_group(threads) (transport.py:174-200), each round trip bracketed by
+    worker barriers; returns (seconds per round trip list, kind)."""
     import numpy as np
 
-    sys.path.insert(0, str(ROOT / "oracle"))
-    import ref_numpy as ora
-
-    cores = cpu_cores()
     x = np.random.default_rng(0).standard_normal((n, n, n))
-    times = []
-    t_end = time.perf_counter() + seconds
-    while True:
+    ref = ref_package()
+    if ref is None:
+        ora = _oracle()
+        ora.dist_roundtrip_threads(x, threads)  # warm-up
+        times = []
+        t_end = time.perf_counter() + budget_s
+        for _ in range(steps):
+            t0 = time.perf_counter()
+            ora.dist_roundtrip_threads(x, threads)
+            times.append(time.perf_counter() - t0)
+            if time.perf_counter() > t_end:
+                break
+        return times, "port"
+    from pfcspectral import distfft as rdf
+    from pfcspectral.grid import GridSpec as RGrid
+    from pfcspectral.transport import spawn_group as rspawn
+
+    grid = RGrid((n, n, n), (1.0, 1.0, 1.0))
+    plan = {"steps": steps}
+
+    def body(w):
+        f = rdf.scatter(x, w, grid, rdf.Layout.Z_SLAB)
+        w.barrier()
         t0 = time.perf_counter()
-        _, back = ora.dist_roundtrip_threads(x, cores)
-        times.append(time.perf_counter() - t0)
-        if time.perf_counter() > t_end or len(times) >= 10:
-            break
+        rdf.inverse(rdf.forward(f, w), w)  # warm-up round trip, sizes the sample
+        w.barrier()
+        t1 = time.perf_counter() - t0
+        if w.rank == 0:
+            plan["steps"] = max(1, min(steps, int(budget_s / max(t1, 1e-9))))
+        w.barrier()
+        out = []
+        for _ in range(plan["steps"]):
+            t0 = time.perf_counter()
+            rdf.inverse(rdf.forward(f, w), w)
+            w.barrier()
+            out.append(time.perf_counter() - t0)
+        return out
+
+    return rspawn(threads, body, timeout=600.0)[0], "reference"
+
+
+def cpu_fft_baseline(n: int, seconds: float) -> dict:
+    threads = cpu_threads()
+    times, kind = ref_fft_roundtrips(n, threads, 10, seconds)
     best = min(times)
-    return {"value": round(fft_bytes(n) / best / 1e9, 4), "unit": "GB/s", "cores": cores,
-            "kind": "port", "s_per_roundtrip": round(best, 3),
-            "sample": f"{len(times)} x C2C round trip of a real {n}^3 fp64 field (reference "
-                      f"algorithm, {cores} worker threads), best of {len(times)}"}
+    src = ("reference package pfcspectral (oracle/_ref), distfft.forward/inverse over spawn_group"
+           if kind == "reference" else "oracle restatement of distfft.py on host threads")
+    return {"value": round(fft_bytes(n) / best / 1e9, 4), "unit": "GB/s", "cores": threads, "kind": kind,
+            "s_per_roundtrip": round(best, 3), "host": cpu_info(),
+            "sample": f"{len(times)} C2C round trips of a real {n}^3 fp64 field ({src}, {threads} worker "
+                      f"threads), best of {len(times)}"}
+
+
+def cpu_pfc2d_baseline(steps: int = 100) -> dict | None:
+    """configs[0] on the host: the reference's pfc_step (pfc.py:96-128) on 2D
+    256^2, 100 steps, G = 1 and G = 4 thread workers (its fastest count in
+    SURVEY.md §6); reports the faster."""
+    ref = ref_package()
+    if ref is None:
+        return None
+    from pfcspectral import distfft as rdf, pfc as rpfc
+    from pfcspectral.grid import GridSpec as RGrid, make_symbols as rsym
+    from pfcspectral.transport import spawn_group as rspawn
+
+    n = (256, 256, 1)
+    grid = RGrid(n, rpfc.default_domain_length(n))
+    psi0 = rpfc.initial_field("constant_plus_noise", grid, psi_bar=-0.3, seed=0, noise_amplitude=0.01)
+    params = rpfc.PfcParams()
+    best = None
+    for G in sorted({1, min(4, cpu_threads())}):
+        def body(w):
+            lay = rdf.layout_for(grid, rdf.Layout.X_SLAB, w.size)
+            st = rpfc.PfcState(psi_hat=rdf.forward(rdf.scatter(psi0, w, grid, rdf.physical_layout(grid)), w),
+                               grid=grid, symbols=rsym(grid, -0.3, layout=lay, rank=w.rank), worker=w)
+            w.barrier()
+            t0 = time.perf_counter()
+            for _ in range(steps):
+                rpfc.pfc_step(st, params)
+            w.barrier()
+            return time.perf_counter() - t0
+
+        t = max(rspawn(G, body, timeout=600.0)) / steps
+        if best is None or t < best[0]:
+            best = (t, G)
+    return {"value": round(1.0 / best[0], 2), "unit": "steps/s", "cores": best[1], "kind": "reference",
+            "sample": f"{steps} steps of the reference pfc_step on 2D 256^2 (configs[0]), best of G = 1 / "
+                      f"{min(4, cpu_threads())} thread workers (G = {best[1]} fastest)"}
+
+
+def cpu_pfc3d_baseline(n: int) -> dict | None:
+    """configs[2] grid on the host: the reference itself needs ~210 B/point of
+    RAM (~210 GiB at 1024^3), so one step of the oracle's lean R2C
+    restatement of pfc.py:96-128 (scipy pocketfft, all host threads) is timed
+    instead, labelled as such; at 512^3 when the host lacks the RAM for n."""
+    import numpy as np
+
+    ora = _oracle()
+    threads = cpu_threads()
+    m = n
+    while m > 256 and host_gib() < 48.0 * (m / 1024) ** 3 + 4:
+        m //= 2
+    shape = (m, m, m)
+    psi_hat = np.fft.rfftn(-0.3 + np.random.default_rng(0).uniform(-0.01, 0.01, shape), axes=(1, 2, 0))
+    L = (2 * np.pi * np.sqrt(3) * (m // 8),) * 3
+    ora.pfc_step_r2c_lean(np.zeros((5, 8, 8), np.complex128), (8, 8, 8), L, -0.3, 0.1, workers=threads)  # warm-up
+    t0 = time.perf_counter()
+    ora.pfc_step_r2c_lean(psi_hat, shape, L, -0.3, 0.1, workers=threads)
+    t = time.perf_counter() - t0
+    return {"value": round(1.0 / t, 5), "unit": "steps/s", "cores": threads, "kind": "port",
+            "grid": list(shape), "s_per_step": round(t, 3),
+            "sample": f"1 step of the oracle's lean R2C restatement of pfc.pfc_step at {m}^3 (the reference "
+                      f"package needs ~210 B/point of host RAM: not runnable at {n}^3), scipy pocketfft with "
+                      f"{threads} threads"}
+
+
+def cpu_hydro_baseline(n: int = 128) -> dict | None:
+    """configs[4] on the host, scaled down: the reference's serial 4-field
+    hydro step (hydro.py:110-126) at 128^3 (512^3 needs ~40 GiB and minutes
+    per step); the composition field has no reference."""
+    import numpy as np
+
+    ref = ref_package()
+    if ref is None:
+        return None
+    from pfcspectral import hydro as rh
+    from pfcspectral.fftcore import fft_nd as rfft
+    from pfcspectral.grid import GridSpec as RGrid, make_symbols as rsym
+    from pfcspectral.pfc import PfcParams as RP
+
+    grid = RGrid((n,) * 3, (2 * np.pi * np.sqrt(3) * (n // 8),) * 3)
+    sym = rsym(grid, -0.3, a0=2.0)
+    hp = rh.HydroParams(pfc=RP(eps=-0.3, dt=0.1), rho=1.0, gamma=1.0, a0=2.0)
+    psi = (-0.3 + 0.02 * (np.random.default_rng(11).random((n,) * 3) - 0.5)).astype(np.complex128)
+    z = np.zeros((n,) * 3, np.complex128)
+    f = rh.HydroFields(psi_hat=rfft(psi), psi=psi, v_hat=[z.copy() for _ in range(3)], v=[z.copy() for _ in range(3)])
+    rh.serial_hydro_step(f, sym, hp)
+    t0 = time.perf_counter()
+    rh.serial_hydro_step(f, sym, hp)
+    t = time.perf_counter() - t0
+    return {"value": round(1.0 / t, 4), "unit": "steps/s", "cores": 1, "kind": "reference",
+            "grid": [n] * 3, "s_per_step": round(t, 3),
+            "sample": f"1 serial 4-field hydro step (psi, v1..v3) of the reference package at {n}^3 on one "
+                      f"thread (serial mode; 512^3 is out of the few-minute budget)"}
+
+
+def spec_bytes(n: int) -> float:
+    """S: one R2C half spectrum of an n^3 fp64 field."""
+    return 16.0 * n * n * (n // 2 + 1)
+
+
+NVLINK_GBS = 770.0  # measured peer copy per direction per GPU (B200_PROFILING.md); nominal 900
+
+
+def combined_roofline(hbm_bytes: float, xchg_bytes: float, G: int, hbm_gbs: float, ms: float) -> dict:
+    """t_roof = HBM bytes / (G B_HBM) + each GPU's transpose bytes
+    X (G-1)/G^2 / B_NVL (SURVEY.md §8d phase-sum); frac = t_roof / t."""
+    t_hbm = hbm_bytes / (G * hbm_gbs * 1e9)
+    nv = xchg_bytes * (G - 1) / (G * G)
+    t_nvl = nv / (NVLINK_GBS * 1e9)
+    t_nom = hbm_bytes / (G * hbm_gbs * 1e9) + nv / 900e9
+    return {"t_roof_ms": round(1e3 * (t_hbm + t_nvl), 4), "t_hbm_ms": round(1e3 * t_hbm, 4),
+            "t_nvlink_ms": round(1e3 * t_nvl, 4), "nvlink_bytes_per_gpu": nv,
+            "frac": round((t_hbm + t_nvl) / (ms * 1e-3), 4), "frac_nominal_nvlink_900": round(t_nom / (ms * 1e-3), 4),
+            "peaks": {"hbm_gbs": hbm_gbs, "nvlink_gbs": NVLINK_GBS}}
+
+
+def _guard(fn):
+    try:
+        return fn()
+    except Exception as exc:  # noqa: BLE001 - a failed side measurement is reported, not fatal
+        return {"error": f"{type(exc).__name__}: {str(exc)[:200]}"}
+
+
+def run_yardstick(ctx, args) -> dict:
+    """Non-product yardstick: cuFFT (torch.fft.rfftn / irfftn, fp64) on the
+    same 512^3 round trip, same algorithmic bytes, CUDA events."""
+    import torch
+
+    n = args.fft_n
+    x = torch.randn((n, n, n), dtype=torch.float64, device=ctx.device)
+
+    def step():
+        torch.fft.irfftn(torch.fft.rfftn(x), s=(n, n, n))
+
+    ms = timed(ctx, step, max(5, args.steps // 2), 3)
+    del x
+    torch.cuda.empty_cache()
+    return {"impl": "cuFFT via torch.fft.rfftn/irfftn (library, not the product path)",
+            "ms_per_step": round(ms, 4), "value": round(fft_bytes(n) / (ms * 1e-3) / 1e9, 1), "unit": "GB/s"}
+
+
+def run_exchange(ctx, args) -> dict:
+    """N > 1: the 1024^3 R2C transpose alone as NCCL all_to_all_single (bus
+    GB/s = bytes each rank sends to the others / time, nccl-tests
+    all-to-all convention) vs NVLink's 770 GB/s measured / 900 nominal."""
+    import torch
+
+    from paper_2603_26818_b200.grid import slab_layout
+
+    n, G = args.pfc_n, ctx.world
+    nxm = n // 2 + 1
+    xl, zl = slab_layout(nxm, G), slab_layout(n, G)
+    me = ctx.rank
+    # Z slab -> X slab: my (nxm, n, cz_me) block rows xl[h] go to rank h
+    send_counts = [xl.counts[h] * n * zl.counts[me] for h in range(G)]
+    recv_counts = [xl.counts[me] * n * zl.counts[h] for h in range(G)]
+    send = torch.randn(sum(send_counts), dtype=torch.complex128, device=ctx.device)
+    recv = torch.empty(sum(recv_counts), dtype=torch.complex128, device=ctx.device)
+
+    def step():
+        ctx.dist.all_to_all_single(recv, send, output_split_sizes=recv_counts, input_split_sizes=send_counts)
+
+    ms = timed(ctx, step, 10, 3)
+    off = (sum(send_counts) - send_counts[me]) * 16
+    bus = ctx.max_over_ranks(off) / (ms * 1e-3) / 1e9
+    del send, recv
+    torch.cuda.empty_cache()
+    return {"nccl_all_to_all": {"grid": [n] * 3, "ms": round(ms, 4), "bytes_to_peers_per_rank": off,
+                                "bus_gbs": round(bus, 1), "frac_of_770": round(bus / NVLINK_GBS, 4),
+                                "frac_of_900": round(bus / 900.0, 4)},
+            "note": "the PFC step's default transposes are fused into the FFT kernels' stores "
+                    "(pfc kernels fft_lines_scatter / pfc_update_z_to); their time is in pfc.kernels"}
 
 
 def main():
@@ -590,13 +902,15 @@ def main():
             pfc_res_keep = pfc_res
             torch.cuda.empty_cache()
             try:
-                pfc_big = run_pfc(ctx, args, n=args.pfc_big_n, steps=max(3, args.steps // 4), warmup=2)
+                pfc_big = run_pfc(ctx, args, n=args.pfc_big_n, steps=max(3, args.steps // 4), warmup=2, e2e=False)
             except Exception as exc:  # noqa: BLE001 - keep the rest of the line
                 pfc_big = {"error": f"{type(exc).__name__}: {str(exc)[:200]}"}
             torch.cuda.empty_cache()
             pfc_res = pfc_res_keep
         pfc2d = None if args.no_pfc else run_pfc2d(ctx, args)
         multi = None if args.no_multi else run_multi(ctx, args)
+        exch = run_exchange(ctx, args) if ctx.world > 1 and not args.no_pfc else None
+        yard = _guard(lambda: run_yardstick(ctx, args)) if ctx.world == 1 else None
     out["clocks"] = clk.summary()
     workload = f"fft{args.fft_n}" if ctx.world == 1 else None
     out["roofline"] = roofline_of(table, hbm, peak_kind, measured_traffic(workload))
@@ -618,9 +932,31 @@ def main():
         out["pfc2d"] = pfc2d
     if multi is not None:
         out["multiphysics"] = multi
+    # combined HBM + NVLink roofline: phase-sum of the HBM
+    # passes over G GPUs and each GPU's share of the transposes over NVLink
+    G = ctx.world
+    out["roofline"]["combined"] = combined_roofline(fft_bytes(args.fft_n), 2 * spec_bytes(args.fft_n), G, hbm,
+                                                    out["ms_per_step"])
+    if pfc_res is not None:
+        pfc_res["roofline"]["combined"] = combined_roofline(pfc_bytes(args.pfc_n), 2 * spec_bytes(args.pfc_n), G,
+                                                            hbm, pfc_res["ms_per_step"])
+    if pfc_big is not None and "error" not in pfc_big:
+        pfc_big["roofline_combined"] = combined_roofline(pfc_bytes(args.pfc_big_n), 2 * spec_bytes(args.pfc_big_n),
+                                                         G, hbm, pfc_big["ms_per_step"])
+    if exch is not None:
+        out["exchange"] = exch
+    if yard is not None:
+        out["yardstick"] = yard
     out["gpu_launches"] = int(out.pop("launches_total"))
     if ctx.rank == 0 and ctx.world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_fft_baseline(args.fft_n, args.cpu_seconds)
+        if not args.no_cpu_sub:
+            if pfc_res is not None:
+                pfc_res["cpu_baseline"] = _guard(lambda: cpu_pfc3d_baseline(args.pfc_n))
+            if pfc2d is not None:
+                pfc2d["cpu_baseline"] = _guard(cpu_pfc2d_baseline)
+            if multi is not None:
+                multi["cpu_baseline"] = _guard(cpu_hydro_baseline)
     if ctx.rank == 0:
         print(json.dumps(out))
     if ctx.dist is not None:
@@ -628,39 +964,32 @@ def main():
 
 
 def main_reference(args):
+    """The reference arm: the reference's own CPU implementation of the
+    headline step (distfft.forward + inverse over its thread worker group,
+    the unmodified package staged at oracle/_ref; the oracle restatement
+    when it is absent) on every usable host CPU, same metric / config /
+    units as our arm.  Under torchrun only rank 0 runs."""
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return
-    import numpy as np
-
-    sys.path.insert(0, str(ROOT / "oracle"))
-    import ref_numpy as ora
-
     n = args.fft_n
-    cores = cpu_cores()
-    x = np.random.default_rng(0).standard_normal((n, n, n))
-    for _ in range(max(0, min(args.warmup, 1))):
-        ora.dist_roundtrip_threads(x, cores)
-    times = []
-    budget = time.perf_counter() + 150.0
-    for _ in range(args.steps):
-        t0 = time.perf_counter()
-        ora.dist_roundtrip_threads(x, cores)
-        times.append(time.perf_counter() - t0)
-        if time.perf_counter() > budget:
-            break
+    threads = cpu_threads()
+    times, kind = ref_fft_roundtrips(n, threads, max(1, args.steps), 150.0)
     s = sum(times) / len(times)
     v = fft_bytes(n) / s / 1e9
+    src = ("reference package pfcspectral (oracle/_ref): distfft.forward/inverse over spawn_group"
+           if kind == "reference" else "oracle restatement of distfft.py on host threads")
     out = {"impl": "reference", "metric": "distributed 3D FFT GB/s (fp64)", "value": round(v, 4),
            "unit": "GB/s", "n_gpus": world, "steps": len(times), "warmup": args.warmup,
            "ms_per_step": round(s * 1e3, 2), "higher_is_better": True, "scaling": "strong",
            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
            "config": {"workload": f"3D FFT round trip {n}^3 fp64 (reference C2C slab algorithm on "
                                   f"host threads)", "grid": [n] * 3},
-           "cpu_baseline": {"value": round(v, 4), "unit": "GB/s", "cores": cores, "kind": "port",
-                            "sample": f"{len(times)} C2C round trips of a real {n}^3 field, "
-                                      f"{cores} worker threads (oracle restatement of distfft.py)"},
+           "cpu_baseline": {"value": round(v, 4), "unit": "GB/s", "cores": threads, "kind": kind,
+                            "host": cpu_info(),
+                            "sample": f"{len(times)} C2C round trips of a real {n}^3 field, {threads} worker "
+                                      f"threads ({src}), after one warm-up round trip"},
            "e2e": {"value": round(v, 4), "unit": "GB/s", "h2d_bytes_per_step": 0,
                    "d2h_bytes_per_step": 0},
            "gpu_launches": 0}

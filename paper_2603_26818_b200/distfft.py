@@ -134,7 +134,18 @@ class DistField:
 
     @property
     def local(self) -> np.ndarray:
-        return self._dev.cpu().numpy()
+        """Read-only host copy of the slab: in-place edits of the copy would
+        not reach the device, so they fail loudly instead of being lost
+        (assign ``field.local = array`` to upload).  Code that edits
+        ``field.dev`` in place must call :meth:`touch` so cached work derived
+        from the field (the PFC engine's prepared inverse) is rebuilt."""
+        a = self._dev.cpu().numpy()
+        a.setflags(write=False)
+        return a
+
+    def touch(self) -> None:
+        """Mark the device slab as modified in place (bumps the version)."""
+        self._version += 1
 
     @local.setter
     def local(self, value) -> None:
@@ -313,10 +324,12 @@ def _pow2(n: int) -> bool:
 def _peer_plan(worker, g: "_Geometry"):
     """Fused-exchange plan for this pipeline, or None (collective path):
     needs G > 1, a y axis to carry the forward scatter and power-of-two
-    y/z lines (PFCS_EXCHANGE=collective disables it)."""
+    y/z lines <= 4096 (PFCS_EXCHANGE=collective disables it)."""
     from .pfc import exchange_mode
 
     if g.G == 1 or g.ny < 2 or not (_pow2(g.ny) and _pow2(g.nz)) or exchange_mode() != "peer":
+        return None
+    if g.ny > 4096 or g.nz > 4096:  # the fused scatter kernels' Stockham lengths
         return None
     if min(g.cz_all) < 2:  # the y-line scatter tiles need >= 2 contiguous z columns
         return None

@@ -63,15 +63,14 @@ def fft_axis(a, axis: int, forward: bool = True):
 
 
 def fft_2d(a, forward: bool = True):
-    """Axes 0 and 1, every z-plane independently (fftcore.py:43-45);
-    forward 0 then 1, inverse 1 then 0."""
+    """Axes 0 and 1, every z-plane independently: axis 0 then axis 1 in
+    both directions, the reference's composition (fftcore.py:43-45)."""
     _check(a.shape, 0)
     t, host = _to_device(a)
     out = torch.empty_like(t)
     if t.numel():
-        first, second = (0, 1) if forward else (1, 0)
-        _axis_inplace(t, first, forward, out)
-        _axis_inplace(out, second, forward, out)
+        _axis_inplace(t, 0, forward, out)
+        _axis_inplace(out, 1, forward, out)
     return out.cpu().numpy() if host else out
 
 

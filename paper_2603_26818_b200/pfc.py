@@ -153,7 +153,10 @@ class _StepEngine:
         if self.G == 1:
             self.work = torch.empty(max(g.zslab_elems, 1), dtype=cdt, device=self.device)
             self.send = self.recv_z = self.recv_x = self.work
-        elif self.fused and g.ny > 1 and min(g.cz_all) > 1 and exchange_mode() == "peer":
+        elif (self.fused and g.ny > 1 and _pow2(g.ny) and g.ny <= 4096 and min(g.cz_all) > 1
+              and exchange_mode() == "peer"):
+            # the fused y-line scatter (pfcs_fft_lines_scatter) needs
+            # power-of-two y lines <= 4096; other y extents take the collective
             self._setup_peer()
         else:
             self.send = torch.empty(max(g.xslab_elems, 1), dtype=cdt, device=self.device)

@@ -206,10 +206,15 @@ def run_pfc(config: RunConfig, *, real: bool = True) -> RunResult:
             done = 0
             for ev in _events(params.n_steps, config.io.diag_every,
                               config.io.snap_every if out is not None else None):
+                # steps before the last one of the block run back to back;
+                # step_wall_seconds is the wall time of the single step just
+                # before the diagnostic row, as in the reference (run.py:166-169)
+                if ev - done > 1:
+                    pfc.pfc_run(state, params, ev - done - 1, realness=result.realness)
                 torch.cuda.synchronize()
                 t0 = time.perf_counter()
-                pfc.pfc_run(state, params, ev - done, realness=result.realness)
-                wall = (time.perf_counter() - t0) / (ev - done)
+                pfc.pfc_run(state, params, 1, realness=result.realness)
+                wall = time.perf_counter() - t0
                 done = ev
                 if ev % config.io.diag_every == 0 or ev == params.n_steps:
                     record(wall)

@@ -96,6 +96,17 @@ def read_snapshot(path) -> tuple[SnapshotHeader, np.ndarray]:
     return hdr, data.reshape(hdr.shape, order="F").copy()
 
 
+def _pwrite_all(fd: int, data: memoryview, offset: int) -> None:
+    """os.pwrite until every byte is written (short writes happen on network
+    and parallel filesystems); a zero-byte write raises."""
+    done = 0
+    while done < len(data):
+        n = os.pwrite(fd, data[done:], offset + done)
+        if n <= 0:
+            raise OSError(f"short snapshot write at offset {offset + done}")
+        done += n
+
+
 def write_snapshot_slabs(path, field, worker, step: int, sim_time: float, meta: dict | None = None,
                          chunk_planes: int | None = None) -> Path:
     """Collective snapshot of a physical field (3D Z_SLAB or 2D Y_SLAB)
@@ -146,7 +157,7 @@ def write_snapshot_slabs(path, field, worker, step: int, sim_time: float, meta: 
                 buf = host.numpy()
             else:
                 buf = np.ascontiguousarray(blk.reshape(-1).numpy())
-            os.pwrite(fd, memoryview(buf).cast("B"), HEADER_BYTES + 8 * plane * (p0 + c0))
+            _pwrite_all(fd, memoryview(buf).cast("B"), HEADER_BYTES + 8 * plane * (p0 + c0))
     finally:
         os.close(fd)
     worker.barrier()

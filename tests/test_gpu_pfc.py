@@ -337,3 +337,25 @@ np.savez(sys.argv[1], a=a, r=r, k=k)
     assert int(out["1"]["k"]) == 58
     np.testing.assert_array_equal(out["0"]["a"], out["1"]["a"])
     np.testing.assert_array_equal(out["0"]["r"], out["1"]["r"])
+
+
+@pytest.mark.parametrize("real", [True, False])
+@pytest.mark.parametrize("n", [(32, 24, 32), (16, 12, 64)])
+def test_peer_default_with_non_pow2_y(pkg, n, real):
+    """Power-of-two x and z with a non-power-of-two y at G = 2 (default
+    PFCS_EXCHANGE=peer): the fused y-line scatter only takes power-of-two y
+    lines, so the engine must fall back to the collective exchange and stay
+    bit-identical to G = 1."""
+    from paper_2603_26818_b200 import distfft, pfc
+
+    grid = pkg.GridSpec(n, pfc.default_domain_length(n))
+    psi0 = pfc.initial_field("constant_plus_noise", grid, seed=4, noise_amplitude=0.05)
+
+    def body(w):
+        st = make_state(pkg, w, grid, psi0, real=real)
+        pfc.pfc_run(st, pfc.PfcParams(), 5)
+        return distfft.gather(st.psi_hat, w)
+
+    ref = pkg.spawn_group(1, body)[0]
+    got = pkg.spawn_group(2, body)[0]
+    np.testing.assert_array_equal(got, ref)
