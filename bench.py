@@ -463,7 +463,7 @@ def run_pfc2d(ctx, args):
     torch.cuda.synchronize()
     wall = time.perf_counter() - t0
     ms = ctx.max_over_ranks(a.elapsed_time(b) / 100)
-    host = torch.from_numpy(np.ascontiguousarray(f0.local)).pin_memory()
+    host = torch.from_numpy(np.array(f0.local)).pin_memory()
     e2e = pfc_e2e(ctx, st, params, distfft.Layout.Y_SLAB, host, 100)
     return {"metric": "PFC time-steps/sec", "value": round(1000.0 / ms, 1), "unit": "steps/s",
             "ms_per_step": round(ms, 5), "wall_s_per_100_steps": round(wall, 5),

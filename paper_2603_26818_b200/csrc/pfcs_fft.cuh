@@ -257,14 +257,31 @@ __device__ __forceinline__ void dft_r(double2 (&y)[r]) {
   }
 }
 
+// Barrier flavours of the shared-memory exchanges: the whole CTA (tiles whose
+// lines are interleaved across warps), or a named barrier over the `n`
+// threads of one line group (line-major tiles: each line's warps exchange
+// through their own workspace and synchronise only among themselves, so
+// different lines drift into different phases and the fp64 and shared-memory
+// pipes overlap instead of alternating CTA-wide).
+struct CtaSync {
+  __device__ __forceinline__ void operator()() const { __syncthreads(); }
+};
+struct BarSync {
+  unsigned id, n;  // barrier id (1..15; 0 is __syncthreads), participating threads
+  __device__ __forceinline__ void operator()() const {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+  }
+};
+
 // One Stockham pass (span Ns) followed, if more passes remain, by the
 // shared-memory exchange and the next pass.  On entry v[e] holds element
 // j + P*e of this pass's input; on exit of the last pass v[e] holds output
 // element j + P*e.  `tw` is the size-N table exp(-2 pi i m / N), m < N,
 // read with stride TWS (so a size-2N table serves an N-point transform).
-template <int N, int Ns, bool FWD, int TWS, int TWL = PFCS_TW_LOADS, int R = radix_R(N), bool TSM = false>
+template <int N, int Ns, bool FWD, int TWS, int TWL = PFCS_TW_LOADS, int R = radix_R(N), bool TSM = false,
+          class Sync = CtaSync>
 __device__ __forceinline__ void fft_pass(double2 (&v)[R], int j, double2* sl,
-                                         const double2* __restrict__ tw) {
+                                         const double2* __restrict__ tw, Sync sync = Sync{}) {
   // R = values per thread (8, or 4 for the register-heavy fused passes);
   // each pass uses radix min(R, remaining) and R/r butterflies per thread
   constexpr int P = N / R;
@@ -320,7 +337,7 @@ __device__ __forceinline__ void fft_pass(double2 (&v)[R], int j, double2* sl,
     for (int q = 0; q < r; ++q) v[s + q * S] = y[q];
   }
   if constexpr (Ns * r < N) {
-    __syncthreads();
+    sync();
 #pragma unroll
     for (int s = 0; s < S; ++s) {
       const int b = j + s * P;
@@ -329,19 +346,20 @@ __device__ __forceinline__ void fft_pass(double2 (&v)[R], int j, double2* sl,
 #pragma unroll
       for (int q = 0; q < r; ++q) sl[pad_idx(base + q * Ns)] = v[s + q * S];
     }
-    __syncthreads();
+    sync();
 #pragma unroll
     for (int e = 0; e < R; ++e) v[e] = sl[pad_idx(j + P * e)];
-    fft_pass<N, Ns * r, FWD, TWS, TWL, R, TSM>(v, j, sl, tw);
+    fft_pass<N, Ns * r, FWD, TWS, TWL, R, TSM, Sync>(v, j, sl, tw, sync);
   }
 }
 
 // Full N-point transform of the register set (see fft_pass).  All threads of
 // the CTA must call it (it contains __syncthreads when N > 8).
-template <int N, bool FWD, int TWS = 1, int TWL = PFCS_TW_LOADS, int R = radix_R(N), bool TSM = false>
+template <int N, bool FWD, int TWS = 1, int TWL = PFCS_TW_LOADS, int R = radix_R(N), bool TSM = false,
+          class Sync = CtaSync>
 __device__ __forceinline__ void fft_line(double2 (&v)[R], int j, double2* sl,
-                                         const double2* __restrict__ tw) {
-  fft_pass<N, 1, FWD, TWS, TWL, R, TSM>(v, j, sl, tw);
+                                         const double2* __restrict__ tw, Sync sync = Sync{}) {
+  fft_pass<N, 1, FWD, TWS, TWL, R, TSM, Sync>(v, j, sl, tw, sync);
 }
 
 // Stash register set (element j + P*e in v[e]) into the padded smem line.

@@ -34,7 +34,10 @@ inline int ilog2(long long n) {
 // when it does not apply to the call.
 bool tma_enabled();
 bool make_tmap(CUtensorMap* map, int rank, const void* base, const unsigned long long* dims,
-               const unsigned long long* strides_bytes, const unsigned* box);
+               const unsigned long long* strides_bytes, const unsigned* box, int swizzle_bytes = 0);
+// Line-synchronous TMA cube pass (pfcs_cube.cu); returns 1 when it does not
+// apply (the caller then runs k_real_x MODE_CUBE)
+int launch_cube_ls(void* data, long long nx, long long inner, double* diag, cudaStream_t st);
 struct SlabSplitH;
 struct PeerTable;
 struct Pro;

@@ -147,7 +147,7 @@ static EncodeTiledFn encode_fn();
 // Tiled FLOAT64 tensor map (rank <= 3); false when the driver rejects it or
 // the entry point is unavailable (callers then take the non-TMA kernels).
 bool make_tmap(CUtensorMap* map, int rank, const void* base, const unsigned long long* dims,
-               const unsigned long long* strides_bytes, const unsigned* box) {
+               const unsigned long long* strides_bytes, const unsigned* box, int swizzle_bytes) {
   EncodeTiledFn enc = encode_fn();
   if (!enc || ((uintptr_t)base & 15)) return false;
   cuuint64_t d[3], s[2];
@@ -157,8 +157,12 @@ bool make_tmap(CUtensorMap* map, int rank, const void* base, const unsigned long
     b[k] = box[k];
     if (k + 1 < rank) s[k] = strides_bytes[k];
   }
+  const CUtensorMapSwizzle sw = swizzle_bytes == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                                : swizzle_bytes == 64  ? CU_TENSOR_MAP_SWIZZLE_64B
+                                : swizzle_bytes == 32  ? CU_TENSOR_MAP_SWIZZLE_32B
+                                                       : CU_TENSOR_MAP_SWIZZLE_NONE;
   return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, (cuuint32_t)rank, (void*)base, d, s, b, e,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 

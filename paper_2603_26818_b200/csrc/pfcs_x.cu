@@ -22,6 +22,8 @@
 // All kernels are persistent with register-pipelined loads (reg_tile_loop).
 // A tile is T adjacent inner columns (the contiguous y*z extent), so each
 // row of a tile is one T*16 (complex) or T*8 (real) byte segment.
+#include <stdlib.h>
+
 #include "pfcs_diag.cuh"
 #include "pfcs_fft.cuh"
 #include "pfcs_internal.h"
@@ -338,6 +340,249 @@ __global__ void __launch_bounds__(T*(M / real_R(M, MODE)),
   if (MODE == MODE_CUBE) diag_block_max(diag, m_abs, 0.0, m_abs);
 }
 
+// ------------------------------------------- line-synchronous cube pass --
+// Same arithmetic as k_real_x<M, T, 3, MODE_CUBE> (bit-identical), different
+// execution: the CTA-wide barriers of the interleaved tile made all 16 warps
+// alternate in lock step between butterflies (fp64 pipe) and exchanges
+// (shared-memory pipe) — ncu: fp64 49.6 % + smem 48.9 % busy, issue 40 %,
+// i.e. the two pipes never overlap.  Here
+//   * a line's P threads are consecutive (line-major), exchange through that
+//     line's own padded workspace and synchronise on a named barrier of P
+//     threads only, so the T lines of a tile drift into different phases;
+//   * the HBM tile still moves as T*16-byte rows: TMA loads it into a
+//     swizzled stage (row r, column t at chunk t ^ f(r): the line-major
+//     stage reads are conflict-free), results are written back into the same
+//     stage column and leave through a TMA tensor STORE, so the global stores
+//     stay full rows too;
+//   * no CTA-wide barrier in the tile loop: each line's leader counts its line
+//     in on the stage; the LAST line to finish a tile stores the stage and
+//     refills it with the tile after next (no producer warp, so 16 warps keep
+//     128 registers each), while the other lines already work on the other
+//     stage.
+template <int M, int T>
+struct CubeLs {
+  static constexpr int R = 8;
+  static constexpr int P = M / R;
+  static constexpr int LS = pad_idx(M);               // per-line workspace (contiguous mapping)
+  static constexpr int ROWB = T * 16;                 // bytes per stage row (= swizzle span)
+  static constexpr size_t STAGE = (size_t)(M + 1) * ROWB;
+  static constexpr size_t PADDED = (STAGE + 1023) / 1024 * 1024;
+  static constexpr int BR = M < 256 ? M : 256;        // rows per TMA box
+  static constexpr int NB = M / BR;
+  static constexpr int THREADS = T * P;
+  static constexpr size_t SMEM = 2 * PADDED + (size_t)T * LS * 16 + 64 + 1024;
+  // stage element (row r, column t) under the TMA swizzle of a ROWB-byte row
+  __device__ __forceinline__ static int at(int r, int t) {
+    return r * T + (t ^ ((r * ROWB >> 7) & (T - 1)));
+  }
+};
+
+// Results go back into the line's stage column and leave through a TMA
+// tensor store; the stage is refilled once the store has read it.  (Storing
+// straight from registers instead — 16 bytes per thread and row, so the stage
+// could be refilled right after the reads — measured 3.2x slower on the
+// B200: 5.18 -> 16.7 ms per 1024^3 launch.)
+//
+// Scale folding: the inverse transform's fl(1/N) is an exact power of two, so
+// it commutes with every rounding of the cube, the forward FFT and the R2C
+// split; it is applied once, as s^3 (0.5 s^3 where the split halves) on the
+// final modes, and max|psi| is scaled once at the end — bit-identical to
+// scaling each sample (no subnormal intermediates on this path).
+template <int M, int T>
+__global__ void __launch_bounds__(CubeLs<M, T>::THREADS, 1)
+    k_cube_ls(double2* data, i64 inner, const double2* __restrict__ twN, double scale, double* diag,
+              const __grid_constant__ TmaPair tm) {
+  pdl_wait();
+  using C = CubeLs<M, T>;
+  constexpr int R = C::R;
+  constexpr int P = C::P;
+  extern __shared__ unsigned char craw[];
+  unsigned char* cbase = craw + ((1024u - (smem_u32(craw) & 1023u)) & 1023u);
+  double2* ws = (double2*)(cbase + 2 * C::PADDED);
+  unsigned long long* full = (unsigned long long*)(ws + (size_t)T * C::LS);
+  unsigned* done = (unsigned*)(full + 2);  // lines finished with the stage's tile
+  const int tid = threadIdx.x;
+  const i64 ntiles = (inner + T - 1) / T;
+  double m_abs = 0.0;
+
+  // TMA transfer of one tile between global memory and stage s
+  auto xfer = [&](i64 tile, int s, bool load) {
+    const int c0 = (int)(2 * tile * T);
+    unsigned char* buf = cbase + (size_t)s * C::PADDED;
+#pragma unroll
+    for (int b = 0; b < C::NB; ++b) {
+      if (load) tma_load_2d(buf + (size_t)b * C::BR * C::ROWB, &tm.a, &full[s], c0, b * C::BR);
+      else tma_store_2d(&tm.a, buf + (size_t)b * C::BR * C::ROWB, c0, b * C::BR);
+    }
+    if (load) tma_load_2d(buf + (size_t)M * C::ROWB, &tm.b, &full[s], c0, M);
+    else tma_store_2d(&tm.b, buf + (size_t)M * C::ROWB, c0, M);
+  };
+  // line leader, once its line is done with stage s of `tile`: the last line
+  // of the tile (stores the stage and) refills it with the tile after next
+  auto release = [&](i64 tile, int s) {
+    __threadfence_block();
+    const unsigned prev = atomicAdd(&done[s], 1u);
+    if (prev == (unsigned)T - 1) {
+      __threadfence_block();
+      done[s] = 0;
+      const i64 nxt = tile + 2 * (i64)gridDim.x;
+      fence_proxy_async();
+      xfer(tile, s, false);
+      bulk_commit();
+      if (nxt < ntiles) {
+        bulk_wait_read0();
+        fence_proxy_async();
+        mbar_expect_tx(&full[s], (unsigned)C::STAGE);
+        xfer(nxt, s, true);
+      }
+    }
+  };
+
+  if (tid == 0) {
+    mbar_init(&full[0], 1);
+    mbar_init(&full[1], 1);
+    done[0] = done[1] = 0;
+    mbar_fence_init();
+    for (int s = 0; s < 2; ++s) {
+      const i64 tile = blockIdx.x + (i64)s * gridDim.x;
+      if (tile < ntiles) {
+        mbar_expect_tx(&full[s], (unsigned)C::STAGE);
+        xfer(tile, s, true);
+      }
+    }
+  }
+  __syncthreads();
+
+  const int t = tid / P;  // line of the tile, position j = tid % P
+  const BarSync lsync{1u + (unsigned)t, (unsigned)P};
+  double2* sl = ws + t * C::LS;
+  int it = 0;
+  for (i64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+    const int s = it & 1;
+    const int jj = opaque((int)(opaque_tid() % P));
+    const double2* cur = (const double2*)(cbase + (size_t)s * C::PADDED);
+    mbar_wait(&full[s], (unsigned)((it >> 1) & 1));
+    const double2 wj = __ldg(&twN[jj]);
+    double2 v[R];
+#pragma unroll
+    for (int e = 0; e < R; ++e) v[e] = cur[C::at(jj + P * e, t)];
+    // C2R pre-twiddle (as k_real_x MODE_CUBE), mirror rows from the stage
+#pragma unroll
+    for (int e = 0; e < R; ++e) {
+      const int k = jj + P * e;
+      double2 a = v[e];
+      double2 bm = cur[C::at(M - k, t)];  // row M for k = 0
+      if (k == 0) {
+        a.y = 0.0;
+        bm.y = 0.0;
+      }
+      const double2 b = make_double2(bm.x, -bm.y);
+      const double2 sm = cadd(a, b);
+      const double2 d = csub(a, b);
+      const double2 w = twiddle_k<R>(twN, wj, jj, e, P);
+      const double2 wd = make_double2(fma(d.x, w.x, d.y * w.y), fma(d.y, w.x, -d.x * w.y));
+      v[e] = make_double2(sm.x - wd.y, sm.y + wd.x);
+    }
+    fft_line<M, false, 2, PFCS_X_TWL, R, false, BarSync>(v, jj, sl, twN, lsync);
+    const bool ok = (i64)opaque((int)(tile * T)) + t < inner;
+#pragma unroll
+    for (int e = 0; e < R; ++e) {
+      const double a = v[e].x, b = v[e].y;  // unscaled (see above)
+      if (ok) m_abs = dmax_bits(m_abs, dmax_bits(fabs(a), fabs(b)));
+      v[e] = make_double2(__dmul_rn(__dmul_rn(a, a), a), __dmul_rn(__dmul_rn(b, b), b));
+    }
+    const unsigned tid2 = opaque_tid();
+    const int j2 = (int)(tid2 % P), t2 = (int)(tid2 / P);
+    fft_line<M, true, 2, PFCS_X_TWL, R, false, BarSync>(v, j2, ws + t2 * C::LS, twN, lsync);
+    // R2C split: pair Z_k with Z_{M-k} through the line's stage column (rows
+    // last read before the FFT's barriers; the swizzle keeps any 8
+    // consecutive rows on distinct banks, for the stash and the mirrored
+    // reads alike)
+    double2* col = (double2*)(cbase + (size_t)(opaque(it) & 1) * C::PADDED);
+#pragma unroll
+    for (int e = 0; e < R; ++e) col[C::at(j2 + P * e, t2)] = v[e];
+    lsync();
+    {
+      double sc = scale;
+      asm volatile("" : "+d"(sc));  // keep s^3 local (no loop-long registers)
+      const double s3 = sc * sc * sc, hs3 = 0.5 * s3;
+      const double2 wj2 = __ldg(&twN[j2]);
+      const double2 xm = make_double2((v[0].x - v[0].y) * s3, 0.0);  // Nyquist mode (j == 0)
+#pragma unroll
+      for (int e = 0; e < R; ++e) {
+        const int k = j2 + P * e;
+        const int km = (M - k) & (M - 1);
+        const double2 zk = v[e];
+        const double2 zm = col[C::at(km, t2)];
+        double2 x;
+        if (k == 0) {
+          x = make_double2((zk.x + zk.y) * s3, 0.0);
+        } else {
+          const double2 sp = make_double2(zk.x + zm.x, zk.y - zm.y);
+          const double2 d = make_double2(zk.x - zm.x, zk.y + zm.y);
+          const double2 w = twiddle_k<R>(twN, wj2, j2, e, P);
+          const double2 wd = make_double2(fma(d.x, w.x, -d.y * w.y), fma(d.x, w.y, d.y * w.x));
+          x = make_double2(hs3 * (sp.x + wd.y), hs3 * (sp.y - wd.x));
+        }
+        v[e] = x;
+      }
+      lsync();  // every mirror read of the column is done
+#pragma unroll
+      for (int e = 0; e < R; ++e) col[C::at(j2 + P * e, t2)] = v[e];
+      if (j2 == 0) col[C::at(M, t2)] = xm;
+      fence_proxy_async();  // my stage writes before the async-proxy store
+      lsync();
+      if (j2 == 0) release(tile, s);
+    }
+  }
+  if (threadIdx.x % P == 0) bulk_wait0();  // stores this thread issued have completed
+  m_abs *= scale;  // exact (power of two)
+  diag_block_max(diag, m_abs, 0.0, m_abs);
+}
+
+template <int M, int T>
+static int cube_ls_m(void* data, i64 inner, double* diag, cudaStream_t st) {
+  using C = CubeLs<M, T>;
+  static_assert(C::ROWB == 128 || C::ROWB == 64, "stage rows of 64 or 128 bytes (TMA swizzle span)");
+  if (2 * inner >= (1LL << 31) || ((uintptr_t)data & 15)) return 1;
+  const double2* twN = twiddles(2 * M);
+  if (!twN) return PFCS_E_CUDA;
+  TmaPair tm{};
+  const unsigned long long dims[2] = {(unsigned long long)(2 * inner), (unsigned long long)(M + 1)};
+  const unsigned long long str[1] = {(unsigned long long)inner * 16};
+  const unsigned box[2] = {(unsigned)(2 * T), (unsigned)C::BR};
+  const unsigned box1[2] = {(unsigned)(2 * T), 1u};
+  if (!make_tmap(&tm.a, 2, data, dims, str, box, C::ROWB) || !make_tmap(&tm.b, 2, data, dims, str, box1, C::ROWB))
+    return 1;
+  const i64 ntiles = (inner + T - 1) / T;
+  int grid = 0;
+  auto kern = k_cube_ls<M, T>;
+  if (int rc = persistent_grid((const void*)kern, C::THREADS, C::SMEM, ntiles, &grid)) return rc;
+  launch_pdl(kern, dim3(grid), dim3(C::THREADS), C::SMEM, st, (double2*)data, inner, twN, 1.0 / (double)(2 * M),
+             diag, tm);
+  return check_launch("k_cube_ls");
+}
+
+// PFCS_CUBE_LS=0 selects k_real_x MODE_CUBE instead (A/B; bit-identical)
+static int cube_ls_mode() {
+  static const int m = [] {
+    const char* v = getenv("PFCS_CUBE_LS");
+    return (v && *v) ? atoi(v) : 1;
+  }();
+  return m;
+}
+
+int launch_cube_ls(void* data, long long nx, long long inner, double* diag, cudaStream_t st) {
+  const int mode = cube_ls_mode();
+  if (mode == 0 || !tma_enabled()) return 1;
+  // production tiles only: enough T-wide tiles to fill every SM
+  // (T = 4 at M = 512 — two 256-thread CTAs per SM, 64-byte rows — measured
+  // 5.15 -> 7.44 ms per 1024^3 launch: 128-byte rows stay)
+  if (nx == 1024 && inner >= 8 * 148) return cube_ls_m<512, 8>(data, inner, diag, st);
+  if (nx == 2048 && inner >= 4 * 148) return cube_ls_m<1024, 4>(data, inner, diag, st);
+  return 1;
+}
+
 // Fused complex-data cube pass (C2C mode, reference-layout fields):
 // inverse x FFT -> psi*(psi*psi) (numpy complex power, pfc.py:109) -> forward.
 template <int N, int T, int ST>
@@ -496,6 +741,10 @@ int launch_real_x(const void* in, void* out, long long nx, long long inner, int 
   case MM:                                                                              \
     if (mode == MODE_R2C) return real_x_m<MM, MODE_R2C>(in, out, inner, diag, st);     \
     if (mode == MODE_C2R) return real_x_m<MM, MODE_C2R>(in, out, inner, diag, st);     \
+    if (in == out) {                                                                   \
+      const int rc = launch_cube_ls(out, nx, inner, diag, st);                        \
+      if (rc != 1) return rc;                                                         \
+    }                                                                                 \
     return real_x_m<MM, MODE_CUBE>(in, out, inner, diag, st);
     PFCS_M_CASES(PFCS_CASE)
 #undef PFCS_CASE

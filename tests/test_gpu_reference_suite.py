@@ -50,7 +50,7 @@ def test_reference_suite_passes_against_package(tmp_path):
     xml = tmp_path / "refsuite.xml"
     cmd = [sys.executable, "-m", "pytest", str(SUITE), "-q", "-p", "no:cacheprovider", f"--junitxml={xml}",
            *(f"--ignore={SUITE / f}" for f in IGNORED),
-           *(f"--deselect={SUITE / t}" for t in DESELECTED)]
+           "-k", " and ".join(f"not {t.split('::')[-1]}" for t in DESELECTED)]
     res = subprocess.run(cmd, cwd=str(SUITE), capture_output=True, text=True, timeout=1800)
     root = ET.parse(xml).getroot()
     suite = root if root.tag == "testsuite" else root.find("testsuite")

@@ -73,7 +73,9 @@ np.savez({path!r}, **out)
 """
 
 ZCASES = [(3, 5, 256), (2, 7, 1024), (5, 3, 64), (4, 4, 512)]
-XCASES = [(128, 96), (256, 1000), (512, 1030), (1024, 520), (1024, 64)]
+# (1024, 3000) and (2048, 1000): production tiles of the line-synchronous cube
+# pass k_cube_ls (PFCS_TMA=1) against the register-pipelined k_real_x
+XCASES = [(128, 96), (256, 1000), (512, 1030), (1024, 520), (1024, 64), (1024, 3000), (2048, 1000)]
 CASES = [(3, 64, 40), (2, 128, 33), (2, 256, 16), (2, 512, 9), (3, 1024, 12), (1, 2048, 5), (2, 1024, 1000)]
 
 
@@ -137,3 +139,19 @@ def test_tma_z_update_multi_rank_bit_identical(tmp_path):
         res[flag] = np.load(path)
     for k in res["0"].files:
         assert np.array_equal(res["0"][k], res["1"][k]), k
+
+
+def test_cube_ls_bit_identical(tmp_path):
+    """k_cube_ls (line-synchronous, TMA load + store) reproduces the
+    interleaved-tile TMA cube pass k_real_x<M, T, 3, MODE_CUBE> bit for bit,
+    incl. ragged last tiles and the max|psi| diagnostic."""
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    a = _run(tmp_path, "ls1", {"PFCS_CUBE_LS": "1"})
+    b = _run(tmp_path, "ls0", {"PFCS_CUBE_LS": "0"})
+    keys = [k for k in a.files if k.startswith("x")]
+    assert any(k.startswith("x1024_3000") for k in keys)
+    for k in keys:
+        assert np.array_equal(a[k], b[k]), k
