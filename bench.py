@@ -470,10 +470,21 @@ def run_pfc2d(ctx, args):
             "config": "2D PFC 256x256 fp64 R2C, 100 steps (configs[0]), launch-bound", "e2e": e2e}
 
 
+def multi_bytes(n: int) -> float:
+    """Algorithmic HBM bytes of one serial R2C multiphysics step (beta = 0):
+    23 transforms of R + 5S, the real pointwise passes (2 x adv3 7R, 2 x cube
+    2R, chnl 2R, 3 x product 3R = 29R) and the spectral updates / mu
+    (psi 4S, c 4S, mu 3S, 3 x velocity 3S = 20S)."""
+    R = 8.0 * n**3
+    S = spec_bytes(n)
+    return 23 * (R + 5 * S) + 29 * R + 20 * S
+
+
 def run_multi(ctx, args):
     """configs[4]: multiphysics PFC (density + composition + 3 velocities),
-    field-per-GPU: 1 GPU runs all roles, 4 GPUs the reference's four-role
-    hydro dataflow, 5 / 8 GPUs the multiphysics role maps."""
+    field-per-GPU: 1 GPU runs all roles, 5 / 8 GPUs the multiphysics role
+    maps (real fields: the R2C path), 4 GPUs the reference's four-role hydro
+    dataflow (complex full-grid fields, as the reference holds them)."""
     import numpy as np
     import torch
 
@@ -490,37 +501,80 @@ def run_multi(ctx, args):
     mp = mpx.MultiParams(hydro=hp, mobility=1.0, kappa=1.0, alpha=1.0, beta=0.0)
     sym = make_symbols(grid, -0.3, a0=2.0)
     gen = torch.Generator(device=ctx.device).manual_seed(11)
-    C = torch.complex128
+    real = G != 4
 
     def field(scale, base=0.0):
         x = torch.rand((n,) * 3, dtype=torch.float64, device=ctx.device, generator=gen)
-        return (base + scale * (x - 0.5)).to(C)
+        x = base + scale * (x - 0.5)
+        return x if real else x.to(torch.complex128)
 
     psi = field(0.02, -0.3)
     c = field(0.2)
-    zeros = torch.zeros((n,) * 3, dtype=C, device=ctx.device)
-    f = mpx.MultiFields(psi_hat=hydro._fft(psi, True), psi=psi, c_hat=hydro._fft(c, True), c=c,
-                        v_hat=[zeros.clone() for _ in range(3)], v=[zeros.clone() for _ in range(3)])
     w = ctx.worker()
+    if real:
+        R3 = mpx._Real3.of((n,) * 3, sym, ctx.device)
+        zeros = torch.zeros((n,) * 3, dtype=torch.float64, device=ctx.device)
+        f = mpx.MultiFields(psi_hat=R3.fwd(psi), psi=psi, c_hat=R3.fwd(c), c=c,
+                            v_hat=[R3.fwd(zeros) for _ in range(3)], v=[zeros.clone() for _ in range(3)])
+    else:
+        zeros = torch.zeros((n,) * 3, dtype=torch.complex128, device=ctx.device)
+        f = mpx.MultiFields(psi_hat=hydro._fft(psi, True), psi=psi, c_hat=hydro._fft(c, True), c=c,
+                            v_hat=[zeros.clone() for _ in range(3)], v=[zeros.clone() for _ in range(3)])
     torch.cuda.empty_cache()  # the FFT/PFC workloads' blocks are not reused here
     steps = max(3, args.steps // 4)
     if G == 1:
         fn = lambda: mpx.serial_multi_step(f, sym, mp)  # noqa: E731
-        mode = "all 5 roles on 1 GPU"
+        mode = "all 5 roles on 1 GPU (R2C: real fields, x-halved spectra)"
     elif G == 4:
         hf = hydro.HydroFields(psi_hat=f.psi_hat, psi=f.psi, v_hat=f.v_hat, v=f.v)
         st = ({"psi_hat": hf.psi_hat, "psi": hf.psi, "v": list(hf.v), "step_index": 0} if ctx.rank == 0
               else {"v_hat": zeros.clone(), "psi": zeros.clone(), "step_index": 0})
         fn = lambda: hydro.parallel_hydro_step(w, st, sym, hp)  # noqa: E731
-        mode = "reference 4-role hydro dataflow (psi, v1..v3), no composition"
+        mode = "reference 4-role hydro dataflow (psi, v1..v3), complex fields, no composition"
     else:
         st = mpx.initial_role_state(ctx.rank, G, f)
         fn = lambda: mpx.parallel_multi_step(w, st, sym, mp)  # noqa: E731
-        mode = f"{G}-role field-per-GPU map {mpx.ROLES[G]}"
+        mode = f"{G}-role field-per-GPU map {mpx.ROLES[G]} (R2C)"
     ms = timed(ctx, fn, steps, 2)
-    return {"metric": "multiphysics PFC time-steps/sec", "value": round(1000.0 / ms, 3), "unit": "steps/s",
-            "ms_per_step": round(ms, 3), "steps": steps,
-            "config": f"{n}^3 complex128 full-grid fields, density+composition+v1..v3; {mode}"}
+    res = {"metric": "multiphysics PFC time-steps/sec", "value": round(1000.0 / ms, 3), "unit": "steps/s",
+           "ms_per_step": round(ms, 3), "steps": steps,
+           "config": f"{n}^3 fp64 density+composition+v1..v3; {mode}"}
+    if G == 1:
+        hbm, kind = peaks()
+        alg = multi_bytes(n)
+        res["roofline"] = {"bound": "hbm", "alg_bytes_per_step": alg, "achieved": round(alg / (ms * 1e-3) / 1e9, 1),
+                           "peak": hbm, "unit": "GB/s", "frac": round(alg / (ms * 1e-3) / 1e9 / hbm, 4),
+                           "model": "23 R2C transforms x (R + 5S) + 29R real pointwise + 20S spectral updates"}
+        # e2e: host psi, c (pinned) in -> forward transforms -> K steps -> psi, c, v out
+        hp_in = [x.cpu().pin_memory() for x in (psi, c)]
+        outs = [torch.empty_like(hp_in[0]).pin_memory() for _ in range(5)]
+
+        def run_e2e():
+            dev = [x.to(ctx.device, non_blocking=True) for x in hp_in]
+            z = torch.zeros_like(dev[0])
+            ff = mpx.MultiFields(psi_hat=R3.fwd(dev[0]), psi=dev[0], c_hat=R3.fwd(dev[1]), c=dev[1],
+                                 v_hat=[R3.fwd(z) for _ in range(3)], v=[z.clone() for _ in range(3)])
+            for _ in range(steps):
+                mpx.serial_multi_step(ff, sym, mp)
+            for o, x in zip(outs, [ff.psi, ff.c, *ff.v]):
+                o.copy_(x, non_blocking=True)
+
+        run_e2e()
+        torch.cuda.synchronize()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record()
+        run_e2e()
+        b.record()
+        torch.cuda.synchronize()
+        ms_e = a.elapsed_time(b)
+        nb = hp_in[0].numel() * 8
+        res["e2e"] = {"value": round(1000.0 * steps / ms_e, 3), "unit": "steps/s", "ms_per_run": round(ms_e, 3),
+                      "steps_per_run": steps, "h2d_bytes_per_step": int(2 * nb / steps),
+                      "d2h_bytes_per_step": int(5 * nb / steps),
+                      "pipeline": f"host psi, c in (pinned) -> forward transforms -> {steps} serial steps -> host "
+                                  f"psi, c, v1..v3 out; per-step divergence flag read back"}
+    return res
 
 
 def run_pfc(ctx, args, n=None, steps=None, warmup=None, e2e=True):

@@ -218,6 +218,16 @@ int pfcs_ch_update(void* c_hat, const void* f_hat, const void* adv_hat, int64_t 
 int pfcs_ch_mu(const void* f_hat, const void* c_hat, void* out, int64_t n0, int64_t n1, int64_t n2,
                const double* kx, const double* ky, const double* kz, double kappa, void* stream);
 int pfcs_add3(const void* a, const void* b, const void* c, void* out, int64_t n, void* stream);
+/* Real-field pointwise operators of the R2C multiphysics path (physical
+ * fields real: 8-byte samples), numpy evaluation order, no FMA; all operand
+ * pointers 16-byte aligned, unused ones may be NULL:
+ *   kind 0  out = (a*a)*a                        psi**3 (hydro.py:86, 96)
+ *   kind 1  out = a*b                            psi * F^-1(i k mu) (hydro.py:98)
+ *   kind 2  out = (a*b + c*d) + e*f              v . grad psi (hydro.py:83-85)
+ *   kind 3  out = alpha*(a*(a*a) - a)            composition nonlinearity
+ *   kind 4  out = (a + b) + c                    sum of the advection products */
+int pfcs_real_pointwise(int kind, const double* a, const double* b, const double* c, const double* d,
+                        const double* e, const double* f, double* out, int64_t n, double alpha, void* stream);
 int pfcs_axpy(const void* a, const void* b, void* out, int64_t n, double w, void* stream);
 
 /* ---- deterministic reductions (pfc._reduce_sum / free_energy,

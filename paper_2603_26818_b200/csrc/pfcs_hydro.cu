@@ -208,6 +208,47 @@ __global__ void k_axpy(const double2* a, const double2* b, double2* out, i64 n, 
 
 using namespace pfcs;
 
+// Real-field pointwise operators of the R2C multiphysics path (physical
+// fields are real there, so every product / nonlinearity reads and writes
+// 8-byte samples; hydro.py:83-86, 100-103 and the composition model).
+// Two samples per thread (16-byte loads); numpy's evaluation order, no FMA.
+enum { RPW_CUBE = 0, RPW_MUL = 1, RPW_ADV3 = 2, RPW_CHNL = 3, RPW_ADD3 = 4 };
+
+__device__ __forceinline__ double rpw_one(int kind, double a, double b, double c, double d, double e, double f,
+                                          double alpha) {
+  switch (kind) {
+    case RPW_CUBE: return __dmul_rn(__dmul_rn(a, a), a);                          // psi**3
+    case RPW_MUL: return __dmul_rn(a, b);                                          // psi * g
+    case RPW_ADV3:                                                                  // v1 x1 + v2 x2 + v3 x3
+      return __dadd_rn(__dadd_rn(__dmul_rn(a, b), __dmul_rn(c, d)), __dmul_rn(e, f));
+    case RPW_CHNL: return __dmul_rn(alpha, __dsub_rn(__dmul_rn(a, __dmul_rn(a, a)), a));  // alpha (c^3 - c)
+    default: return __dadd_rn(__dadd_rn(a, b), c);                                 // (a + b) + c
+  }
+}
+
+__global__ void k_real_pw(int kind, const double* a, const double* b, const double* c, const double* d,
+                          const double* e, const double* f, double* out, i64 n, double alpha) {
+  const i64 n2 = n >> 1;
+  const i64 stride = (i64)gridDim.x * blockDim.x;
+  const bool two = kind == RPW_MUL || kind == RPW_ADV3 || kind == RPW_ADD3;
+  const bool six = kind == RPW_ADV3;
+  for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n2; i += stride) {
+    const double2 x = __ldg((const double2*)a + i);
+    const double2 y = two ? __ldg((const double2*)b + i) : make_double2(0.0, 0.0);
+    const double2 z = two && kind != RPW_MUL ? __ldg((const double2*)c + i) : make_double2(0.0, 0.0);
+    const double2 w = six ? __ldg((const double2*)d + i) : make_double2(0.0, 0.0);
+    const double2 u = six ? __ldg((const double2*)e + i) : make_double2(0.0, 0.0);
+    const double2 v = six ? __ldg((const double2*)f + i) : make_double2(0.0, 0.0);
+    ((double2*)out)[i] = make_double2(rpw_one(kind, x.x, y.x, z.x, w.x, u.x, v.x, alpha),
+                                      rpw_one(kind, x.y, y.y, z.y, w.y, u.y, v.y, alpha));
+  }
+  if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+    const i64 k = n - 1;
+    out[k] = rpw_one(kind, a[k], two ? b[k] : 0.0, (two && kind != RPW_MUL) ? c[k] : 0.0, six ? d[k] : 0.0,
+                     six ? e[k] : 0.0, six ? f[k] : 0.0, alpha);
+  }
+}
+
 extern "C" {
 
 int pfcs_mul_deriv(const void* in, void* out, int64_t n0, int64_t n1, int64_t n2, const double* d,
@@ -309,6 +350,20 @@ int pfcs_ch_mu(const void* f_hat, const void* c_hat, void* out, int64_t n0, int6
   k_ch_mu<<<grid_for(n), 256, 0, (cudaStream_t)stream>>>((const double2*)f_hat, (const double2*)c_hat,
                                                         (double2*)out, n, (int)n1, (int)n2, kx, ky, kz, kappa);
   return check_launch("k_ch_mu");
+}
+
+int pfcs_real_pointwise(int kind, const double* a, const double* b, const double* c, const double* d,
+                        const double* e, const double* f, double* out, int64_t n, double alpha, void* stream) {
+  if (n <= 0) return PFCS_OK;
+  if (kind < RPW_CUBE || kind > RPW_ADD3) return fail(PFCS_E_ARG, "pfcs_real_pointwise: unknown kind");
+  const bool two = kind == RPW_MUL || kind == RPW_ADV3 || kind == RPW_ADD3;
+  if (!a || !out || (two && !b) || ((kind == RPW_ADV3 || kind == RPW_ADD3) && !c) ||
+      (kind == RPW_ADV3 && (!d || !e || !f)))
+    return fail(PFCS_E_ARG, "pfcs_real_pointwise: missing operand");
+  if (((uintptr_t)a | (uintptr_t)b | (uintptr_t)c | (uintptr_t)d | (uintptr_t)e | (uintptr_t)f | (uintptr_t)out) & 15)
+    return fail(PFCS_E_ARG, "pfcs_real_pointwise: operands must be 16-byte aligned");
+  k_real_pw<<<grid_for((n + 1) / 2), 256, 0, (cudaStream_t)stream>>>(kind, a, b, c, d, e, f, out, n, alpha);
+  return check_launch("k_real_pw");
 }
 
 int pfcs_add3(const void* a, const void* b, const void* c, void* out, int64_t n, void* stream) {

@@ -27,6 +27,19 @@ Messages per step (device tensors; NCCL p2p between processes):
   psi 0 -> 1,2,3 (tag 2) | c, c_hat 4 -> 1,2,3 (tags 7, 8; beta != 0) |
   v_i 1+i -> 0, 4 (tags 4,5,6) and -> 5+i (G=8).
 All modes produce bit-identical fields (same kernels, same summation order).
+
+Representations.  Complex full-grid fields (the reference's own
+representation, hydro.py:60-69) take the C2C path below.  Real physical
+fields (psi, c, v_i float64) select the B200 R2C path (`_Real3`): spectra
+are x-halved (n/2+1, n, n) half spectra, every transform is rfft_x / irfft_x
+plus the y and z C2C passes (R + 5S bytes instead of 6C: half the HBM
+traffic), the pointwise products and nonlinearities read and write 8-byte
+real samples (pfcs_real_pointwise), the derivative multipliers stay fused
+into the first pass of the inverse transforms, and the non-finite checks of
+a step are collected in one device flag read back once per step instead of
+one host round trip per spectral update.  The R2C results equal the C2C
+ones to rounding (<= 1e-12, oracle/ref_numpy.py:multi_step) and the serial
+and field-per-GPU R2C modes are bit-identical to each other.
 """
 
 from __future__ import annotations
@@ -215,7 +228,10 @@ def velocity_step(v_hat, psi, axis: int, sym: SymbolTable, params: MultiParams, 
 
 def serial_multi_step(fields: MultiFields, sym: SymbolTable, params: MultiParams) -> MultiFields:
     """All five roles on one GPU: density and composition from the previous
-    velocities, then the velocities from the fresh density (and composition)."""
+    velocities, then the velocities from the fresh density (and composition).
+    Real physical fields take the R2C path (module doc)."""
+    if _is_real(fields.psi):
+        return _serial_multi_step_r(fields, sym, params)
     host = isinstance(fields.psi_hat, np.ndarray)
     ph = _dev(fields.psi_hat)
     vs = [_dev(v) for v in fields.v]
@@ -240,18 +256,20 @@ def serial_multi_step(fields: MultiFields, sym: SymbolTable, params: MultiParams
 def initial_role_state(rank: int, G: int, fields: MultiFields) -> dict:
     """The slice of a MultiFields a rank owns in the G-role map (device)."""
     role = ROLES[G][rank]
-    st = {"step_index": fields.step_index, "role": role}
+    real = _is_real(fields.psi)
+    st = {"step_index": fields.step_index, "role": role, "real": real}
+    phys = _rdev if real else _dev  # physical fields: real (R2C path) or complex (C2C)
     if role == "psi":
-        st.update(psi_hat=_dev(fields.psi_hat), psi=_dev(fields.psi), v=[_dev(v) for v in fields.v])
+        st.update(psi_hat=_dev(fields.psi_hat), psi=phys(fields.psi), v=[phys(v) for v in fields.v])
     elif role == "c":
-        st.update(c_hat=_dev(fields.c_hat), c=_dev(fields.c), v=[_dev(v) for v in fields.v])
+        st.update(c_hat=_dev(fields.c_hat), c=phys(fields.c), v=[phys(v) for v in fields.v])
     elif role.startswith("v"):
         i = int(role[1]) - 1
-        st.update(v_hat=_dev(fields.v_hat[i]), v_own=_dev(fields.v[i]), psi=_dev(fields.psi),
-                  c=_dev(fields.c), c_hat=_dev(fields.c_hat))
+        st.update(v_hat=_dev(fields.v_hat[i]), v_own=phys(fields.v[i]), psi=phys(fields.psi),
+                  c=phys(fields.c), c_hat=_dev(fields.c_hat))
     elif role.startswith("adv"):
         i = int(role[3]) - 1
-        st.update(v_own=_dev(fields.v[i]), psi_hat=_dev(fields.psi_hat))
+        st.update(v_own=phys(fields.v[i]), psi_hat=_dev(fields.psi_hat))
     return st
 
 
@@ -260,6 +278,8 @@ def parallel_multi_step(worker, st: dict, sym: SymbolTable, params: MultiParams)
     G = worker.size
     if G not in (5, 8):
         raise ValueError(f"multiphysics field-per-GPU mode runs on 5 or 8 workers, got {G}")
+    if st.get("real"):
+        return _parallel_multi_step_r(worker, st, sym, params)
     role = ROLES[G][worker.rank]
     idx = st["step_index"]
     beta = params.beta != 0.0
@@ -299,5 +319,260 @@ def parallel_multi_step(worker, st: dict, sym: SymbolTable, params: MultiParams)
         ph = worker.recv_tensor(0, TAG_PSIHAT, torch.empty_like(st["psi_hat"]))
         worker.send_tensor(0, ADV_TAGS[i], _adv_product(ph, i, st["v_own"], sym))
         st["v_own"] = worker.recv_tensor(1 + i, V_TAGS[i], torch.empty_like(ph))
+    st["step_index"] = idx + 1
+    return st
+
+
+# ------------------------------------------------------------ R2C path ------
+
+RPW_CUBE, RPW_MUL, RPW_ADV3, RPW_CHNL, RPW_ADD3 = 0, 1, 2, 3, 4  # pfcs_real_pointwise kinds
+
+
+def _is_real(x) -> bool:
+    if isinstance(x, torch.Tensor):
+        return not x.is_complex()
+    return isinstance(x, np.ndarray) and not np.iscomplexobj(x)
+
+
+def _rdev(x) -> torch.Tensor:
+    """float64 CUDA tensor (contiguous) of a real field."""
+    if isinstance(x, torch.Tensor):
+        t = x if x.is_cuda else x.cuda()
+        return t.to(torch.float64).contiguous()
+    nat.load()
+    return torch.from_numpy(np.ascontiguousarray(np.asarray(x, dtype=np.float64))).to(
+        torch.device("cuda", torch.cuda.current_device()))
+
+
+def _hdev(x) -> torch.Tensor:
+    """complex128 CUDA tensor of a half spectrum."""
+    return _dev(x)
+
+
+class _Real3:
+    """Full-grid 3D R2C / C2R transforms of an (nx, ny, nz) real field with the
+    x axis halved — the layout of the slab pipeline at G = 1 (distfft):
+    forward rfft_x, y, z; inverse z, y, irfft_x; the inverse may fuse the
+    derivative multiplier i d_axis into its first (z) pass."""
+
+    def __init__(self, shape, sym: SymbolTable, device):
+        nx, ny, nz = shape
+        if nx < 4 or nx & (nx - 1):
+            raise ValueError(f"the R2C multiphysics path needs a power-of-two nx >= 4, got {nx}")
+        self.shape = (nx, ny, nz)
+        self.nh = nx // 2 + 1
+        self.hshape = (self.nh, ny, nz)
+        kx, ky, kz, dx, dy, dz = sym.device_vectors(device)
+        self.k = (kx[: self.nh].contiguous(), ky, kz)
+        self.d = (dx[: self.nh].contiguous(), dy, dz)
+
+    @staticmethod
+    def of(shape, sym: SymbolTable, device) -> "_Real3":
+        cache = sym.__dict__.setdefault("_real3", {})
+        key = (tuple(shape), str(device))
+        if key not in cache:
+            cache[key] = _Real3(shape, sym, device)
+        return cache[key]
+
+    def fwd(self, x: torch.Tensor) -> torch.Tensor:
+        nx, ny, nz = self.shape
+        out = torch.empty(self.hshape, dtype=torch.complex128, device=x.device)
+        st = _st()
+        nat.call("pfcs_rfft_x", nat.ptr(x), nat.ptr(out), nx, ny * nz, st)
+        if ny > 1:
+            nat.call("pfcs_fft_axis_c2c", nat.ptr(out), nat.ptr(out), self.nh, ny, nz, 1, 1, st)
+        if nz > 1:
+            nat.call("pfcs_fft_axis_c2c", nat.ptr(out), nat.ptr(out), self.nh, ny, nz, 2, 1, st)
+        return out
+
+    def inv(self, h: torch.Tensor, deriv: int | None = None) -> torch.Tensor:
+        nx, ny, nz = self.shape
+        nh = self.nh
+        st = _st()
+        tmp = torch.empty_like(h)
+        if deriv is not None:  # i d_axis x_hat fused into the z pass
+            nat.call("pfcs_fft_axis_c2c_pro", nat.ptr(h), nat.ptr(tmp), nh, ny, nz, 2, 0, 3,
+                     nat.ptr(self.d[deriv]), deriv, st)
+        else:
+            nat.call("pfcs_fft_axis_c2c", nat.ptr(h), nat.ptr(tmp), nh, ny, nz, 2, 0, st)
+        if ny > 1:
+            nat.call("pfcs_fft_axis_c2c", nat.ptr(tmp), nat.ptr(tmp), nh, ny, nz, 1, 0, st)
+        out = torch.empty(self.shape, dtype=torch.float64, device=h.device)
+        nat.call("pfcs_irfft_x", nat.ptr(tmp), nat.ptr(out), nx, ny * nz, st)
+        return out
+
+
+def _rpw(kind: int, *ops: torch.Tensor, alpha: float = 0.0) -> torch.Tensor:
+    out = torch.empty_like(ops[0])
+    args = [nat.ptr(o) for o in ops] + [None] * (6 - len(ops))
+    nat.call("pfcs_real_pointwise", kind, *args, nat.ptr(out), out.numel(), float(alpha), _st())
+    return out
+
+
+class _StepFlag:
+    """One device diagnostics block shared by a step's spectral updates; the
+    non-finite flag is read back once per step (not once per update)."""
+
+    def __init__(self, device):
+        self.t = torch.zeros(nat.DIAG_SLOTS * nat.DIAG_VALS, dtype=torch.float64, device=device)
+
+    def check(self, step_index: int, *fields: torch.Tensor) -> None:
+        if self.t.view(nat.DIAG_SLOTS, nat.DIAG_VALS)[:, 3].max().item() > 0:
+            for f in fields:
+                if not bool(torch.isfinite(torch.view_as_real(f) if f.is_complex() else f).all()):
+                    _raise_divergence(step_index, f)
+            _raise_divergence(step_index, fields[0])
+
+
+def _grad_dot_r(R: _Real3, x_hat: torch.Tensor, v) -> torch.Tensor:
+    """v . grad x = sum_i v_i F^-1(i d_i x_hat), real (hydro.py:83-85 order)."""
+    g = [R.inv(x_hat, deriv=i) for i in range(3)]
+    return _rpw(RPW_ADV3, v[0], g[0], v[1], g[1], v[2], g[2])
+
+
+def _adv_term_r(R: _Real3, x_hat: torch.Tensor, axis: int, v_axis: torch.Tensor) -> torch.Tensor:
+    """v_axis F^-1(i d_axis x_hat): one advection product (G = 8 helper roles)."""
+    return _rpw(RPW_MUL, v_axis, R.inv(x_hat, deriv=axis))
+
+
+def _density_r(R: _Real3, ph, ps, adv, sym, params: MultiParams, flag: _StepFlag):
+    nh, ny, nz = R.hshape
+    kx, ky, kz = R.k
+    nl_hat = R.fwd(_rpw(RPW_CUBE, ps))
+    adv_hat = R.fwd(adv)
+    new = torch.empty_like(ph)
+    nat.call("pfcs_hydro_psi_update_to", nat.ptr(ph), nat.ptr(new), nat.ptr(nl_hat), nat.ptr(adv_hat), nh, ny, nz,
+             nat.ptr(kx), nat.ptr(ky), nat.ptr(kz), float(sym.eps), float(params.hydro.pfc.dt), nat.ptr(flag.t),
+             _st())
+    return new, R.inv(new)
+
+
+def _composition_r(R: _Real3, ch, cc, v, sym, params: MultiParams, flag: _StepFlag):
+    nh, ny, nz = R.hshape
+    kx, ky, kz = R.k
+    adv_hat = R.fwd(_grad_dot_r(R, ch, v))
+    f_hat = R.fwd(_rpw(RPW_CHNL, cc, alpha=params.alpha))
+    new = torch.empty_like(ch)
+    nat.call("pfcs_ch_update_to", nat.ptr(ch), nat.ptr(new), nat.ptr(f_hat), nat.ptr(adv_hat), nh, ny, nz, nat.ptr(kx),
+             nat.ptr(ky), nat.ptr(kz), float(params.mobility), float(params.kappa), float(params.hydro.pfc.dt),
+             nat.ptr(flag.t), _st())
+    return new, R.inv(new)
+
+
+def _density_mu_r(R: _Real3, ps, sym) -> torch.Tensor:
+    nh, ny, nz = R.hshape
+    kx, ky, kz = R.k
+    nl_hat = R.fwd(_rpw(RPW_CUBE, ps))
+    f_hat = R.fwd(ps)
+    mu = torch.empty_like(nl_hat)
+    nat.call("pfcs_hydro_mu", nat.ptr(nl_hat), nat.ptr(f_hat), nat.ptr(mu), nh, ny, nz, nat.ptr(kx), nat.ptr(ky),
+             nat.ptr(kz), float(sym.eps), _st())
+    return mu
+
+
+def _composition_mu_r(R: _Real3, cc, ch, params: MultiParams) -> torch.Tensor:
+    nh, ny, nz = R.hshape
+    kx, ky, kz = R.k
+    fc_hat = R.fwd(_rpw(RPW_CHNL, cc, alpha=params.alpha))
+    muc = torch.empty_like(fc_hat)
+    nat.call("pfcs_ch_mu", nat.ptr(fc_hat), nat.ptr(ch), nat.ptr(muc), nh, ny, nz, nat.ptr(kx), nat.ptr(ky),
+             nat.ptr(kz), float(params.kappa), _st())
+    return muc
+
+
+def _velocity_r(R: _Real3, vh, ps, axis: int, mu_hat, sym, params: MultiParams, flag: _StepFlag, cc=None,
+                muc=None):
+    nh, ny, nz = R.hshape
+    kx, ky, kz = R.k
+    force = R.fwd(_rpw(RPW_MUL, ps, R.inv(mu_hat, deriv=axis)))  # F(psi F^-1(i k mu_hat))
+    if params.beta != 0.0:
+        force_c = R.fwd(_rpw(RPW_MUL, cc, R.inv(muc, deriv=axis)))
+        total = torch.empty_like(force)
+        nat.call("pfcs_axpy", nat.ptr(force), nat.ptr(force_c), nat.ptr(total), total.numel(), float(params.beta),
+                 _st())
+        force = total
+    hp = params.hydro
+    dt, rho = float(hp.pfc.dt), float(hp.rho)
+    new = torch.empty_like(vh)
+    nat.call("pfcs_hydro_vel_update_to", nat.ptr(vh), nat.ptr(new), nat.ptr(force), nh, ny, nz, nat.ptr(kx),
+             nat.ptr(ky), nat.ptr(kz), dt / rho, (dt / rho) * float(hp.gamma), -0.5 * float(sym.a0) ** 2,
+             nat.ptr(flag.t), _st())
+    return new, R.inv(new)
+
+
+def _serial_multi_step_r(fields: MultiFields, sym: SymbolTable, params: MultiParams) -> MultiFields:
+    host = isinstance(fields.psi, np.ndarray)
+    ps = _rdev(fields.psi)
+    R = _Real3.of(ps.shape, sym, ps.device)
+    flag = _StepFlag(ps.device)
+    ph, ch, cc = _hdev(fields.psi_hat), _hdev(fields.c_hat), _rdev(fields.c)
+    vs = [_rdev(v) for v in fields.v]
+    psi_hat, psi = _density_r(R, ph, ps, _grad_dot_r(R, ph, vs), sym, params, flag)
+    c_hat, c = _composition_r(R, ch, cc, vs, sym, params, flag)
+    mu_hat = _density_mu_r(R, psi, sym)
+    muc = _composition_mu_r(R, c, c_hat, params) if params.beta != 0.0 else None
+    out = [_velocity_r(R, _hdev(fields.v_hat[i]), psi, i, mu_hat, sym, params, flag, c, muc) for i in range(3)]
+    flag.check(fields.step_index, psi_hat, c_hat, *(o[0] for o in out))
+    for i in range(3):
+        fields.v_hat[i], fields.v[i] = _out(out[i][0], host), _out(out[i][1], host)
+    fields.psi_hat, fields.psi = _out(psi_hat, host), _out(psi, host)
+    fields.c_hat, fields.c = _out(c_hat, host), _out(c, host)
+    fields.step_index += 1
+    fields.sim_time += params.hydro.pfc.dt
+    return fields
+
+
+def _parallel_multi_step_r(worker, st: dict, sym: SymbolTable, params: MultiParams) -> dict:
+    """The G = 5 / 8 dataflow of parallel_multi_step on real fields: the
+    messages are real physical fields (8 bytes per point) and half spectra."""
+    G = worker.size
+    role = ROLES[G][worker.rank]
+    idx = st["step_index"]
+    beta = params.beta != 0.0
+    like = st.get("psi") if st.get("psi") is not None else st.get("c", st.get("v_own"))
+    R = _Real3.of(tuple(like.shape), sym, like.device)
+    flag = _StepFlag(like.device)
+    if role == "psi":
+        ph = st["psi_hat"]
+        if G == 8:
+            for h in (5, 6, 7):
+                worker.send_tensor(h, TAG_PSIHAT, ph)
+            p = [worker.recv_tensor(5 + i, ADV_TAGS[i], torch.empty_like(st["psi"])) for i in range(3)]
+            adv = _rpw(RPW_ADD3, *p)
+        else:
+            adv = _grad_dot_r(R, ph, st["v"])
+        st["psi_hat"], st["psi"] = _density_r(R, ph, st["psi"], adv, sym, params, flag)
+        flag.check(idx, st["psi_hat"])
+        for dst in (1, 2, 3):
+            worker.send_tensor(dst, TAG_PSI, st["psi"])
+        st["v"] = [worker.recv_tensor(1 + i, V_TAGS[i], torch.empty_like(st["psi"])) for i in range(3)]
+    elif role == "c":
+        st["c_hat"], st["c"] = _composition_r(R, st["c_hat"], st["c"], st["v"], sym, params, flag)
+        flag.check(idx, st["c_hat"])
+        if beta:
+            for dst in (1, 2, 3):
+                worker.send_tensor(dst, TAG_C, st["c"])
+                worker.send_tensor(dst, TAG_CHAT, st["c_hat"])
+        st["v"] = [worker.recv_tensor(1 + i, V_TAGS[i], torch.empty_like(st["c"])) for i in range(3)]
+    elif role.startswith("v"):
+        i = int(role[1]) - 1
+        psi = worker.recv_tensor(0, TAG_PSI, torch.empty_like(st["psi"]))
+        st["psi"] = psi
+        muc = None
+        if beta:
+            st["c"] = worker.recv_tensor(4, TAG_C, torch.empty_like(st["c"]))
+            st["c_hat"] = worker.recv_tensor(4, TAG_CHAT, torch.empty_like(st["c_hat"]))
+            muc = _composition_mu_r(R, st["c"], st["c_hat"], params)
+        mu_hat = _density_mu_r(R, psi, sym)
+        st["v_hat"], st["v_own"] = _velocity_r(R, st["v_hat"], psi, i, mu_hat, sym, params, flag, st.get("c"), muc)
+        flag.check(idx, st["v_hat"])
+        dsts = (0, 4) + ((5 + i,) if G == 8 else ())
+        for dst in dsts:
+            worker.send_tensor(dst, V_TAGS[i], st["v_own"])
+    else:  # advection helper (G = 8)
+        i = int(role[3]) - 1
+        ph = worker.recv_tensor(0, TAG_PSIHAT, torch.empty_like(st["psi_hat"]))
+        worker.send_tensor(0, ADV_TAGS[i], _adv_term_r(R, ph, i, st["v_own"]))
+        st["v_own"] = worker.recv_tensor(1 + i, V_TAGS[i], torch.empty_like(st["v_own"]))
     st["step_index"] = idx + 1
     return st

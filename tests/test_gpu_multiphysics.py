@@ -115,3 +115,106 @@ def test_field_per_gpu_equals_serial_bitwise(pkg, G, beta):
             np.testing.assert_array_equal(val, ref.v[int(role[1]) - 1])
         else:  # adv helpers keep the latest v_i
             np.testing.assert_array_equal(val, ref.v[int(role[3]) - 1])
+
+
+# ---------------------------------------------------------------- R2C path --
+
+def to_real(f):
+    """The same state as real physical fields + x-halved half spectra (the
+    B200 R2C representation of multiphysics.py)."""
+    from paper_2603_26818_b200.multiphysics import MultiFields
+
+    def half(x):
+        return np.fft.rfftn(np.real(x), axes=(1, 2, 0))
+
+    return MultiFields(psi_hat=half(f.psi), psi=np.real(f.psi).copy(), c_hat=half(f.c), c=np.real(f.c).copy(),
+                       v_hat=[half(x) for x in f.v], v=[np.real(x).copy() for x in f.v])
+
+
+@pytest.mark.parametrize("beta", [0.0, 0.5])
+def test_r2c_serial_vs_oracle(pkg, beta):
+    """R2C path (real fields, half spectra) vs the complex oracle restatement:
+    same tolerances as the C2C path."""
+    import ref_numpy as ora
+    from paper_2603_26818_b200.multiphysics import serial_multi_step
+
+    grid, sym, mp, f = setup(pkg, beta=beta)
+    o = {"psi_hat": f.psi_hat.copy(), "psi": f.psi.copy(), "c_hat": f.c_hat.copy(), "c": f.c.copy(),
+         "v_hat": [x.copy() for x in f.v_hat], "v": [x.copy() for x in f.v]}
+    r = to_real(f)
+    osym = ora.symbols(grid.n, grid.length, EPS, a0=2.0)
+    for _ in range(8):
+        serial_multi_step(r, sym, mp)
+        ora.multi_step(o, osym, 0.1, 1.0, 1.0, 0.7, 0.5, 1.0, beta)
+    assert r.psi.dtype == np.float64 and r.psi_hat.shape == (9, 16, 16)
+    assert rel_inf(r.psi, o["psi"].real) <= 1e-12
+    assert rel_inf(r.c, o["c"].real) <= 1e-12
+    for i in range(3):
+        assert rel_inf(r.v[i], o["v"][i].real) <= 1e-9
+    assert rel_inf(r.psi_hat, o["psi_hat"][:9]) <= 1e-12
+
+
+def test_r2c_device_fields_and_c2c_agree(pkg):
+    """Device-resident R2C fields (the hot path) vs the C2C path, 6 steps."""
+    import torch
+    from paper_2603_26818_b200.multiphysics import MultiFields, serial_multi_step
+
+    grid, sym, mp, f = setup(pkg, n=32)
+    r = to_real(f)
+    d = MultiFields(psi_hat=torch.from_numpy(r.psi_hat).cuda(), psi=torch.from_numpy(r.psi).cuda(),
+                    c_hat=torch.from_numpy(r.c_hat).cuda(), c=torch.from_numpy(r.c).cuda(),
+                    v_hat=[torch.from_numpy(x).cuda() for x in r.v_hat], v=[torch.from_numpy(x).cuda() for x in r.v])
+    for _ in range(6):
+        serial_multi_step(d, sym, mp)
+        serial_multi_step(f, sym, mp)
+    assert d.psi.dtype == torch.float64 and d.psi.is_cuda
+    assert rel_inf(d.psi.cpu().numpy(), f.psi.real) <= 1e-12
+    assert rel_inf(d.c.cpu().numpy(), f.c.real) <= 1e-12
+    for i in range(3):
+        assert rel_inf(d.v[i].cpu().numpy(), f.v[i].real) <= 1e-9
+
+
+@pytest.mark.parametrize("G", [5, 8])
+@pytest.mark.parametrize("beta", [0.0, 0.5])
+def test_r2c_field_per_gpu_equals_serial_bitwise(pkg, G, beta):
+    from paper_2603_26818_b200.multiphysics import (ROLES, initial_role_state, parallel_multi_step,
+                                                    serial_multi_step)
+
+    grid, sym, mp, f0 = setup(pkg, beta=beta)
+    f = to_real(f0)
+    ref = to_real(f0)
+    for _ in range(4):
+        serial_multi_step(ref, sym, mp)
+
+    def body(w):
+        st = initial_role_state(w.rank, G, f)
+        for _ in range(4):
+            parallel_multi_step(w, st, sym, mp)
+        role = ROLES[G][w.rank]
+        key = {"psi": "psi", "c": "c"}.get(role, "v_own")
+        return role, st[key].cpu().numpy()
+
+    for role, val in pkg.spawn_group(G, body):
+        assert val.dtype == np.float64
+        if role == "psi":
+            np.testing.assert_array_equal(val, ref.psi)
+        elif role == "c":
+            np.testing.assert_array_equal(val, ref.c)
+        elif role.startswith("v"):
+            np.testing.assert_array_equal(val, ref.v[int(role[1]) - 1])
+        else:
+            np.testing.assert_array_equal(val, ref.v[int(role[3]) - 1])
+
+
+def test_r2c_divergence_raises(pkg):
+    """A non-finite update raises DivergenceError at the step it happens
+    (checked once per step on the R2C path)."""
+    from paper_2603_26818_b200.multiphysics import serial_multi_step
+    from paper_2603_26818_b200.pfc import DivergenceError
+
+    grid, sym, mp, f = setup(pkg)
+    r = to_real(f)
+    r.psi = r.psi.copy()
+    r.psi[3, 4, 5] = np.inf
+    with pytest.raises(DivergenceError):
+        serial_multi_step(r, sym, mp)
