@@ -14,9 +14,9 @@ their mapping:
   corresponding buffer.  Thread groups share the address space (peer access
   is enabled between distinct devices); process groups exchange CUDA IPC
   handles over torch.distributed and open them (lazy peer enable);
-* `fence(worker)` — the ordering point of a fused exchange: the local
-  stream is drained, then all ranks meet (writers done before readers read,
-  readers done before the next writes).
+* `fence(worker)` — the ordering point of a fused exchange (writers done
+  before readers read, readers done before the next writes): device-side
+  event waits between thread ranks, drain + barrier between processes.
 """
 
 from __future__ import annotations
@@ -100,9 +100,34 @@ def map_peers(worker, buf: DeviceBuffer) -> PeerMap:
 
 
 def fence(worker) -> None:
-    """Drain the local stream, then meet every rank."""
-    nat.check(nat.load().pfcs_stream_sync(ctypes.c_void_p(nat.stream_ptr())), "pfcs_stream_sync")
-    worker.barrier()
+    """Order a fused exchange: every rank's work issued so far (its stores
+    into the peers' receive buffers, its reads of its own) completes before
+    any rank's subsequent work does.
+
+    Thread groups (one process, a GPU per thread: spawn_group) order it on
+    the devices: each rank records an event on its stream, the ranks meet on
+    the host — without draining anything — and every stream waits for its
+    peers' events, so the GPUs never idle at a transpose and the host runs
+    ahead.  Two events per rank, alternating: a rank cannot re-record an
+    event before every peer has issued its wait on it (that needs the next
+    fence's meeting).  Process groups drain the local stream and meet
+    (dist.barrier), as CUDA IPC events would need a host barrier that does
+    not synchronise the device."""
+    if hasattr(worker, "_dist"):
+        nat.check(nat.load().pfcs_stream_sync(ctypes.c_void_p(nat.stream_ptr())), "pfcs_stream_sync")
+        worker.barrier()
+        return
+    st = worker.__dict__.get("_pfcs_fence")
+    if st is None:
+        st = worker.__dict__.setdefault("_pfcs_fence", {"k": 0, "ev": (torch.cuda.Event(), torch.cuda.Event())})
+    ev = st["ev"][st["k"] & 1]
+    st["k"] += 1
+    stream = torch.cuda.current_stream()
+    ev.record(stream)
+    events = worker.all_to_all([ev] * worker.size)
+    for h, e in enumerate(events):
+        if h != worker.rank:
+            stream.wait_event(e)
 
 
 class Table:
