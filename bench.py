@@ -638,6 +638,56 @@ def run_pfc(ctx, args, n=None, steps=None, warmup=None, e2e=True):
     return res
 
 
+def run_pfc_pencil(ctx, args, n: int, steps: int, warmup: int = 2) -> dict:
+    """configs[3]: 3D PFC on a pr x pc pencil grid (PencilGrid.for_workers(G):
+    2 x 4 at G = 8) — x-pencil physical field, z-pencil half spectrum, row
+    and column all-to-alls (pencil.py), same timing rules as run_pfc."""
+    import torch
+
+    from paper_2603_26818_b200 import distfft, pfc
+    from paper_2603_26818_b200.grid import GridSpec, make_symbols
+    from paper_2603_26818_b200.pencil import PencilGeometry, PencilGrid, PencilLayout
+
+    pg = PencilGrid.for_workers(ctx.world)
+    w = ctx.worker()
+    grid = GridSpec((n, n, n), pfc.default_domain_length((n, n, n)))
+    g = PencilGeometry(grid, pg, ctx.rank, True)
+    gen = torch.Generator(device=ctx.device).manual_seed(17 + ctx.rank)
+    x = torch.rand((n, g.cy, g.cz), dtype=torch.float64, device=ctx.device, generator=gen)
+    x.mul_(0.02).add_(-0.31)
+    f0 = distfft.DistField(grid, PencilLayout(pg, "x"), distfft.Space.PHYSICAL, x)
+    st = pfc.PfcState(psi_hat=distfft.forward(f0, w), grid=grid, symbols=make_symbols(grid, -0.3), worker=w)
+    del f0, x
+    params = pfc.PfcParams()
+    for _ in range(max(1, warmup)):
+        pfc.pfc_run(st, params, 1)
+    torch.cuda.synchronize()
+    ctx.barrier()
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    a.record()
+    pfc.pfc_run(st, params, steps)
+    b.record()
+    torch.cuda.synchronize()
+    ctx.barrier()
+    ms = ctx.max_over_ranks(a.elapsed_time(b) / steps)
+    hbm, _ = peaks()
+    res = {"metric": "PFC time-steps/sec", "value": round(1000.0 / ms, 3), "unit": "steps/s",
+           "ms_per_step": round(ms, 4), "steps": steps,
+           "config": f"3D PFC {n}^3 fp64 R2C pencil {pg.pr}x{pg.pc} (configs[3] decomposition)",
+           "alg_hbm_bytes_per_step": pfc_bytes(n) / ctx.world}
+    # each rank moves its half-spectrum share twice through the row and twice
+    # through the column all-to-all per step
+    S = spec_bytes(n)
+    nv = 2 * S / ctx.world * ((pg.pr - 1) / pg.pr + (pg.pc - 1) / pg.pc)
+    t_hbm = pfc_bytes(n) / (ctx.world * hbm * 1e9)
+    t_nvl = nv / (NVLINK_GBS * 1e9)
+    res["roofline_combined"] = {"t_roof_ms": round(1e3 * (t_hbm + t_nvl), 4), "t_hbm_ms": round(1e3 * t_hbm, 4),
+                                "t_nvlink_ms": round(1e3 * t_nvl, 4), "nvlink_bytes_per_gpu": nv,
+                                "frac": round((t_hbm + t_nvl) / (ms * 1e-3), 4)}
+    return res
+
+
 # ------------------------------------------------------------ CPU baseline --
 # The reference's CPU path, timed on this box's host cores.  Preferred: the
 # UNMODIFIED reference package staged by oracle/vendor_reference.py under
@@ -907,6 +957,8 @@ def run_exchange(ctx, args) -> dict:
 
     from paper_2603_26818_b200.grid import slab_layout
 
+    if ctx.dist.get_backend() != "nccl":
+        return {"skipped": "NCCL all-to-all microbenchmark needs the nccl backend (gloo smoke run)"}
     n, G = args.pfc_n, ctx.world
     nxm = n // 2 + 1
     xl, zl = slab_layout(nxm, G), slab_layout(n, G)
@@ -964,6 +1016,13 @@ def main():
                 pfc_big = {"error": f"{type(exc).__name__}: {str(exc)[:200]}"}
             torch.cuda.empty_cache()
             pfc_res = pfc_res_keep
+        pencil = None
+        if not args.no_pfc and ctx.world >= 4:
+            import torch
+
+            torch.cuda.empty_cache()
+            pencil = _guard(lambda: run_pfc_pencil(ctx, args, args.pfc_big_n, max(3, args.steps // 4)))
+            torch.cuda.empty_cache()
         pfc2d = None if args.no_pfc else run_pfc2d(ctx, args)
         multi = None if args.no_multi else run_multi(ctx, args)
         exch = run_exchange(ctx, args) if ctx.world > 1 and not args.no_pfc else None
@@ -985,6 +1044,8 @@ def main():
             pfc_big["roofline_step_frac"] = round(t_roof / (pfc_big["ms_per_step"] * 1e-3), 4)
             pfc_big["config"] += " (configs[3] grid; slab decomposition)" if args.pfc_big_n == 2048 else ""
         out["pfc2048"] = pfc_big
+    if pencil is not None:
+        out["pfc_pencil"] = pencil
     if pfc2d is not None:
         out["pfc2d"] = pfc2d
     if multi is not None:
