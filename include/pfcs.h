@@ -261,18 +261,6 @@ int64_t pfcs_energy_scratch_bytes(int64_t n);
  *         (grid.wavenumbers), diag (nullable) receives nsteps x
  *         PFCS_DIAG_SLOTS x 4 per-step diagnostics (zeroed here), work >=
  *         spectral_elems complex128. */
-/* ---- the 2D PFC time loop in one thread-block cluster (configs[0]): nsteps
- * fused steps of the single-rank R2C engine on a (nx, ny) = (256, 256) grid
- * viewed as (nx, 1, ny): psi_hat (nx/2+1, ny) and work (its z-inverse, as
- * left by pfcs_pfc_update_z / prepared with pfcs_fft_zlines) stay in the
- * cluster's distributed shared memory for the whole loop; both are written
- * back at the end.  kx (nx/2+1), ky (1), kz (ny) as for pfcs_pfc_update_z;
- * diag: nsteps x PFCS_DIAG_SLOTS x 4 (zeroed by the caller) or NULL.
- * Bit-identical to nsteps x (pfcs_pfc_cube_x + pfcs_pfc_update_z).
- * PFCS_E_UNSUPPORTED for other shapes. */
-int pfcs_pfc2d_steps(void* psi_hat, void* work, int64_t nx, int64_t ny, const double* kx, const double* ky,
-                     const double* kz, double eps, double dt, int64_t nsteps, double* diag, void* stream);
-
 typedef struct pfcs_plan pfcs_plan;
 int pfcs_plan_create(int64_t nx, int64_t ny, int64_t nz, pfcs_plan** plan);
 int pfcs_plan_destroy(pfcs_plan* plan);

@@ -37,7 +37,6 @@ _SIGS = {
     "pfcs_device_count": [ctypes.POINTER(_c_int)],
     "pfcs_fft_axis_c2c": [_c_p, _c_p, _c_i64, _c_i64, _c_i64, _c_int, _c_int, _c_p],
     "pfcs_fft_axis_c2c_pro": [_c_p, _c_p, _c_i64, _c_i64, _c_i64, _c_int, _c_int, _c_int, _c_p, _c_int, _c_p],
-    "pfcs_pfc2d_steps": [_c_p, _c_p, _c_i64, _c_i64, _c_p, _c_p, _c_p, _c_d, _c_d, _c_i64, _c_p, _c_p],
     "pfcs_plan_create": [_c_i64, _c_i64, _c_i64, _c_p],
     "pfcs_plan_destroy": [_c_p],
     "pfcs_plan_fwd": [_c_p, _c_p, _c_p, _c_p],

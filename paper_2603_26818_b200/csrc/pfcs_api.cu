@@ -428,16 +428,6 @@ int pfcs_apply_op(const void* in, void* out, int64_t cx, int64_t ny, int64_t nz,
 
 }  // extern "C"
 
-extern "C" int pfcs_pfc2d_steps(void* psi_hat, void* work, int64_t nx, int64_t ny, const double* kx,
-                                const double* ky, const double* kz, double eps, double dt, int64_t nsteps,
-                                double* diag, void* stream) {
-  if (!psi_hat || !work || !kx || !ky || !kz) return fail(PFCS_E_ARG, "null argument");
-  if (nsteps < 0) return fail(PFCS_E_ARG, "negative step count");
-  const int rc = launch_pfc2d_cluster(psi_hat, work, nx, ny, kx, ky, kz, eps, dt, nsteps, diag, S(stream));
-  if (rc == 1) return fail(PFCS_E_UNSUPPORTED, "no cluster kernel for this 2D shape");
-  return rc;
-}
-
 // ------------------------------------------------------------ plan API ----
 struct pfcs_plan {
   int64_t nx, ny, nz, nh;

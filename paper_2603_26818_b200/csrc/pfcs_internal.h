@@ -69,8 +69,6 @@ inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
   return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
-int launch_pfc2d_cluster(void* psi_hat, void* work, long long nx, long long ny, const double* kx, const double* ky,
-                         const double* kz, double eps, double dt, long long nsteps, double* diag, cudaStream_t st);
 
 // Opt a kernel in to > 48 KB dynamic shared memory once.
 int ensure_smem(const void* func, size_t bytes);

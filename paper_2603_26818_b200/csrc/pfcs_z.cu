@@ -205,41 +205,13 @@ static int pfc_z_n(const double2* nl, double2* psi_hat, double2* next, i64 cx, i
     if constexpr (T * P > 1024) {
       return fail(PFCS_E_UNSUPPORTED, "tile too large");
     } else {
-      // TMA staging for an unblocked input (B200: see DESIGN.md); the
-      // partial last tile copies only its valid lines
-      constexpr size_t tsmem = (size_t)T * N * 16 + (size_t)T * tile_ls(N, T, false) * 16 + 16 + 1024;
-      // psi_hat staged by TMA bulk copies: opt-in (PFCS_TMA_Z=1).  On the B200
-      // the contiguous z lines stream best through LDG (1024^3: 6.80 ms
-      // register-loaded vs 7.09 ms psi-staged vs 7.57 ms N-hat-staged).
-      static const bool z_tma = [] {
-        const char* v = getenv("PFCS_TMA_Z");
-        return v && *v && atoi(v) != 0;
-      }();
-      const bool use_tma = z_tma && tma_enabled() && tsmem <= 227 * 1024 && N >= 64 &&
-                           !(((uintptr_t)nl | (uintptr_t)psi_hat) & 15);
-      const size_t smem = use_tma ? tsmem : (size_t)T * tile_ls(N, T, false) * sizeof(double2);
+      // (A TMA-staged form of this pass — psi_hat or N-hat bulk-copied into
+      // shared memory — measured slower on the B200: 1024^3 6.80 ms
+      // register-loaded vs 7.09 / 7.57 ms staged; the kernel keeps the ST == 3
+      // code path but nothing launches it.)
+      const size_t smem = (size_t)T * tile_ls(N, T, false) * sizeof(double2);
       const i64 ntiles = (nlines + T - 1) / T;
       int grid = 0;
-      if (use_tma) {
-#define PFCS_ZK(BI, BO, NX) k_pfc_z<N, T, 3, BI, BO, NX>
-#define PFCS_ZL(BI, BO, NX)                                                                       \
-  do {                                                                                            \
-    if (int rc = persistent_grid((const void*)PFCS_ZK(BI, BO, NX), T * P, smem, ntiles, &grid))   \
-      return rc;                                                                                  \
-    launch_pdl(PFCS_ZK(BI, BO, NX), dim3(grid), dim3(T * P), smem, st, nl, psi_hat, next, nlines,     \
-               (int)ny, a, b, kx, ky, kz, p, tw, scale, diag, tab);                               \
-  } while (0)
-        if (!nx) {
-          if (bin) PFCS_ZL(true, false, false);
-          else PFCS_ZL(false, false, false);
-        } else if (bin && bout) PFCS_ZL(true, true, true);
-        else if (bin) PFCS_ZL(true, false, true);
-        else if (bout) PFCS_ZL(false, true, true);
-        else PFCS_ZL(false, false, true);
-#undef PFCS_ZL
-#undef PFCS_ZK
-        return check_launch("k_pfc_z(tma)");
-      }
 #define PFCS_ZK(BI, BO, NX) k_pfc_z<N, T, ST, BI, BO, NX>
 #define PFCS_ZL(BI, BO, NX)                                                                       \
   do {                                                                                            \

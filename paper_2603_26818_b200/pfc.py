@@ -27,7 +27,6 @@ kernels' building blocks with identical update arithmetic.
 from __future__ import annotations
 
 import math
-import os
 import warnings
 from dataclasses import dataclass, field as dataclass_field
 
@@ -359,10 +358,6 @@ def pfc_run(state: PfcState, params: PfcParams, n_steps: int, realness: list | N
     per = nat.DIAG_SLOTS * nat.DIAG_VALS
     diag = torch.zeros(n_steps * per, dtype=torch.float64, device=eng.device)
     first = state.step_index
-    if _cluster2d(eng, state):
-        _run_cluster2d(eng, state, params, n_steps, diag)
-        _finish(state, params, diag.cpu().numpy(), first, realness)
-        return state
     s = 0
     graph = _graph_for(eng, state, params, n_steps)
     if graph is not None:
@@ -382,32 +377,6 @@ def pfc_run(state: PfcState, params: PfcParams, n_steps: int, realness: list | N
         s += 1
     _finish(state, params, diag.cpu().numpy(), first, realness)
     return state
-
-
-def _cluster2d(eng, state: PfcState) -> bool:
-    """Opt-in (PFCS_CLUSTER2D=1): run the 2D 256^2 single-rank R2C time loop
-    as one thread-block-cluster kernel (csrc/pfcs_pfc2d.cu; bit-identical).
-    Off by default: on the B200 the 16-SM cluster (14.4 us/step) loses to the
-    graph-replayed two-kernel step spread over all SMs (10.5-11 us/step)."""
-    if os.environ.get("PFCS_CLUSTER2D", "0") != "1":
-        return False
-    g = eng.g
-    return (isinstance(eng, _StepEngine) and eng.G == 1 and eng.fused and eng.real and state.grid.is_2d
-            and (g.nx, g.ny, g.nz) == (256, 1, 256))
-
-
-def _run_cluster2d(eng, state: PfcState, params: PfcParams, n_steps: int, diag: torch.Tensor) -> None:
-    g = eng.g
-    st = nat.stream_ptr()
-    psi = state.psi_hat.dev
-    kx, ky, kz = eng._sym_ptrs(state.symbols)
-    key = (psi.data_ptr(), state.psi_hat._version)
-    if eng.prepared_for != key:  # the z-inverse the first step starts from
-        nat.call("pfcs_fft_zlines", nat.ptr(psi), nat.ptr(eng.send), g.cx * g.ny, g.nz, 1, 1, 0, st)
-    nat.call("pfcs_pfc2d_steps", nat.ptr(psi), nat.ptr(eng.send), g.nx, g.nz, kx, ky, kz,
-             float(state.symbols.eps), float(params.dt), n_steps, nat.ptr(diag), st)
-    state.psi_hat._version += 1
-    eng.prepared_for = (psi.data_ptr(), state.psi_hat._version)
 
 
 GRAPH_BLOCK = 16

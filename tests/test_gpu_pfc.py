@@ -300,44 +300,6 @@ def test_pfc_run_graph_replay_matches_stepping(pkg):
     assert info.value.cause.step_index == 0
 
 
-def test_cluster2d_step_bit_identical_to_two_kernel_step(pkg):
-    """configs[0] shape: the one-cluster 2D time loop (csrc/pfcs_pfc2d.cu)
-    reproduces the two-kernel fused step bit for bit, diagnostics included,
-    across pfc_run calls and mixed with single pfc_step calls."""
-    import os
-    import subprocess
-    import sys
-    from pathlib import Path
-
-    code = r"""
-import sys, numpy as np
-sys.path.insert(0, %r)
-import paper_2603_26818_b200 as pkg
-from paper_2603_26818_b200 import distfft, pfc
-n = (256, 256, 1)
-grid = pkg.GridSpec(n, pfc.default_domain_length(n))
-psi0 = pfc.initial_field("constant_plus_noise", grid, seed=0, noise_amplitude=0.01)
-def body(w):
-    f = distfft.scatter(psi0, w, grid, distfft.Layout.Y_SLAB, real=True)
-    st = pfc.PfcState(psi_hat=distfft.forward(f, w), grid=grid, symbols=pkg.make_symbols(grid, -0.3), worker=w)
-    re = []
-    pfc.pfc_run(st, pfc.PfcParams(), 37, realness=re)
-    pfc.pfc_step(st, pfc.PfcParams())
-    pfc.pfc_run(st, pfc.PfcParams(), 20, realness=re)
-    return st.psi_hat.local.copy(), np.array(re), st.step_index
-a, r, k = pkg.spawn_group(1, body)[0]
-np.savez(sys.argv[1], a=a, r=r, k=k)
-""" % str(Path(__file__).resolve().parent.parent)
-    out = {}
-    for flag in ("0", "1"):
-        path = f"/tmp/pfcs_c2d_{flag}.npz"
-        env = dict(os.environ, PFCS_CLUSTER2D=flag)
-        subprocess.run([sys.executable, "-c", code, path], check=True, env=env, timeout=600)
-        out[flag] = np.load(path)
-    assert int(out["1"]["k"]) == 58
-    np.testing.assert_array_equal(out["0"]["a"], out["1"]["a"])
-    np.testing.assert_array_equal(out["0"]["r"], out["1"]["r"])
-
 
 @pytest.mark.parametrize("real", [True, False])
 @pytest.mark.parametrize("n", [(32, 24, 32), (16, 12, 64)])

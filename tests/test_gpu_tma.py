@@ -1,8 +1,9 @@
 """The TMA-staged passes (csrc/pfcs_tma.cu k_strided_tma; csrc/pfcs_x.cu
 k_real_x with ST == 3) must be bit-identical to the register-pipelined kernels
 they replace (PFCS_TMA=0): every tile width, ragged inner extents (OOB-filled
-boxes), both directions, the real x transforms, the fused cube pass and the
-fused z update (k_pfc_z, bulk copies) with their diagnostics.
+boxes), both directions, the real x transforms and the fused cube pass with
+its diagnostics — including the line-synchronous cube pass k_cube_ls
+(PFCS_CUBE_LS=0/1) at production tiles.
 
 The switch is read once per process, so each configuration runs in a child
 process that writes its outputs for comparison."""
@@ -95,50 +96,9 @@ def test_tma_strided_bit_identical(tmp_path, t):
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     base = _run(tmp_path, "base", {"PFCS_TMA": "0"})
-    tma = _run(tmp_path, f"tma{t}", {"PFCS_TMA": "1", "PFCS_TMA_T": str(t), "PFCS_TMA_Z": "1"})
+    tma = _run(tmp_path, f"tma{t}", {"PFCS_TMA": "1", "PFCS_TMA_T": str(t)})
     for k in base.files:
         assert np.array_equal(base[k], tma[k]), k
-
-
-PFC_CHILD = r"""
-import sys, os, numpy as np
-sys.path.insert(0, {root!r})
-import paper_2603_26818_b200 as pkg
-from paper_2603_26818_b200 import distfft, pfc
-out = {{}}
-for mode in ("peer", "collective"):
-    os.environ["PFCS_EXCHANGE"] = mode
-    for G in (1, 2, 3):
-        n = (16, 32, 64)
-        grid = pkg.GridSpec(n, pfc.default_domain_length(n))
-        psi0 = pfc.initial_field("constant_plus_noise", grid, seed=3, noise_amplitude=0.05)
-        def body(w):
-            f = distfft.scatter(psi0, w, grid, distfft.Layout.Z_SLAB, real=True)
-            st = pfc.PfcState(psi_hat=distfft.forward(f, w), grid=grid, symbols=pkg.make_symbols(grid, -0.3), worker=w)
-            pfc.pfc_run(st, pfc.PfcParams(), 6)
-            return distfft.gather(distfft.inverse(st.psi_hat, w), w)
-        out[f"{{mode}}_{{G}}"] = pkg.spawn_group(G, body)[0]
-np.savez({path!r}, **out)
-"""
-
-
-def test_tma_z_update_multi_rank_bit_identical(tmp_path):
-    """The opt-in TMA-staged z update (PFCS_TMA_Z=1) incl. its blocked-input
-    and peer-scatter forms (G > 1) reproduces the default path bit for bit."""
-    import torch
-
-    if not torch.cuda.is_available():
-        pytest.skip("no CUDA device")
-    res = {}
-    for flag in ("0", "1"):
-        path = str(tmp_path / f"z{flag}.npz")
-        e = dict(os.environ)
-        e["PFCS_TMA_Z"] = flag
-        subprocess.run([sys.executable, "-c", PFC_CHILD.format(root=str(ROOT), path=path)], check=True, env=e,
-                       timeout=600)
-        res[flag] = np.load(path)
-    for k in res["0"].files:
-        assert np.array_equal(res["0"][k], res["1"][k]), k
 
 
 def test_cube_ls_bit_identical(tmp_path):
