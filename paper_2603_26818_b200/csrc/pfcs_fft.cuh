@@ -273,14 +273,21 @@ struct BarSync {
   }
 };
 
+// Exchange workspace of one line: a padded shared-memory line (double2*,
+// element n at PAD(n)) or any accessor with ref(n) (e.g. the line's column
+// of a swizzled TMA stage, pfcs_x.cu k_cube_ls).
+__device__ __forceinline__ double2& ws_ref(double2* sl, int n) { return sl[pad_idx(n)]; }
+template <class W>
+__device__ __forceinline__ double2& ws_ref(const W& w, int n) { return w.ref(n); }
+
 // One Stockham pass (span Ns) followed, if more passes remain, by the
 // shared-memory exchange and the next pass.  On entry v[e] holds element
 // j + P*e of this pass's input; on exit of the last pass v[e] holds output
 // element j + P*e.  `tw` is the size-N table exp(-2 pi i m / N), m < N,
 // read with stride TWS (so a size-2N table serves an N-point transform).
 template <int N, int Ns, bool FWD, int TWS, int TWL = PFCS_TW_LOADS, int R = radix_R(N), bool TSM = false,
-          class Sync = CtaSync>
-__device__ __forceinline__ void fft_pass(double2 (&v)[R], int j, double2* sl,
+          class Sync = CtaSync, class WS = double2*>
+__device__ __forceinline__ void fft_pass(double2 (&v)[R], int j, WS sl,
                                          const double2* __restrict__ tw, Sync sync = Sync{}) {
   // R = values per thread (8, or 4 for the register-heavy fused passes);
   // each pass uses radix min(R, remaining) and R/r butterflies per thread
@@ -344,22 +351,22 @@ __device__ __forceinline__ void fft_pass(double2 (&v)[R], int j, double2* sl,
       const int k = b & (Ns - 1);
       const int base = (b / Ns) * Ns * r + k;
 #pragma unroll
-      for (int q = 0; q < r; ++q) sl[pad_idx(base + q * Ns)] = v[s + q * S];
+      for (int q = 0; q < r; ++q) ws_ref(sl, base + q * Ns) = v[s + q * S];
     }
     sync();
 #pragma unroll
-    for (int e = 0; e < R; ++e) v[e] = sl[pad_idx(j + P * e)];
-    fft_pass<N, Ns * r, FWD, TWS, TWL, R, TSM, Sync>(v, j, sl, tw, sync);
+    for (int e = 0; e < R; ++e) v[e] = ws_ref(sl, j + P * e);
+    fft_pass<N, Ns * r, FWD, TWS, TWL, R, TSM, Sync, WS>(v, j, sl, tw, sync);
   }
 }
 
 // Full N-point transform of the register set (see fft_pass).  All threads of
 // the CTA must call it (it contains __syncthreads when N > 8).
 template <int N, bool FWD, int TWS = 1, int TWL = PFCS_TW_LOADS, int R = radix_R(N), bool TSM = false,
-          class Sync = CtaSync>
-__device__ __forceinline__ void fft_line(double2 (&v)[R], int j, double2* sl,
+          class Sync = CtaSync, class WS = double2*>
+__device__ __forceinline__ void fft_line(double2 (&v)[R], int j, WS sl,
                                          const double2* __restrict__ tw, Sync sync = Sync{}) {
-  fft_pass<N, 1, FWD, TWS, TWL, R, TSM, Sync>(v, j, sl, tw, sync);
+  fft_pass<N, 1, FWD, TWS, TWL, R, TSM, Sync, WS>(v, j, sl, tw, sync);
 }
 
 // Stash register set (element j + P*e in v[e]) into the padded smem line.

@@ -363,17 +363,36 @@ template <int M, int T>
 struct CubeLs {
   static constexpr int R = 8;
   static constexpr int P = M / R;
-  static constexpr int LS = pad_idx(M);               // per-line workspace (contiguous mapping)
   static constexpr int ROWB = T * 16;                 // bytes per stage row (= swizzle span)
   static constexpr size_t STAGE = (size_t)(M + 1) * ROWB;
   static constexpr size_t PADDED = (STAGE + 1023) / 1024 * 1024;
+  static constexpr int NS = 3;                        // pipeline stages (no separate FFT workspace)
   static constexpr int BR = M < 256 ? M : 256;        // rows per TMA box
   static constexpr int NB = M / BR;
   static constexpr int THREADS = T * P;
-  static constexpr size_t SMEM = 2 * PADDED + (size_t)T * LS * 16 + 64 + 1024;
-  // stage element (row r, column t) under the TMA swizzle of a ROWB-byte row
+  static constexpr size_t SMEM = NS * PADDED + 64 + 1024;
+  // stage element (row r, column t) under the TMA swizzle of a ROWB-byte row:
+  // line t owns chunk t ^ f(r) of every row, and the 16-byte slot of any 8
+  // rows with distinct r & 7 fall on distinct banks (ROWB = 128 or 64)
   __device__ __forceinline__ static int at(int r, int t) {
     return r * T + (t ^ ((r * ROWB >> 7) & (T - 1)));
+  }
+};
+
+// The FFT exchanges of line t run inside the line's own stage column (the
+// slots it owns in every row), with logical element n on row
+// rho(n) = (n & ~7) | ((n ^ (n >> 3)) & 7): any 8 aligned consecutive
+// elements and any 8 elements of stride 8 (the Stockham write pattern of the
+// first radix-8 pass) land on rows with distinct r & 7, i.e. distinct banks.
+// The inputs were consumed before the first exchange, so the padded
+// per-line workspace is not needed and its 74 KB buy a third stage.
+template <class C>
+struct StageCol {
+  double2* base;
+  int t;
+  __device__ __forceinline__ double2& ref(int n) const {
+    const int r = (n & ~7) | ((n ^ (n >> 3)) & 7);
+    return base[C::at(r, t)];
   }
 };
 
@@ -396,11 +415,11 @@ __global__ void __launch_bounds__(CubeLs<M, T>::THREADS, 1)
   using C = CubeLs<M, T>;
   constexpr int R = C::R;
   constexpr int P = C::P;
+  constexpr int NS = C::NS;
   extern __shared__ unsigned char craw[];
   unsigned char* cbase = craw + ((1024u - (smem_u32(craw) & 1023u)) & 1023u);
-  double2* ws = (double2*)(cbase + 2 * C::PADDED);
-  unsigned long long* full = (unsigned long long*)(ws + (size_t)T * C::LS);
-  unsigned* done = (unsigned*)(full + 2);  // lines finished with the stage's tile
+  unsigned long long* full = (unsigned long long*)(cbase + NS * C::PADDED);
+  unsigned* done = (unsigned*)(full + NS);  // lines finished with the stage's tile
   const int tid = threadIdx.x;
   const i64 ntiles = (inner + T - 1) / T;
   double m_abs = 0.0;
@@ -418,14 +437,14 @@ __global__ void __launch_bounds__(CubeLs<M, T>::THREADS, 1)
     else tma_store_2d(&tm.b, buf + (size_t)M * C::ROWB, c0, M);
   };
   // line leader, once its line is done with stage s of `tile`: the last line
-  // of the tile (stores the stage and) refills it with the tile after next
+  // of the tile stores the stage and refills it with this CTA's tile NS later
   auto release = [&](i64 tile, int s) {
     __threadfence_block();
     const unsigned prev = atomicAdd(&done[s], 1u);
     if (prev == (unsigned)T - 1) {
       __threadfence_block();
       done[s] = 0;
-      const i64 nxt = tile + 2 * (i64)gridDim.x;
+      const i64 nxt = tile + NS * (i64)gridDim.x;
       fence_proxy_async();
       xfer(tile, s, false);
       bulk_commit();
@@ -439,11 +458,12 @@ __global__ void __launch_bounds__(CubeLs<M, T>::THREADS, 1)
   };
 
   if (tid == 0) {
-    mbar_init(&full[0], 1);
-    mbar_init(&full[1], 1);
-    done[0] = done[1] = 0;
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&full[s], 1);
+      done[s] = 0;
+    }
     mbar_fence_init();
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < NS; ++s) {
       const i64 tile = blockIdx.x + (i64)s * gridDim.x;
       if (tile < ntiles) {
         mbar_expect_tx(&full[s], (unsigned)C::STAGE);
@@ -455,13 +475,11 @@ __global__ void __launch_bounds__(CubeLs<M, T>::THREADS, 1)
 
   const int t = tid / P;  // line of the tile, position j = tid % P
   const BarSync lsync{1u + (unsigned)t, (unsigned)P};
-  double2* sl = ws + t * C::LS;
-  int it = 0;
+  int it = 0, s = 0, ph = 0;  // stage s = it % NS, its phase parity ph = (it / NS) & 1
   for (i64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
-    const int s = it & 1;
     const int jj = opaque((int)(opaque_tid() % P));
-    const double2* cur = (const double2*)(cbase + (size_t)s * C::PADDED);
-    mbar_wait(&full[s], (unsigned)((it >> 1) & 1));
+    double2* cur = (double2*)(cbase + (size_t)s * C::PADDED);
+    mbar_wait(&full[s], (unsigned)ph);
     const double2 wj = __ldg(&twN[jj]);
     double2 v[R];
 #pragma unroll
@@ -483,7 +501,7 @@ __global__ void __launch_bounds__(CubeLs<M, T>::THREADS, 1)
       const double2 wd = make_double2(fma(d.x, w.x, d.y * w.y), fma(d.y, w.x, -d.x * w.y));
       v[e] = make_double2(sm.x - wd.y, sm.y + wd.x);
     }
-    fft_line<M, false, 2, PFCS_X_TWL, R, false, BarSync>(v, jj, sl, twN, lsync);
+    fft_line<M, false, 2, PFCS_X_TWL, R, false, BarSync>(v, jj, StageCol<C>{cur, t}, twN, lsync);
     const bool ok = (i64)opaque((int)(tile * T)) + t < inner;
 #pragma unroll
     for (int e = 0; e < R; ++e) {
@@ -493,12 +511,12 @@ __global__ void __launch_bounds__(CubeLs<M, T>::THREADS, 1)
     }
     const unsigned tid2 = opaque_tid();
     const int j2 = (int)(tid2 % P), t2 = (int)(tid2 / P);
-    fft_line<M, true, 2, PFCS_X_TWL, R, false, BarSync>(v, j2, ws + t2 * C::LS, twN, lsync);
-    // R2C split: pair Z_k with Z_{M-k} through the line's stage column (rows
-    // last read before the FFT's barriers; the swizzle keeps any 8
-    // consecutive rows on distinct banks, for the stash and the mirrored
-    // reads alike)
-    double2* col = (double2*)(cbase + (size_t)(opaque(it) & 1) * C::PADDED);
+    double2* col = (double2*)(cbase + (size_t)opaque(s) * C::PADDED);
+    fft_line<M, true, 2, PFCS_X_TWL, R, false, BarSync>(v, j2, StageCol<C>{col, t2}, twN, lsync);
+    // R2C split: pair Z_k with Z_{M-k} through the line's stage column (the
+    // TMA-swizzle layout keeps any 8 consecutive rows on distinct banks, for
+    // the stash and the mirrored reads alike)
+    lsync();  // the last exchange's reads of the column are done
 #pragma unroll
     for (int e = 0; e < R; ++e) col[C::at(j2 + P * e, t2)] = v[e];
     lsync();
@@ -533,6 +551,10 @@ __global__ void __launch_bounds__(CubeLs<M, T>::THREADS, 1)
       fence_proxy_async();  // my stage writes before the async-proxy store
       lsync();
       if (j2 == 0) release(tile, s);
+    }
+    if (++s == NS) {
+      s = 0;
+      ph ^= 1;
     }
   }
   if (threadIdx.x % P == 0) bulk_wait0();  // stores this thread issued have completed
