@@ -486,8 +486,8 @@ def multi_bytes(n: int) -> float:
 def run_multi(ctx, args):
     """configs[4]: multiphysics PFC (density + composition + 3 velocities),
     field-per-GPU: 1 GPU runs all roles, 5 / 8 GPUs the multiphysics role
-    maps (real fields: the R2C path), 4 GPUs the reference's four-role hydro
-    dataflow (complex full-grid fields, as the reference holds them)."""
+    maps, 4 GPUs the reference's four-role hydro dataflow — all on real
+    fields (the R2C path)."""
     import numpy as np
     import torch
 
@@ -504,36 +504,28 @@ def run_multi(ctx, args):
     mp = mpx.MultiParams(hydro=hp, mobility=1.0, kappa=1.0, alpha=1.0, beta=0.0)
     sym = make_symbols(grid, -0.3, a0=2.0)
     gen = torch.Generator(device=ctx.device).manual_seed(11)
-    real = G != 4
 
-    def field(scale, base=0.0):
+    def field(scale, base=0.0):  # real physical fields: every role map takes the R2C path
         x = torch.rand((n,) * 3, dtype=torch.float64, device=ctx.device, generator=gen)
-        x = base + scale * (x - 0.5)
-        return x if real else x.to(torch.complex128)
+        return base + scale * (x - 0.5)
 
     psi = field(0.02, -0.3)
     c = field(0.2)
     w = ctx.worker()
-    if real:
-        R3 = mpx._Real3.of((n,) * 3, sym, ctx.device)
-        zeros = torch.zeros((n,) * 3, dtype=torch.float64, device=ctx.device)
-        f = mpx.MultiFields(psi_hat=R3.fwd(psi), psi=psi, c_hat=R3.fwd(c), c=c,
-                            v_hat=[R3.fwd(zeros) for _ in range(3)], v=[zeros.clone() for _ in range(3)])
-    else:
-        zeros = torch.zeros((n,) * 3, dtype=torch.complex128, device=ctx.device)
-        f = mpx.MultiFields(psi_hat=hydro._fft(psi, True), psi=psi, c_hat=hydro._fft(c, True), c=c,
-                            v_hat=[zeros.clone() for _ in range(3)], v=[zeros.clone() for _ in range(3)])
+    R3 = mpx._Real3.of((n,) * 3, sym, ctx.device)
+    zeros = torch.zeros((n,) * 3, dtype=torch.float64, device=ctx.device)
+    f = mpx.MultiFields(psi_hat=R3.fwd(psi), psi=psi, c_hat=R3.fwd(c), c=c,
+                        v_hat=[R3.fwd(zeros) for _ in range(3)], v=[zeros.clone() for _ in range(3)])
     torch.cuda.empty_cache()  # the FFT/PFC workloads' blocks are not reused here
     steps = max(3, args.steps // 4)
     if G == 1:
         fn = lambda: mpx.serial_multi_step(f, sym, mp)  # noqa: E731
         mode = "all 5 roles on 1 GPU (R2C: real fields, x-halved spectra)"
     elif G == 4:
-        hf = hydro.HydroFields(psi_hat=f.psi_hat, psi=f.psi, v_hat=f.v_hat, v=f.v)
-        st = ({"psi_hat": hf.psi_hat, "psi": hf.psi, "v": list(hf.v), "step_index": 0} if ctx.rank == 0
-              else {"v_hat": zeros.clone(), "psi": zeros.clone(), "step_index": 0})
+        st = ({"psi_hat": f.psi_hat, "psi": f.psi, "v": list(f.v), "step_index": 0} if ctx.rank == 0
+              else {"v_hat": f.v_hat[ctx.rank - 1].clone(), "psi": zeros.clone(), "step_index": 0})
         fn = lambda: hydro.parallel_hydro_step(w, st, sym, hp)  # noqa: E731
-        mode = "reference 4-role hydro dataflow (psi, v1..v3), complex fields, no composition"
+        mode = "reference 4-role hydro dataflow (psi, v1..v3; R2C), no composition"
     else:
         st = mpx.initial_role_state(ctx.rank, G, f)
         fn = lambda: mpx.parallel_multi_step(w, st, sym, mp)  # noqa: E731

@@ -9,11 +9,15 @@ coupled to a coarse-grained velocity (v1, v2, v3):
 Parallel strategy (paper strategy 2, hydro.py:129-156): one field per GPU —
 rank 0 owns psi, ranks 1..3 own v1..v3 — with the physical psi broadcast
 from rank 0 (tag 2) and the physical velocities returned (tags 4, 5, 6)
-once per step.  Fields are full-grid complex128 CUDA tensors; transforms are
-the libpfcs line kernels (serial 3D FFT, one HBM pass per axis) and the
-pointwise operators are libpfcs kernels in numpy's evaluation order
-(csrc/pfcs_hydro.cu).  numpy inputs are accepted (and numpy returned) for
-drop-in use; CUDA tensors stay on the device.
+once per step.  Complex full-grid fields (the reference's representation)
+are transformed C2C by the libpfcs line kernels (one HBM pass per axis) with
+the pointwise operators as libpfcs kernels in numpy's evaluation order
+(csrc/pfcs_hydro.cu).  Real physical fields (float64 psi, v_i with x-halved
+half spectra) take the B200 R2C path at the end of this module: half the
+bytes per transform, 8-byte real products (pfcs_real_pointwise), the i k
+multipliers fused into the inverse transforms, one divergence read-back per
+step; results equal the C2C path to rounding.  numpy inputs are accepted
+(and numpy returned) for drop-in use; CUDA tensors stay on the device.
 """
 
 from __future__ import annotations
@@ -250,7 +254,11 @@ def hydro_velocity_step(v_hat, psi, d_axis, sym: SymbolTable, params: HydroParam
 
 def serial_hydro_step(fields: HydroFields, sym: SymbolTable, params: HydroParams) -> HydroFields:
     """The four-role dataflow on one worker (hydro.py:110-126): density
-    first with the previous velocities, then v1..v3 with the fresh density."""
+    first with the previous velocities, then v1..v3 with the fresh density.
+    Real physical fields (float64 psi, v_i; x-halved spectra) take the R2C
+    path (module doc)."""
+    if _is_real(fields.psi):
+        return _serial_hydro_step_r(fields, sym, params)
     fields.psi_hat, fields.psi = hydro_psi_step(fields.psi_hat, fields.psi, *fields.v, sym, params,
                                                 step_index=fields.step_index)
     ps = _dev(fields.psi)
@@ -270,6 +278,8 @@ def parallel_hydro_step(worker, role_state: dict, sym: SymbolTable, params: Hydr
     device copies between threads); host arrays as host objects."""
     rank = worker.rank
     device_msgs = isinstance(role_state.get("psi"), torch.Tensor)
+    if device_msgs and not role_state["psi"].is_complex():
+        return _parallel_hydro_step_r(worker, role_state, sym, params)
     if rank == 0:
         psi_hat, psi = hydro_psi_step(role_state["psi_hat"], role_state["psi"], *role_state["v"], sym,
                                       params, step_index=role_state["step_index"])
@@ -322,3 +332,206 @@ def free_energy_full(psi, sym: SymbolTable, grid: GridSpec) -> float:
                           device=dev)
     nat.call("pfcs_energy_sum", nat.ptr(a), 2, nat.ptr(b), 2, n, nat.ptr(out), nat.ptr(scratch), st)
     return float(out.item()) * grid.cell_volume
+
+
+# ------------------------------------------------------------ R2C path ------
+# Real physical fields (float64) with x-halved spectra: the B200
+# representation of the hydro / multiphysics fields (multiphysics.py doc).
+
+RPW_CUBE, RPW_MUL, RPW_ADV3, RPW_CHNL, RPW_ADD3 = 0, 1, 2, 3, 4  # pfcs_real_pointwise kinds
+
+
+def _is_real(x) -> bool:
+    if isinstance(x, torch.Tensor):
+        return not x.is_complex()
+    return isinstance(x, np.ndarray) and not np.iscomplexobj(x)
+
+
+def _rdev(x) -> torch.Tensor:
+    """float64 CUDA tensor (contiguous) of a real field."""
+    if isinstance(x, torch.Tensor):
+        t = x if x.is_cuda else x.cuda()
+        return t.to(torch.float64).contiguous()
+    nat.load()
+    return torch.from_numpy(np.ascontiguousarray(np.asarray(x, dtype=np.float64))).to(
+        torch.device("cuda", torch.cuda.current_device()))
+
+
+def _hdev(x) -> torch.Tensor:
+    """complex128 CUDA tensor of a half spectrum."""
+    return _dev(x)
+
+
+class _Real3:
+    """Full-grid 3D R2C / C2R transforms of an (nx, ny, nz) real field with the
+    x axis halved — the layout of the slab pipeline at G = 1 (distfft):
+    forward rfft_x, y, z; inverse z, y, irfft_x; the inverse may fuse the
+    derivative multiplier i d_axis into its first (z) pass."""
+
+    def __init__(self, shape, sym: SymbolTable, device):
+        nx, ny, nz = shape
+        if nx < 4 or nx & (nx - 1):
+            raise ValueError(f"the R2C multiphysics path needs a power-of-two nx >= 4, got {nx}")
+        self.shape = (nx, ny, nz)
+        self.nh = nx // 2 + 1
+        self.hshape = (self.nh, ny, nz)
+        kx, ky, kz, dx, dy, dz = sym.device_vectors(device)
+        self.k = (kx[: self.nh].contiguous(), ky, kz)
+        self.d = (dx[: self.nh].contiguous(), dy, dz)
+
+    @staticmethod
+    def of(shape, sym: SymbolTable, device) -> "_Real3":
+        cache = sym.__dict__.setdefault("_real3", {})
+        key = (tuple(shape), str(device))
+        if key not in cache:
+            cache[key] = _Real3(shape, sym, device)
+        return cache[key]
+
+    def fwd(self, x: torch.Tensor) -> torch.Tensor:
+        nx, ny, nz = self.shape
+        out = torch.empty(self.hshape, dtype=torch.complex128, device=x.device)
+        st = nat.stream_ptr()
+        nat.call("pfcs_rfft_x", nat.ptr(x), nat.ptr(out), nx, ny * nz, st)
+        if ny > 1:
+            nat.call("pfcs_fft_axis_c2c", nat.ptr(out), nat.ptr(out), self.nh, ny, nz, 1, 1, st)
+        if nz > 1:
+            nat.call("pfcs_fft_axis_c2c", nat.ptr(out), nat.ptr(out), self.nh, ny, nz, 2, 1, st)
+        return out
+
+    def inv(self, h: torch.Tensor, deriv: int | None = None) -> torch.Tensor:
+        nx, ny, nz = self.shape
+        nh = self.nh
+        st = nat.stream_ptr()
+        tmp = torch.empty_like(h)
+        if deriv is not None:  # i d_axis x_hat fused into the z pass
+            nat.call("pfcs_fft_axis_c2c_pro", nat.ptr(h), nat.ptr(tmp), nh, ny, nz, 2, 0, 3,
+                     nat.ptr(self.d[deriv]), deriv, st)
+        else:
+            nat.call("pfcs_fft_axis_c2c", nat.ptr(h), nat.ptr(tmp), nh, ny, nz, 2, 0, st)
+        if ny > 1:
+            nat.call("pfcs_fft_axis_c2c", nat.ptr(tmp), nat.ptr(tmp), nh, ny, nz, 1, 0, st)
+        out = torch.empty(self.shape, dtype=torch.float64, device=h.device)
+        nat.call("pfcs_irfft_x", nat.ptr(tmp), nat.ptr(out), nx, ny * nz, st)
+        return out
+
+
+def _rpw(kind: int, *ops: torch.Tensor, alpha: float = 0.0) -> torch.Tensor:
+    out = torch.empty_like(ops[0])
+    args = [nat.ptr(o) for o in ops] + [None] * (6 - len(ops))
+    nat.call("pfcs_real_pointwise", kind, *args, nat.ptr(out), out.numel(), float(alpha), nat.stream_ptr())
+    return out
+
+
+class _StepFlag:
+    """One device diagnostics block shared by a step's spectral updates; the
+    non-finite flag is read back once per step (not once per update)."""
+
+    def __init__(self, device):
+        self.t = torch.zeros(nat.DIAG_SLOTS * nat.DIAG_VALS, dtype=torch.float64, device=device)
+
+    def check(self, step_index: int, *fields: torch.Tensor) -> None:
+        if self.t.view(nat.DIAG_SLOTS, nat.DIAG_VALS)[:, 3].max().item() > 0:
+            for f in fields:
+                if not bool(torch.isfinite(torch.view_as_real(f) if f.is_complex() else f).all()):
+                    _raise_divergence(step_index, f)
+            _raise_divergence(step_index, fields[0])
+
+
+def _grad_dot_r(R: _Real3, x_hat: torch.Tensor, v) -> torch.Tensor:
+    """v . grad x = sum_i v_i F^-1(i d_i x_hat), real (hydro.py:83-85 order)."""
+    g = [R.inv(x_hat, deriv=i) for i in range(3)]
+    return _rpw(RPW_ADV3, v[0], g[0], v[1], g[1], v[2], g[2])
+
+
+def _adv_term_r(R: _Real3, x_hat: torch.Tensor, axis: int, v_axis: torch.Tensor) -> torch.Tensor:
+    """v_axis F^-1(i d_axis x_hat): one advection product (G = 8 helper roles)."""
+    return _rpw(RPW_MUL, v_axis, R.inv(x_hat, deriv=axis))
+
+
+def _density_r(R: _Real3, ph, ps, adv, sym, hp: HydroParams, flag: _StepFlag):
+    nh, ny, nz = R.hshape
+    kx, ky, kz = R.k
+    nl_hat = R.fwd(_rpw(RPW_CUBE, ps))
+    adv_hat = R.fwd(adv)
+    new = torch.empty_like(ph)
+    nat.call("pfcs_hydro_psi_update_to", nat.ptr(ph), nat.ptr(new), nat.ptr(nl_hat), nat.ptr(adv_hat), nh, ny, nz,
+             nat.ptr(kx), nat.ptr(ky), nat.ptr(kz), float(sym.eps), float(hp.pfc.dt), nat.ptr(flag.t),
+             nat.stream_ptr())
+    return new, R.inv(new)
+
+
+def _density_mu_r(R: _Real3, ps, sym) -> torch.Tensor:
+    nh, ny, nz = R.hshape
+    kx, ky, kz = R.k
+    nl_hat = R.fwd(_rpw(RPW_CUBE, ps))
+    f_hat = R.fwd(ps)
+    mu = torch.empty_like(nl_hat)
+    nat.call("pfcs_hydro_mu", nat.ptr(nl_hat), nat.ptr(f_hat), nat.ptr(mu), nh, ny, nz, nat.ptr(kx), nat.ptr(ky),
+             nat.ptr(kz), float(sym.eps), nat.stream_ptr())
+    return mu
+
+
+def _velocity_r(R: _Real3, vh, ps, axis: int, mu_hat, sym, hp: HydroParams, flag: _StepFlag, cc=None,
+                muc=None, beta: float = 0.0):
+    nh, ny, nz = R.hshape
+    kx, ky, kz = R.k
+    force = R.fwd(_rpw(RPW_MUL, ps, R.inv(mu_hat, deriv=axis)))  # F(psi F^-1(i k mu_hat))
+    if beta != 0.0:
+        force_c = R.fwd(_rpw(RPW_MUL, cc, R.inv(muc, deriv=axis)))
+        total = torch.empty_like(force)
+        nat.call("pfcs_axpy", nat.ptr(force), nat.ptr(force_c), nat.ptr(total), total.numel(), float(beta),
+                 nat.stream_ptr())
+        force = total
+    dt, rho = float(hp.pfc.dt), float(hp.rho)
+    new = torch.empty_like(vh)
+    nat.call("pfcs_hydro_vel_update_to", nat.ptr(vh), nat.ptr(new), nat.ptr(force), nh, ny, nz, nat.ptr(kx),
+             nat.ptr(ky), nat.ptr(kz), dt / rho, (dt / rho) * float(hp.gamma), -0.5 * float(sym.a0) ** 2,
+             nat.ptr(flag.t), nat.stream_ptr())
+    return new, R.inv(new)
+
+
+def _serial_hydro_step_r(fields: HydroFields, sym: SymbolTable, params: HydroParams) -> HydroFields:
+    host = isinstance(fields.psi, np.ndarray)
+    ps = _rdev(fields.psi)
+    R = _Real3.of(ps.shape, sym, ps.device)
+    flag = _StepFlag(ps.device)
+    ph = _hdev(fields.psi_hat)
+    vs = [_rdev(v) for v in fields.v]
+    psi_hat, psi = _density_r(R, ph, ps, _grad_dot_r(R, ph, vs), sym, params, flag)
+    mu_hat = _density_mu_r(R, psi, sym)  # shared by the three components
+    out = [_velocity_r(R, _hdev(fields.v_hat[i]), psi, i, mu_hat, sym, params, flag) for i in range(3)]
+    flag.check(fields.step_index, psi_hat, *(o[0] for o in out))
+    fields.psi_hat, fields.psi = _out(psi_hat, host), _out(psi, host)
+    for i in range(3):
+        fields.v_hat[i], fields.v[i] = _out(out[i][0], host), _out(out[i][1], host)
+    fields.step_index += 1
+    fields.sim_time += params.pfc.dt
+    return fields
+
+
+def _parallel_hydro_step_r(worker, role_state: dict, sym: SymbolTable, params: HydroParams) -> dict:
+    """parallel_hydro_step on real device fields: psi and v_i travel as 8-byte
+    real fields, the spectra are x-halved (bit-identical to the R2C serial step)."""
+    rank = worker.rank
+    psi0 = role_state["psi"]
+    R = _Real3.of(tuple(psi0.shape), sym, psi0.device)
+    flag = _StepFlag(psi0.device)
+    idx = role_state["step_index"]
+    if rank == 0:
+        ph = role_state["psi_hat"]
+        psi_hat, psi = _density_r(R, ph, psi0, _grad_dot_r(R, ph, role_state["v"]), sym, params, flag)
+        flag.check(idx, psi_hat)
+        role_state["psi_hat"], role_state["psi"] = psi_hat, psi
+        for dst in (1, 2, 3):
+            worker.send_tensor(dst, TAG_PSI, psi)
+        role_state["v"] = [worker.recv_tensor(i + 1, V_TAGS[i], torch.empty_like(psi)) for i in range(3)]
+    else:
+        i = rank - 1
+        psi = worker.recv_tensor(0, TAG_PSI, torch.empty_like(psi0))
+        role_state["psi"] = psi
+        v_hat, v = _velocity_r(R, role_state["v_hat"], psi, i, _density_mu_r(R, psi, sym), sym, params, flag)
+        flag.check(idx, v_hat)
+        role_state["v_hat"], role_state["v_own"] = v_hat, v
+        worker.send_tensor(0, V_TAGS[i], v)
+    role_state["step_index"] = idx + 1
+    return role_state

@@ -51,8 +51,9 @@ import torch
 
 from . import _native as nat
 from .grid import SymbolTable
-from .hydro import (HydroParams, TAG_PSI, V_TAGS, _dev, _Diag, _fft, _fft_cmul, _fft_cube, _ifft_deriv, _out,
-                    _raise_divergence, _vectors)
+from .hydro import (HydroParams, TAG_PSI, V_TAGS, RPW_ADD3, RPW_CHNL, _dev, _Diag, _Real3, _StepFlag, _adv_term_r,
+                    _density_mu_r, _density_r, _fft, _fft_cmul, _fft_cube, _grad_dot_r, _hdev, _ifft_deriv, _is_real,
+                    _out, _raise_divergence, _rdev, _rpw, _vectors, _velocity_r)
 
 __all__ = [
     "MultiParams",
@@ -325,128 +326,6 @@ def parallel_multi_step(worker, st: dict, sym: SymbolTable, params: MultiParams)
 
 # ------------------------------------------------------------ R2C path ------
 
-RPW_CUBE, RPW_MUL, RPW_ADV3, RPW_CHNL, RPW_ADD3 = 0, 1, 2, 3, 4  # pfcs_real_pointwise kinds
-
-
-def _is_real(x) -> bool:
-    if isinstance(x, torch.Tensor):
-        return not x.is_complex()
-    return isinstance(x, np.ndarray) and not np.iscomplexobj(x)
-
-
-def _rdev(x) -> torch.Tensor:
-    """float64 CUDA tensor (contiguous) of a real field."""
-    if isinstance(x, torch.Tensor):
-        t = x if x.is_cuda else x.cuda()
-        return t.to(torch.float64).contiguous()
-    nat.load()
-    return torch.from_numpy(np.ascontiguousarray(np.asarray(x, dtype=np.float64))).to(
-        torch.device("cuda", torch.cuda.current_device()))
-
-
-def _hdev(x) -> torch.Tensor:
-    """complex128 CUDA tensor of a half spectrum."""
-    return _dev(x)
-
-
-class _Real3:
-    """Full-grid 3D R2C / C2R transforms of an (nx, ny, nz) real field with the
-    x axis halved — the layout of the slab pipeline at G = 1 (distfft):
-    forward rfft_x, y, z; inverse z, y, irfft_x; the inverse may fuse the
-    derivative multiplier i d_axis into its first (z) pass."""
-
-    def __init__(self, shape, sym: SymbolTable, device):
-        nx, ny, nz = shape
-        if nx < 4 or nx & (nx - 1):
-            raise ValueError(f"the R2C multiphysics path needs a power-of-two nx >= 4, got {nx}")
-        self.shape = (nx, ny, nz)
-        self.nh = nx // 2 + 1
-        self.hshape = (self.nh, ny, nz)
-        kx, ky, kz, dx, dy, dz = sym.device_vectors(device)
-        self.k = (kx[: self.nh].contiguous(), ky, kz)
-        self.d = (dx[: self.nh].contiguous(), dy, dz)
-
-    @staticmethod
-    def of(shape, sym: SymbolTable, device) -> "_Real3":
-        cache = sym.__dict__.setdefault("_real3", {})
-        key = (tuple(shape), str(device))
-        if key not in cache:
-            cache[key] = _Real3(shape, sym, device)
-        return cache[key]
-
-    def fwd(self, x: torch.Tensor) -> torch.Tensor:
-        nx, ny, nz = self.shape
-        out = torch.empty(self.hshape, dtype=torch.complex128, device=x.device)
-        st = _st()
-        nat.call("pfcs_rfft_x", nat.ptr(x), nat.ptr(out), nx, ny * nz, st)
-        if ny > 1:
-            nat.call("pfcs_fft_axis_c2c", nat.ptr(out), nat.ptr(out), self.nh, ny, nz, 1, 1, st)
-        if nz > 1:
-            nat.call("pfcs_fft_axis_c2c", nat.ptr(out), nat.ptr(out), self.nh, ny, nz, 2, 1, st)
-        return out
-
-    def inv(self, h: torch.Tensor, deriv: int | None = None) -> torch.Tensor:
-        nx, ny, nz = self.shape
-        nh = self.nh
-        st = _st()
-        tmp = torch.empty_like(h)
-        if deriv is not None:  # i d_axis x_hat fused into the z pass
-            nat.call("pfcs_fft_axis_c2c_pro", nat.ptr(h), nat.ptr(tmp), nh, ny, nz, 2, 0, 3,
-                     nat.ptr(self.d[deriv]), deriv, st)
-        else:
-            nat.call("pfcs_fft_axis_c2c", nat.ptr(h), nat.ptr(tmp), nh, ny, nz, 2, 0, st)
-        if ny > 1:
-            nat.call("pfcs_fft_axis_c2c", nat.ptr(tmp), nat.ptr(tmp), nh, ny, nz, 1, 0, st)
-        out = torch.empty(self.shape, dtype=torch.float64, device=h.device)
-        nat.call("pfcs_irfft_x", nat.ptr(tmp), nat.ptr(out), nx, ny * nz, st)
-        return out
-
-
-def _rpw(kind: int, *ops: torch.Tensor, alpha: float = 0.0) -> torch.Tensor:
-    out = torch.empty_like(ops[0])
-    args = [nat.ptr(o) for o in ops] + [None] * (6 - len(ops))
-    nat.call("pfcs_real_pointwise", kind, *args, nat.ptr(out), out.numel(), float(alpha), _st())
-    return out
-
-
-class _StepFlag:
-    """One device diagnostics block shared by a step's spectral updates; the
-    non-finite flag is read back once per step (not once per update)."""
-
-    def __init__(self, device):
-        self.t = torch.zeros(nat.DIAG_SLOTS * nat.DIAG_VALS, dtype=torch.float64, device=device)
-
-    def check(self, step_index: int, *fields: torch.Tensor) -> None:
-        if self.t.view(nat.DIAG_SLOTS, nat.DIAG_VALS)[:, 3].max().item() > 0:
-            for f in fields:
-                if not bool(torch.isfinite(torch.view_as_real(f) if f.is_complex() else f).all()):
-                    _raise_divergence(step_index, f)
-            _raise_divergence(step_index, fields[0])
-
-
-def _grad_dot_r(R: _Real3, x_hat: torch.Tensor, v) -> torch.Tensor:
-    """v . grad x = sum_i v_i F^-1(i d_i x_hat), real (hydro.py:83-85 order)."""
-    g = [R.inv(x_hat, deriv=i) for i in range(3)]
-    return _rpw(RPW_ADV3, v[0], g[0], v[1], g[1], v[2], g[2])
-
-
-def _adv_term_r(R: _Real3, x_hat: torch.Tensor, axis: int, v_axis: torch.Tensor) -> torch.Tensor:
-    """v_axis F^-1(i d_axis x_hat): one advection product (G = 8 helper roles)."""
-    return _rpw(RPW_MUL, v_axis, R.inv(x_hat, deriv=axis))
-
-
-def _density_r(R: _Real3, ph, ps, adv, sym, params: MultiParams, flag: _StepFlag):
-    nh, ny, nz = R.hshape
-    kx, ky, kz = R.k
-    nl_hat = R.fwd(_rpw(RPW_CUBE, ps))
-    adv_hat = R.fwd(adv)
-    new = torch.empty_like(ph)
-    nat.call("pfcs_hydro_psi_update_to", nat.ptr(ph), nat.ptr(new), nat.ptr(nl_hat), nat.ptr(adv_hat), nh, ny, nz,
-             nat.ptr(kx), nat.ptr(ky), nat.ptr(kz), float(sym.eps), float(params.hydro.pfc.dt), nat.ptr(flag.t),
-             _st())
-    return new, R.inv(new)
-
-
 def _composition_r(R: _Real3, ch, cc, v, sym, params: MultiParams, flag: _StepFlag):
     nh, ny, nz = R.hshape
     kx, ky, kz = R.k
@@ -459,17 +338,6 @@ def _composition_r(R: _Real3, ch, cc, v, sym, params: MultiParams, flag: _StepFl
     return new, R.inv(new)
 
 
-def _density_mu_r(R: _Real3, ps, sym) -> torch.Tensor:
-    nh, ny, nz = R.hshape
-    kx, ky, kz = R.k
-    nl_hat = R.fwd(_rpw(RPW_CUBE, ps))
-    f_hat = R.fwd(ps)
-    mu = torch.empty_like(nl_hat)
-    nat.call("pfcs_hydro_mu", nat.ptr(nl_hat), nat.ptr(f_hat), nat.ptr(mu), nh, ny, nz, nat.ptr(kx), nat.ptr(ky),
-             nat.ptr(kz), float(sym.eps), _st())
-    return mu
-
-
 def _composition_mu_r(R: _Real3, cc, ch, params: MultiParams) -> torch.Tensor:
     nh, ny, nz = R.hshape
     kx, ky, kz = R.k
@@ -480,26 +348,6 @@ def _composition_mu_r(R: _Real3, cc, ch, params: MultiParams) -> torch.Tensor:
     return muc
 
 
-def _velocity_r(R: _Real3, vh, ps, axis: int, mu_hat, sym, params: MultiParams, flag: _StepFlag, cc=None,
-                muc=None):
-    nh, ny, nz = R.hshape
-    kx, ky, kz = R.k
-    force = R.fwd(_rpw(RPW_MUL, ps, R.inv(mu_hat, deriv=axis)))  # F(psi F^-1(i k mu_hat))
-    if params.beta != 0.0:
-        force_c = R.fwd(_rpw(RPW_MUL, cc, R.inv(muc, deriv=axis)))
-        total = torch.empty_like(force)
-        nat.call("pfcs_axpy", nat.ptr(force), nat.ptr(force_c), nat.ptr(total), total.numel(), float(params.beta),
-                 _st())
-        force = total
-    hp = params.hydro
-    dt, rho = float(hp.pfc.dt), float(hp.rho)
-    new = torch.empty_like(vh)
-    nat.call("pfcs_hydro_vel_update_to", nat.ptr(vh), nat.ptr(new), nat.ptr(force), nh, ny, nz, nat.ptr(kx),
-             nat.ptr(ky), nat.ptr(kz), dt / rho, (dt / rho) * float(hp.gamma), -0.5 * float(sym.a0) ** 2,
-             nat.ptr(flag.t), _st())
-    return new, R.inv(new)
-
-
 def _serial_multi_step_r(fields: MultiFields, sym: SymbolTable, params: MultiParams) -> MultiFields:
     host = isinstance(fields.psi, np.ndarray)
     ps = _rdev(fields.psi)
@@ -507,11 +355,12 @@ def _serial_multi_step_r(fields: MultiFields, sym: SymbolTable, params: MultiPar
     flag = _StepFlag(ps.device)
     ph, ch, cc = _hdev(fields.psi_hat), _hdev(fields.c_hat), _rdev(fields.c)
     vs = [_rdev(v) for v in fields.v]
-    psi_hat, psi = _density_r(R, ph, ps, _grad_dot_r(R, ph, vs), sym, params, flag)
+    psi_hat, psi = _density_r(R, ph, ps, _grad_dot_r(R, ph, vs), sym, params.hydro, flag)
     c_hat, c = _composition_r(R, ch, cc, vs, sym, params, flag)
     mu_hat = _density_mu_r(R, psi, sym)
     muc = _composition_mu_r(R, c, c_hat, params) if params.beta != 0.0 else None
-    out = [_velocity_r(R, _hdev(fields.v_hat[i]), psi, i, mu_hat, sym, params, flag, c, muc) for i in range(3)]
+    out = [_velocity_r(R, _hdev(fields.v_hat[i]), psi, i, mu_hat, sym, params.hydro, flag, c, muc, params.beta)
+           for i in range(3)]
     flag.check(fields.step_index, psi_hat, c_hat, *(o[0] for o in out))
     for i in range(3):
         fields.v_hat[i], fields.v[i] = _out(out[i][0], host), _out(out[i][1], host)
@@ -541,7 +390,7 @@ def _parallel_multi_step_r(worker, st: dict, sym: SymbolTable, params: MultiPara
             adv = _rpw(RPW_ADD3, *p)
         else:
             adv = _grad_dot_r(R, ph, st["v"])
-        st["psi_hat"], st["psi"] = _density_r(R, ph, st["psi"], adv, sym, params, flag)
+        st["psi_hat"], st["psi"] = _density_r(R, ph, st["psi"], adv, sym, params.hydro, flag)
         flag.check(idx, st["psi_hat"])
         for dst in (1, 2, 3):
             worker.send_tensor(dst, TAG_PSI, st["psi"])
@@ -564,7 +413,8 @@ def _parallel_multi_step_r(worker, st: dict, sym: SymbolTable, params: MultiPara
             st["c_hat"] = worker.recv_tensor(4, TAG_CHAT, torch.empty_like(st["c_hat"]))
             muc = _composition_mu_r(R, st["c"], st["c_hat"], params)
         mu_hat = _density_mu_r(R, psi, sym)
-        st["v_hat"], st["v_own"] = _velocity_r(R, st["v_hat"], psi, i, mu_hat, sym, params, flag, st.get("c"), muc)
+        st["v_hat"], st["v_own"] = _velocity_r(R, st["v_hat"], psi, i, mu_hat, sym, params.hydro, flag, st.get("c"),
+                                                muc, params.beta)
         flag.check(idx, st["v_hat"])
         dsts = (0, 4) + ((5 + i,) if G == 8 else ())
         for dst in dsts:

@@ -204,3 +204,61 @@ def test_free_energy_full_matches_oracle(pkg):
     psi = (-0.3 + 0.05 * rng.standard_normal(grid.shape)).astype(np.complex128)
     want = ora.free_energy(ora.fft_nd(psi), ora.symbols(grid.n, grid.length, EPS, 2.0), grid.cell_volume)
     assert free_energy_full(psi, sym, grid) == pytest.approx(want, rel=1e-12)
+
+
+def _half(x):
+    return np.fft.rfftn(np.real(x), axes=(1, 2, 0))
+
+
+def test_serial_hydro_r2c_vs_reference_golden(pkg, golden):
+    """Real fields (R2C path) vs the reference's 10-step golden run: same
+    tolerances as the C2C path."""
+    from paper_2603_26818_b200.hydro import HydroFields, serial_hydro_step
+
+    g = golden("hydro16")
+    grid = fcc_grid(pkg, 16)
+    p = params(pkg, a0=2.0)
+    sym = pkg.make_symbols(grid, EPS, a0=2.0)
+    psi0 = np.real(g["psi0"]).astype(np.float64)
+    z = np.zeros((16,) * 3)
+    f = HydroFields(psi_hat=_half(psi0), psi=psi0.copy(), v_hat=[_half(z) for _ in range(3)],
+                    v=[z.copy() for _ in range(3)])
+    for _ in range(10):
+        serial_hydro_step(f, sym, p)
+    assert f.psi.dtype == np.float64 and f.psi_hat.shape == (9, 16, 16)
+    assert rel_inf(f.psi, g["psi"].real) <= 1e-12
+    assert rel_inf(f.psi_hat, g["psi_hat"][:9]) <= 1e-12
+    for i in range(3):
+        assert rel_inf(f.v[i], g[f"v{i + 1}"].real) <= 1e-9
+
+
+def test_parallel_four_roles_r2c_equal_serial_bitwise(pkg, golden):
+    import torch
+
+    from paper_2603_26818_b200.hydro import HydroFields, parallel_hydro_step, serial_hydro_step
+
+    g = golden("hydro16")
+    grid = fcc_grid(pkg, 16)
+    p = params(pkg, a0=2.0)
+    sym = pkg.make_symbols(grid, EPS, a0=2.0)
+    psi0 = np.real(g["psi0"]).astype(np.float64)
+    z = np.zeros((16,) * 3)
+    f = HydroFields(psi_hat=_half(psi0), psi=psi0.copy(), v_hat=[_half(z) for _ in range(3)],
+                    v=[z.copy() for _ in range(3)])
+    for _ in range(6):
+        serial_hydro_step(f, sym, p)
+
+    def body(w):
+        d = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()  # noqa: E731
+        if w.rank == 0:
+            st = {"psi_hat": d(_half(psi0)), "psi": d(psi0), "v": [d(z) for _ in range(3)], "step_index": 0}
+        else:
+            st = {"v_hat": d(_half(z)), "psi": d(z), "step_index": 0}
+        for _ in range(6):
+            parallel_hydro_step(w, st, sym, p)
+        return (st["psi"] if w.rank == 0 else st["v_own"]).cpu().numpy()
+
+    res = pkg.spawn_group(4, body)
+    np.testing.assert_array_equal(res[0], f.psi)
+    for i in range(3):
+        np.testing.assert_array_equal(res[i + 1], f.v[i])
