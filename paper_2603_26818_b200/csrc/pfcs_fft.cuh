@@ -27,6 +27,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 namespace pfcs {
 
 typedef long long i64;
@@ -351,11 +353,17 @@ __device__ __forceinline__ void fft_pass(double2 (&v)[R], int j, WS sl,
       const int k = b & (Ns - 1);
       const int base = (b / Ns) * Ns * r + k;
 #pragma unroll
-      for (int q = 0; q < r; ++q) ws_ref(sl, base + q * Ns) = v[s + q * S];
+      for (int q = 0; q < r; ++q) {
+        if constexpr (std::is_pointer_v<WS>) sl[pad_idx(base + q * Ns)] = v[s + q * S];
+        else ws_ref(sl, base + q * Ns) = v[s + q * S];
+      }
     }
     sync();
 #pragma unroll
-    for (int e = 0; e < R; ++e) v[e] = ws_ref(sl, j + P * e);
+    for (int e = 0; e < R; ++e) {
+      if constexpr (std::is_pointer_v<WS>) v[e] = sl[pad_idx(j + P * e)];
+      else v[e] = ws_ref(sl, j + P * e);
+    }
     fft_pass<N, Ns * r, FWD, TWS, TWL, R, TSM, Sync, WS>(v, j, sl, tw, sync);
   }
 }
