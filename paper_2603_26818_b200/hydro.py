@@ -415,6 +415,16 @@ class _Real3:
         return out
 
 
+def _check_half(R: _Real3, *spectra: torch.Tensor) -> None:
+    """The R2C path takes x-halved spectra: a full-grid spectrum next to a
+    real field is a representation mix-up, not something to compute on."""
+    for h in spectra:
+        if tuple(h.shape) != R.hshape or not h.is_complex():
+            raise ValueError(f"real physical fields select the R2C path, which needs x-halved complex spectra of "
+                             f"shape {R.hshape}; got {tuple(h.shape)} {h.dtype} (pass complex fields for the "
+                             f"reference's full-grid C2C representation)")
+
+
 def _rpw(kind: int, *ops: torch.Tensor, alpha: float = 0.0) -> torch.Tensor:
     out = torch.empty_like(ops[0])
     args = [nat.ptr(o) for o in ops] + [None] * (6 - len(ops))
@@ -496,10 +506,12 @@ def _serial_hydro_step_r(fields: HydroFields, sym: SymbolTable, params: HydroPar
     R = _Real3.of(ps.shape, sym, ps.device)
     flag = _StepFlag(ps.device)
     ph = _hdev(fields.psi_hat)
+    vh = [_hdev(x) for x in fields.v_hat]
+    _check_half(R, ph, *vh)
     vs = [_rdev(v) for v in fields.v]
     psi_hat, psi = _density_r(R, ph, ps, _grad_dot_r(R, ph, vs), sym, params, flag)
     mu_hat = _density_mu_r(R, psi, sym)  # shared by the three components
-    out = [_velocity_r(R, _hdev(fields.v_hat[i]), psi, i, mu_hat, sym, params, flag) for i in range(3)]
+    out = [_velocity_r(R, vh[i], psi, i, mu_hat, sym, params, flag) for i in range(3)]
     flag.check(fields.step_index, psi_hat, *(o[0] for o in out))
     fields.psi_hat, fields.psi = _out(psi_hat, host), _out(psi, host)
     for i in range(3):
@@ -519,6 +531,7 @@ def _parallel_hydro_step_r(worker, role_state: dict, sym: SymbolTable, params: H
     idx = role_state["step_index"]
     if rank == 0:
         ph = role_state["psi_hat"]
+        _check_half(R, ph)
         psi_hat, psi = _density_r(R, ph, psi0, _grad_dot_r(R, ph, role_state["v"]), sym, params, flag)
         flag.check(idx, psi_hat)
         role_state["psi_hat"], role_state["psi"] = psi_hat, psi
@@ -529,6 +542,7 @@ def _parallel_hydro_step_r(worker, role_state: dict, sym: SymbolTable, params: H
         i = rank - 1
         psi = worker.recv_tensor(0, TAG_PSI, torch.empty_like(psi0))
         role_state["psi"] = psi
+        _check_half(R, role_state["v_hat"])
         v_hat, v = _velocity_r(R, role_state["v_hat"], psi, i, _density_mu_r(R, psi, sym), sym, params, flag)
         flag.check(idx, v_hat)
         role_state["v_hat"], role_state["v_own"] = v_hat, v

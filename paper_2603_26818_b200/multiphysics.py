@@ -51,7 +51,8 @@ import torch
 
 from . import _native as nat
 from .grid import SymbolTable
-from .hydro import (HydroParams, TAG_PSI, V_TAGS, RPW_ADD3, RPW_CHNL, _dev, _Diag, _Real3, _StepFlag, _adv_term_r,
+from .hydro import (HydroParams, TAG_PSI, V_TAGS, RPW_ADD3, RPW_CHNL, _check_half, _dev, _Diag, _Real3, _StepFlag,
+                    _adv_term_r,
                     _density_mu_r, _density_r, _fft, _fft_cmul, _fft_cube, _grad_dot_r, _hdev, _ifft_deriv, _is_real,
                     _out, _raise_divergence, _rdev, _rpw, _vectors, _velocity_r)
 
@@ -354,13 +355,14 @@ def _serial_multi_step_r(fields: MultiFields, sym: SymbolTable, params: MultiPar
     R = _Real3.of(ps.shape, sym, ps.device)
     flag = _StepFlag(ps.device)
     ph, ch, cc = _hdev(fields.psi_hat), _hdev(fields.c_hat), _rdev(fields.c)
+    vh = [_hdev(x) for x in fields.v_hat]
+    _check_half(R, ph, ch, *vh)
     vs = [_rdev(v) for v in fields.v]
     psi_hat, psi = _density_r(R, ph, ps, _grad_dot_r(R, ph, vs), sym, params.hydro, flag)
     c_hat, c = _composition_r(R, ch, cc, vs, sym, params, flag)
     mu_hat = _density_mu_r(R, psi, sym)
     muc = _composition_mu_r(R, c, c_hat, params) if params.beta != 0.0 else None
-    out = [_velocity_r(R, _hdev(fields.v_hat[i]), psi, i, mu_hat, sym, params.hydro, flag, c, muc, params.beta)
-           for i in range(3)]
+    out = [_velocity_r(R, vh[i], psi, i, mu_hat, sym, params.hydro, flag, c, muc, params.beta) for i in range(3)]
     flag.check(fields.step_index, psi_hat, c_hat, *(o[0] for o in out))
     for i in range(3):
         fields.v_hat[i], fields.v[i] = _out(out[i][0], host), _out(out[i][1], host)
@@ -380,6 +382,7 @@ def _parallel_multi_step_r(worker, st: dict, sym: SymbolTable, params: MultiPara
     beta = params.beta != 0.0
     like = st.get("psi") if st.get("psi") is not None else st.get("c", st.get("v_own"))
     R = _Real3.of(tuple(like.shape), sym, like.device)
+    _check_half(R, *(st[k] for k in ("psi_hat", "c_hat", "v_hat") if k in st))
     flag = _StepFlag(like.device)
     if role == "psi":
         ph = st["psi_hat"]

@@ -218,3 +218,20 @@ def test_r2c_divergence_raises(pkg):
     r.psi[3, 4, 5] = np.inf
     with pytest.raises(DivergenceError):
         serial_multi_step(r, sym, mp)
+
+
+def test_r2c_rejects_full_grid_spectra(pkg):
+    """Real physical fields with full-grid (C2C) spectra are a representation
+    mix-up: the R2C path raises instead of computing on part of the array."""
+    from paper_2603_26818_b200.hydro import HydroFields, serial_hydro_step
+    from paper_2603_26818_b200.multiphysics import serial_multi_step
+
+    grid, sym, mp, f = setup(pkg)
+    r = to_real(f)
+    r.psi_hat = f.psi_hat  # full complex spectrum next to a real psi
+    with pytest.raises(ValueError, match="x-halved"):
+        serial_multi_step(r, sym, mp)
+    h = HydroFields(psi_hat=f.psi_hat, psi=np.real(f.psi).copy(), v_hat=[x for x in f.v_hat],
+                    v=[np.real(x).copy() for x in f.v])
+    with pytest.raises(ValueError, match="x-halved"):
+        serial_hydro_step(h, sym, mp.hydro)
