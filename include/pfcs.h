@@ -112,6 +112,14 @@ int pfcs_ipc_get_handle(const void* ptr, void* handle64);
 int pfcs_ipc_open_handle(const void* handle64, void** ptr);
 int pfcs_ipc_close(void* ptr);
 int pfcs_stream_sync(void* stream);
+/* Interprocess events (device-side ordering of the fused exchanges between
+ * processes): create an interprocess event and its 64-byte IPC handle, open
+ * a peer's handle, record on a stream, make a stream wait for an event. */
+int pfcs_ipc_event_create(void** event, void* handle64);
+int pfcs_ipc_event_open(const void* handle64, void** event);
+int pfcs_event_record(void* event, void* stream);
+int pfcs_stream_wait_event(void* stream, void* event);
+int pfcs_event_destroy(void* event);
 
 /* ---- real transforms along axis 0 (x) of a C-order array (new: R2C/C2R,
  * north-star item (1)).  rfft: real (nx, inner) -> complex (nx/2+1, inner),

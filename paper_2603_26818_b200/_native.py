@@ -56,6 +56,11 @@ _SIGS = {
     "pfcs_ipc_open_handle": [_c_p, ctypes.POINTER(_c_p)],
     "pfcs_ipc_close": [_c_p],
     "pfcs_stream_sync": [_c_p],
+    "pfcs_ipc_event_create": [ctypes.POINTER(_c_p), _c_p],
+    "pfcs_ipc_event_open": [_c_p, ctypes.POINTER(_c_p)],
+    "pfcs_event_record": [_c_p, _c_p],
+    "pfcs_stream_wait_event": [_c_p, _c_p],
+    "pfcs_event_destroy": [_c_p],
     "pfcs_rfft_x": [_c_p, _c_p, _c_i64, _c_i64, _c_p],
     "pfcs_irfft_x": [_c_p, _c_p, _c_i64, _c_i64, _c_p],
     "pfcs_pfc_cube_x": [_c_p, _c_i64, _c_i64, _c_int, _c_p, _c_p],
@@ -146,7 +151,8 @@ def check(rc: int, what: str) -> None:
 launches = 0
 trace: list | None = None
 _NO_LAUNCH = {"pfcs_version", "pfcs_last_error", "pfcs_device_count", "pfcs_energy_scratch_bytes",
-              "pfcs_plan_create", "pfcs_plan_destroy", "pfcs_plan_spectral_elems"}
+              "pfcs_plan_create", "pfcs_plan_destroy", "pfcs_plan_spectral_elems", "pfcs_ipc_event_create",
+              "pfcs_ipc_event_open", "pfcs_event_record", "pfcs_stream_wait_event", "pfcs_event_destroy"}
 
 
 def call(name: str, *args) -> None:

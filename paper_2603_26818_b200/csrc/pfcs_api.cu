@@ -395,6 +395,42 @@ int pfcs_ipc_close(void* ptr) { return check_cuda(cudaIpcCloseMemHandle(ptr), "c
 
 int pfcs_stream_sync(void* stream) { return check_cuda(cudaStreamSynchronize(S(stream)), "cudaStreamSynchronize"); }
 
+// Interprocess events: device-side ordering of the fused exchanges between
+// processes (peer.fence) — record on one process's stream, wait on another's.
+int pfcs_ipc_event_create(void** event, void* handle64) {
+  cudaEvent_t ev;
+  if (int rc = check_cuda(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming | cudaEventInterprocess),
+                          "cudaEventCreateWithFlags"))
+    return rc;
+  cudaIpcEventHandle_t h;
+  if (int rc = check_cuda(cudaIpcGetEventHandle(&h, ev), "cudaIpcGetEventHandle")) {
+    cudaEventDestroy(ev);
+    return rc;
+  }
+  memcpy(handle64, &h, sizeof(h));
+  *event = (void*)ev;
+  return PFCS_OK;
+}
+
+int pfcs_ipc_event_open(const void* handle64, void** event) {
+  cudaIpcEventHandle_t h;
+  memcpy(&h, handle64, sizeof(h));
+  cudaEvent_t ev;
+  if (int rc = check_cuda(cudaIpcOpenEventHandle(&ev, h), "cudaIpcOpenEventHandle")) return rc;
+  *event = (void*)ev;
+  return PFCS_OK;
+}
+
+int pfcs_event_record(void* event, void* stream) {
+  return check_cuda(cudaEventRecord((cudaEvent_t)event, S(stream)), "cudaEventRecord");
+}
+
+int pfcs_stream_wait_event(void* stream, void* event) {
+  return check_cuda(cudaStreamWaitEvent(S(stream), (cudaEvent_t)event, 0), "cudaStreamWaitEvent");
+}
+
+int pfcs_event_destroy(void* event) { return check_cuda(cudaEventDestroy((cudaEvent_t)event), "cudaEventDestroy"); }
+
 int pfcs_pfc_cube(void* data, int64_t n, int real, double* diag, void* stream) {
   if (n < 0) return fail(PFCS_E_ARG, "negative count");
   return launch_pfc_cube(data, n, real, diag, S(stream));

@@ -16,7 +16,8 @@ their mapping:
   handles over torch.distributed and open them (lazy peer enable);
 * `fence(worker)` — the ordering point of a fused exchange (writers done
   before readers read, readers done before the next writes): device-side
-  event waits between thread ranks, drain + barrier between processes.
+  event waits between thread ranks and between processes (interprocess
+  events + a gloo host barrier).
 """
 
 from __future__ import annotations
@@ -99,23 +100,77 @@ def map_peers(worker, buf: DeviceBuffer) -> PeerMap:
     return PeerMap([p for p, _ in infos], [])
 
 
+class _IpcFence:
+    """Per-process state of the device-ordered fence between processes: two
+    interprocess events of this rank (alternating) and every peer's two,
+    opened from their IPC handles, plus a host barrier that does not touch
+    the device (gloo: the default group if it is gloo, else a gloo group
+    over the same ranks, created collectively at the first fence)."""
+
+    def __init__(self, worker):
+        import torch.distributed as dist
+
+        lib = nat.load()
+        self.lib = lib
+        self.own, handles = [], []
+        for _ in range(2):
+            ev = ctypes.c_void_p()
+            h = ctypes.create_string_buffer(64)
+            nat.check(lib.pfcs_ipc_event_create(ctypes.byref(ev), ctypes.addressof(h)), "pfcs_ipc_event_create")
+            self.own.append(ev.value)
+            handles.append(bytes(h.raw))
+        all_h = worker.all_to_all([handles] * worker.size)
+        self.peers = []
+        for r, hs in enumerate(all_h):
+            if r == worker.rank:
+                continue
+            evs = []
+            for raw in hs:
+                ev = ctypes.c_void_p()
+                hb = ctypes.create_string_buffer(raw, 64)
+                nat.check(lib.pfcs_ipc_event_open(ctypes.addressof(hb), ctypes.byref(ev)), "pfcs_ipc_event_open")
+                evs.append(ev.value)
+            self.peers.append(evs)
+        if worker.backend == "gloo":
+            self.barrier = worker.barrier
+        else:
+            hg = dist.new_group(worker._global, backend="gloo")
+            self.barrier = lambda: dist.barrier(group=hg)
+        self.k = 0
+
+    def __call__(self) -> None:
+        st = ctypes.c_void_p(nat.stream_ptr())
+        i = self.k & 1
+        self.k += 1
+        nat.check(self.lib.pfcs_event_record(ctypes.c_void_p(self.own[i]), st), "pfcs_event_record")
+        self.barrier()
+        for evs in self.peers:
+            nat.check(self.lib.pfcs_stream_wait_event(st, ctypes.c_void_p(evs[i])), "pfcs_stream_wait_event")
+
+
 def fence(worker) -> None:
     """Order a fused exchange: every rank's work issued so far (its stores
     into the peers' receive buffers, its reads of its own) completes before
-    any rank's subsequent work does.
+    any rank's subsequent work does — on the devices, without draining:
+    each rank records an event on its stream, the ranks meet on the host, and
+    every stream waits for its peers' events, so the GPUs never idle at a
+    transpose and the host runs ahead.  Two events per rank, alternating: a
+    rank cannot re-record an event before every peer has issued its wait on
+    it (that needs the next fence's meeting).
 
-    Thread groups (one process, a GPU per thread: spawn_group) order it on
-    the devices: each rank records an event on its stream, the ranks meet on
-    the host — without draining anything — and every stream waits for its
-    peers' events, so the GPUs never idle at a transpose and the host runs
-    ahead.  Two events per rank, alternating: a rank cannot re-record an
-    event before every peer has issued its wait on it (that needs the next
-    fence's meeting).  Process groups drain the local stream and meet
-    (dist.barrier), as CUDA IPC events would need a host barrier that does
-    not synchronise the device."""
+    Thread groups (one process, a GPU per thread: spawn_group) use ordinary
+    CUDA events; process groups over the whole world use interprocess events
+    (CUDA IPC handles) and a gloo host barrier; process sub-groups drain the
+    local stream and meet (dist.barrier)."""
     if hasattr(worker, "_dist"):
-        nat.check(nat.load().pfcs_stream_sync(ctypes.c_void_p(nat.stream_ptr())), "pfcs_stream_sync")
-        worker.barrier()
+        if worker.pg is not None:
+            nat.check(nat.load().pfcs_stream_sync(ctypes.c_void_p(nat.stream_ptr())), "pfcs_stream_sync")
+            worker.barrier()
+            return
+        f = worker.__dict__.get("_pfcs_ipc_fence")
+        if f is None:
+            f = worker.__dict__.setdefault("_pfcs_ipc_fence", _IpcFence(worker))
+        f()
         return
     st = worker.__dict__.get("_pfcs_fence")
     if st is None:
