@@ -252,6 +252,11 @@ def timed(ctx, fn, steps: int, warmup: int, drain=None):
     return ctx.max_over_ranks(a.elapsed_time(b) / steps)
 
 
+KERNELS_NOTE = ("per-kernel times from a separate traced pass of the same steps (CUDA events recorded on the "
+                "launching stream around every launch); the tracing serialises launches, so the kernels sum to "
+                "a few % more than the untraced ms_per_step")
+
+
 def kernel_table(trace, steps):
     agg = {}
     for name, args, a, b in trace:
@@ -386,6 +391,7 @@ def run_fft(ctx, args, out):
                 "pipeline": "H2D of step k+1 overlaps D2H of step k (separate copy streams)",
                 "roundtrip_rel_l2": ctx.max_over_ranks(e2e_err)},
         "kernels": table,
+        "kernels_note": KERNELS_NOTE,
         "parity": {"roundtrip_rel_l2": err, "tol": 1e-12, "ok": err <= 1e-12},
     })
     return table
@@ -623,7 +629,7 @@ def run_pfc(ctx, args, n=None, steps=None, warmup=None, e2e=True):
     steps_s = 1000.0 / ms
     res = {"metric": "PFC time-steps/sec", "value": round(steps_s, 3), "unit": "steps/s",
            "ms_per_step": round(ms, 4), "config": f"3D PFC {n}^3 fp64 R2C slab, dt=0.1 eps=-0.3",
-           "kernels": table, "mass_bit_invariant": mass_ok,
+           "kernels": table, "kernels_note": KERNELS_NOTE, "mass_bit_invariant": mass_ok,
            "alg_hbm_bytes_per_step": pfc_bytes(n) / ctx.world}
     if e2e:
         res["e2e"] = pfc_e2e(ctx, st, params, distfft.Layout.Z_SLAB, host, steps)
