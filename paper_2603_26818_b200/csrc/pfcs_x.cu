@@ -27,38 +27,12 @@
 #include "pfcs_diag.cuh"
 #include "pfcs_fft.cuh"
 #include "pfcs_internal.h"
+#include "pfcs_pfcmath.cuh"
 #include "pfcs_tma.cuh"
 
 namespace pfcs {
 
 enum { MODE_R2C = 0, MODE_C2R = 1, MODE_CUBE = 2 };
-
-// exp(-2 pi i e / 16): for R = 8 the post/pre-twiddle W_N^k of element
-// k = j + P e (N = 2M = 16 P) is W_N^j * W_16^e, one table load per thread.
-__device__ __forceinline__ double2 w16(int e) {
-  constexpr double c1 = 0.92387953251128675613, s1 = 0.38268343236508977173;
-  constexpr double h = 0.70710678118654752440;
-  switch (e & 7) {
-    case 0: return make_double2(1.0, 0.0);
-    case 1: return make_double2(c1, -s1);
-    case 2: return make_double2(h, -h);
-    case 3: return make_double2(s1, -c1);
-    case 4: return make_double2(0.0, -1.0);
-    case 5: return make_double2(-s1, -c1);
-    case 6: return make_double2(-h, -h);
-    default: return make_double2(-c1, -s1);
-  }
-}
-
-// W_N^k for k = j + P e with N = 2M = 2 R P: W_N^j * W_{2R}^e = W_N^j * W_16^{e 8/R}
-template <int R>
-__device__ __forceinline__ double2 twiddle_k(const double2* __restrict__ twN, double2 wj, int j, int e, int P) {
-  if constexpr (R == 8 || R == 4) {
-    return cmul(wj, w16(e * (8 / R)));
-  } else {
-    return __ldg(&twN[j + P * e]);
-  }
-}
 
 // values per thread of the fused cube pass (A/B experiments: -DPFCS_CUBE_R,
 // -DPFCS_CUBE_TARGET = resident threads per SM the register cap aims for)

@@ -22,30 +22,10 @@
 #include "pfcs_diag.cuh"
 #include "pfcs_fft.cuh"
 #include "pfcs_internal.h"
+#include "pfcs_pfcmath.cuh"
 #include "pfcs_tma.cuh"
 
 namespace pfcs {
-
-struct PfcSym {
-  double eps, dt;
-};
-
-__device__ __forceinline__ double k2_of(double kx, double ky, double kz) {
-  return __dadd_rn(__dadd_rn(__dmul_rn(kx, kx), __dmul_rn(ky, ky)), __dmul_rn(kz, kz));
-}
-
-// returns (lap, fl(1/(1 - dt*linear)))
-__device__ __forceinline__ void pfc_symbols(double k2, double eps, double dt, double& lap,
-                                            double& rden) {
-  lap = -k2;
-  const double a = __dsub_rn(1.0, k2);
-  const double b = __dsub_rn(4.0 / 3.0, k2);
-  const double two_ring = __dmul_rn(__dmul_rn(a, a), __dmul_rn(b, b));
-  const double op = __dadd_rn(eps, two_ring);
-  const double lin = __dmul_rn(lap, op);
-  const double den = __dsub_rn(1.0, __dmul_rn(dt, lin));
-  rden = __drcp_rn(den);
-}
 
 template <int R>
 struct RegsZ {
@@ -53,9 +33,6 @@ struct RegsZ {
   double2 p[R];  // psi_hat z line
 };
 
-#ifndef PFCS_Z_TWL
-#define PFCS_Z_TWL 1  // twiddle loads per butterfly in the fused z update (B200 1024^3: 1 -> 6.46 ms, 3 -> 8.05 ms)
-#endif
 #ifndef PFCS_Z_TARGET
 #define PFCS_Z_TARGET 640  // resident threads per SM the register cap of k_pfc_z aims for (B200: 640 -> 96 regs, 5 CTAs; 1024^3 6.80 -> 6.46 ms)
 #endif
