@@ -14,7 +14,7 @@ Then the benchmarked workloads themselves:
     inverse of the scipy spectrum (not only the round trip);
   * 512^3 PFC, 10 steps vs the lean R2C restatement of pfc.py:96-128
     (oracle/ref_numpy.py:pfc_step_r2c_lean), field <= 1e-9;
-  * 1024^3 PFC (configs[2] grid): G = 1 bit-identical to G = 2 and 4 (thread
+  * 1024^3 PFC (configs[2] grid): G = 1 bit-identical to G = 2, 3 and 4 (thread
     ranks on one GPU: blocked z kernels, fused peer-scatter kernels at the
     production tiles), and 1 step vs the lean restatement when the host has
     the RAM for it.
