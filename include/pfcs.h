@@ -128,6 +128,13 @@ int pfcs_event_destroy(void* event);
  * irfft convention).  nx must be an even power of two in [4, 8192]. */
 int pfcs_rfft_x(const double* in, void* out, int64_t nx, int64_t inner, void* stream);
 int pfcs_irfft_x(const void* in, double* out, int64_t nx, int64_t inner, void* stream);
+/* rfft of f(in) with the pointwise f fused into the x pass (the R2C
+ * multiphysics transforms of hydro.py:86, 96-98): kind 0 f(x) = (x*x)*x,
+ * kind 1 f(x) = x*aux (aux: a real array of in's layout), kind 3
+ * f(x) = alpha*(x*(x*x) - x) — pfcs_real_pointwise's arithmetic, so
+ * bit-identical to that kernel followed by pfcs_rfft_x. */
+int pfcs_rfft_x_pro(const double* in, void* out, int64_t nx, int64_t inner, int kind, const double* aux,
+                    double alpha, void* stream);
 
 /* ---- fused PFC step kernels: pfc.pfc_step (pfc.py:96-128) ---------------
  * Diagnostics block `diag` (device, PFCS_DIAG_SLOTS x 4 doubles; the caller

@@ -176,6 +176,8 @@ int tune_variant(int kind, int n, int dflt) {
 int launch_real_x(const void* in, void* out, long long nx, long long inner, int mode, double* diag,
                   cudaStream_t st);
 int launch_cube_c2c(void* data, long long nx, long long inner, double* diag, cudaStream_t st);
+int launch_rfft_x_pro(const double* in, void* out, long long nx, long long inner, int kind, const double* aux,
+                      double alpha, cudaStream_t st);
 int launch_pfc_z(const double2* nl, double2* psi_hat, double2* next, long long cx, long long ny,
                  long long nz, int g_in, int g_out, const double* kx, const double* ky,
                  const double* kz, double eps, double dt, double* diag, cudaStream_t st,
@@ -295,6 +297,12 @@ int pfcs_fft_lines(const void* in, void* out, int64_t outer, int64_t n, int64_t 
   }
   return launch_strided_blocked((const double2*)in, (double2*)out, outer, (int)n, inner, g_in, g_out,
                                 forward != 0, S(stream));
+}
+
+int pfcs_rfft_x_pro(const double* in, void* out, int64_t nx, int64_t inner, int kind, const double* aux,
+                    double alpha, void* stream) {
+  if (!in || !out) return fail(PFCS_E_ARG, "null argument");
+  return launch_rfft_x_pro(in, out, nx, inner, kind, aux, alpha, S(stream));
 }
 
 int pfcs_rfft_x(const double* in, void* out, int64_t nx, int64_t inner, void* stream) {

@@ -32,7 +32,24 @@
 
 namespace pfcs {
 
-enum { MODE_R2C = 0, MODE_C2R = 1, MODE_CUBE = 2 };
+enum { MODE_R2C = 0, MODE_C2R = 1, MODE_CUBE = 2, MODE_R2C_PRO = 3 };
+__host__ __device__ constexpr bool is_r2c(int mode) { return mode == MODE_R2C || mode == MODE_R2C_PRO; }
+
+// Pointwise prologue of an R2C x pass (MODE_R2C_PRO): the real sample x of
+// the transformed field is replaced by f(x) before the transform — the
+// R2C multiphysics path's psi**3, psi * g and alpha (c^3 - c) (hydro.py:86,
+// 96-98), in pfcs_real_pointwise's arithmetic (kinds 0, 1, 3), so fused and
+// two-pass results are bit-identical and the product never reaches HBM.
+struct RPro {
+  int kind;           // 0 cube, 1 product with aux, 3 alpha (x^3 - x)
+  double alpha;
+  const double* aux;  // kind 1: the other factor, same (nx, inner) layout
+};
+__device__ __forceinline__ double rpro_apply(const RPro& p, double x, i64 idx, bool ok) {
+  if (p.kind == 0) return __dmul_rn(__dmul_rn(x, x), x);
+  if (p.kind == 1) return __dmul_rn(x, ok ? __ldg(p.aux + idx) : 0.0);
+  return __dmul_rn(p.alpha, __dsub_rn(__dmul_rn(x, __dmul_rn(x, x)), x));
+}
 
 // values per thread of the fused cube pass (A/B experiments: -DPFCS_CUBE_R,
 // -DPFCS_CUBE_TARGET = resident threads per SM the register cap aims for)
@@ -81,9 +98,9 @@ __host__ __device__ constexpr int real_ls(int m, int t) {
 // T values wide; two stages (1024-byte aligned) + the FFT workspace + bars.
 template <int M, int T, int MODE>
 struct XStage {
-  static constexpr size_t BYTES = MODE == 0 ? (size_t)2 * M * T * 8 : (size_t)(M + 1) * T * 16;
+  static constexpr size_t BYTES = is_r2c(MODE) ? (size_t)2 * M * T * 8 : (size_t)(M + 1) * T * 16;
   static constexpr size_t PADDED = (BYTES + 1023) / 1024 * 1024;
-  static constexpr int ROWS = MODE == 0 ? 2 * M : M;          // rows moved by the tiled map
+  static constexpr int ROWS = is_r2c(MODE) ? 2 * M : M;       // rows moved by the tiled map
   static constexpr int BR = ROWS < 256 ? ROWS : 256;          // rows per box
   static constexpr int NB = ROWS / BR;
   static constexpr size_t SMEM = 2 * PADDED + (size_t)T * real_ls(M, T) * 16 + 16 + 1024;
@@ -93,13 +110,13 @@ template <int M, int T, int ST, int MODE>
 __global__ void __launch_bounds__(T*(M / real_R(M, MODE)),
                                   min_blocks(T*(M / real_R(M, MODE)), ST == 3 ? 512 : (MODE == 2 ? PFCS_CUBE_TARGET : (ST == 2 ? 640 : 768))))
     k_real_x(const void* in_, void* out_, i64 inner, const double2* __restrict__ twN, double scale,
-             double* diag, const __grid_constant__ TmaPair tm) {
+             double* diag, const __grid_constant__ TmaPair tm, RPro rp = RPro{}) {
   pdl_wait();
   constexpr int R = real_R(M, MODE);
   constexpr int P = M / R;
   constexpr int LS = real_ls(M, T);
   constexpr bool TMA = ST == 3;
-  constexpr bool SMIR = TMA && MODE != MODE_R2C;  // mirror rows read from the TMA stage
+  constexpr bool SMIR = TMA && !is_r2c(MODE);  // mirror rows read from the TMA stage
   constexpr bool LMIR = !TMA && late_mirror(MODE);
   using XS = XStage<M, T, MODE>;
   extern __shared__ unsigned char xraw[];
@@ -118,13 +135,18 @@ __global__ void __launch_bounds__(T*(M / real_R(M, MODE)),
   auto load = [&](i64 tile, RegsX<R>& r) {
     const i64 i = tile * T + t;
     const bool ok = i < inner;
-    if (MODE == MODE_R2C) {
+    if (is_r2c(MODE)) {
       const double* in = (const double*)in_;
 #pragma unroll
       for (int e = 0; e < R; ++e) {
         const i64 m = j + P * e;
         r.v[e] = ok ? make_double2(in[(2 * m) * inner + i], in[(2 * m + 1) * inner + i])
                     : make_double2(0.0, 0.0);
+        if constexpr (MODE == MODE_R2C_PRO) {
+          if (ok)
+            r.v[e] = make_double2(rpro_apply(rp, r.v[e].x, (2 * m) * inner + i, true),
+                                  rpro_apply(rp, r.v[e].y, (2 * m + 1) * inner + i, true));
+        }
       }
     } else {
       const double2* in = (const double2*)in_;
@@ -145,7 +167,7 @@ __global__ void __launch_bounds__(T*(M / real_R(M, MODE)),
     const i64 i = tile * T + t;
     const bool ok = i < inner;
     double2* v = r.v;
-    if (MODE != MODE_R2C) {
+    if (!is_r2c(MODE)) {
       // Z'[k] = (X_k + conj X_{M-k}) + i W_N^{-k} (X_k - conj X_{M-k});
       // Im X_0 and Im X_M are ignored (numpy irfft convention)
       double2 wl[LMIR ? R : 1];
@@ -263,11 +285,11 @@ __global__ void __launch_bounds__(T*(M / real_R(M, MODE)),
       const int i0 = (int)(tile * T);
       unsigned char* dst = (unsigned char*)(sidx ? stage1 : stage0);
       mbar_expect_tx(&bars[sidx], (unsigned)XS::BYTES);
-      constexpr int W = MODE == MODE_R2C ? 8 : 16;  // bytes per stage element
+      constexpr int W = is_r2c(MODE) ? 8 : 16;  // bytes per stage element
 #pragma unroll
       for (int b = 0; b < XS::NB; ++b)
-        tma_load_2d(dst + (size_t)b * XS::BR * T * W, &tm.a, &bars[sidx], (MODE == MODE_R2C ? 1 : 2) * i0, b * XS::BR);
-      if (MODE != MODE_R2C) tma_load_2d(dst + (size_t)M * T * W, &tm.b, &bars[sidx], 2 * i0, M);
+        tma_load_2d(dst + (size_t)b * XS::BR * T * W, &tm.a, &bars[sidx], (is_r2c(MODE) ? 1 : 2) * i0, b * XS::BR);
+      if (!is_r2c(MODE)) tma_load_2d(dst + (size_t)M * T * W, &tm.b, &bars[sidx], 2 * i0, M);
     };
     if (tid == 0) {
       mbar_init(&bars[0], 1);
@@ -289,7 +311,7 @@ __global__ void __launch_bounds__(T*(M / real_R(M, MODE)),
       mbar_wait(&bars[sidx], (unsigned)((it >> 1) & 1));
       cur = sidx ? stage1 : stage0;
       RegsX<R> r;
-      if (MODE == MODE_R2C) {
+      if (is_r2c(MODE)) {
         // rows 2m and 2m+1 of a T-double stage row pair sit in opposite
         // halves of the 32 banks when T = 8: odd-j threads read their odd
         // row first, so each load instruction touches both halves (2
@@ -302,6 +324,12 @@ __global__ void __launch_bounds__(T*(M / real_R(M, MODE)),
           const double a = sd[(2 * m + sw) * T + t];
           const double b = sd[(2 * m + 1 - sw) * T + t];
           r.v[e] = sw ? make_double2(b, a) : make_double2(a, b);
+          if constexpr (MODE == MODE_R2C_PRO) {
+            const i64 i = tile * T + t;
+            const bool ok = i < inner;
+            r.v[e] = make_double2(rpro_apply(rp, r.v[e].x, (2 * m) * inner + i, ok),
+                                  rpro_apply(rp, r.v[e].y, (2 * m + 1) * inner + i, ok));
+          }
         }
       } else {
 #pragma unroll
@@ -641,7 +669,7 @@ template <int M, int T, int MODE>
 static bool x_tmaps(TmaPair* tm, const void* in, i64 inner) {
   if (2 * inner >= (1LL << 31)) return false;
   using XS = XStage<M, T, MODE>;
-  if (MODE == MODE_R2C) {
+  if (is_r2c(MODE)) {
     if (inner % 2) return false;  // row stride must be a multiple of 16 bytes
     const unsigned long long dims[2] = {(unsigned long long)inner, (unsigned long long)(2 * M)};
     const unsigned long long str[1] = {(unsigned long long)inner * 8};
@@ -656,7 +684,7 @@ static bool x_tmaps(TmaPair* tm, const void* in, i64 inner) {
 }
 
 template <int M, int MODE>
-static int real_x_m(const void* in, void* out, i64 inner, double* diag, cudaStream_t st) {
+static int real_x_m(const void* in, void* out, i64 inner, double* diag, cudaStream_t st, RPro rp = RPro{}) {
   const double2* twN = twiddles(2 * M);
   if (!twN) return PFCS_E_CUDA;
   constexpr int PM = M / real_R(M, MODE);
@@ -680,13 +708,13 @@ static int real_x_m(const void* in, void* out, i64 inner, double* diag, cudaStre
       // 512^3 0.79 -> 0.67; C2R 1024^3 4.96 -> 4.75; R2C 512^3 0.57 -> 0.50 but
       // 1024^3 4.94 -> 5.58 (64-byte real rows, one CTA per SM), so R2C keeps
       // the register pipeline from M = 512 up.
-      if constexpr (XStage<M, T, MODE>::SMEM <= 227 * 1024 && (MODE != MODE_R2C || (T >= 2 && M <= 256))) {
+      if constexpr (XStage<M, T, MODE>::SMEM <= 227 * 1024 && (!is_r2c(MODE) || (T >= 2 && M <= 256))) {
         if (tma_enabled() && x_tmaps<M, T, MODE>(&tm, in, inner)) {
           constexpr size_t smem = XStage<M, T, MODE>::SMEM;
           int grid = 0;
           if (int rc = persistent_grid((const void*)k_real_x<M, T, 3, MODE>, T * P, smem, ntiles, &grid)) return rc;
           launch_pdl(k_real_x<M, T, 3, MODE>, dim3(grid), dim3(T * P), smem, st, in, out, inner, twN,
-                     1.0 / (double)(2 * M), diag, tm);
+                     1.0 / (double)(2 * M), diag, tm, rp);
           return check_launch("k_real_x(tma)");
         }
       }
@@ -694,7 +722,7 @@ static int real_x_m(const void* in, void* out, i64 inner, double* diag, cudaStre
       int grid = 0;
       if (int rc = persistent_grid((const void*)k_real_x<M, T, ST, MODE>, T * P, smem, ntiles, &grid)) return rc;
       launch_pdl(k_real_x<M, T, ST, MODE>, dim3(grid), dim3(T * P), smem, st, in, out, inner, twN,
-                 1.0 / (double)(2 * M), diag, tm);
+                 1.0 / (double)(2 * M), diag, tm, rp);
       return check_launch("k_real_x");
     }
   });
@@ -742,6 +770,27 @@ int launch_real_x(const void* in, void* out, long long nx, long long inner, int 
       if (rc != 1) return rc;                                                         \
     }                                                                                 \
     return real_x_m<MM, MODE_CUBE>(in, out, inner, diag, st);
+    PFCS_M_CASES(PFCS_CASE)
+#undef PFCS_CASE
+    default:
+      break;
+  }
+  return fail(PFCS_E_UNSUPPORTED, "unsupported nx");
+}
+
+// R2C x pass with a pointwise prologue (kinds of pfcs_real_pointwise 0, 1, 3)
+int launch_rfft_x_pro(const double* in, void* out, long long nx, long long inner, int kind, const double* aux,
+                      double alpha, cudaStream_t st) {
+  if (inner <= 0) return PFCS_OK;
+  if (kind != 0 && kind != 1 && kind != 3) return fail(PFCS_E_ARG, "rfft_x prologue kind must be 0, 1 or 3");
+  if (kind == 1 && !aux) return fail(PFCS_E_ARG, "rfft_x product prologue needs aux");
+  if (!is_pow2(nx) || nx < 4 || nx > 8192)
+    return fail(PFCS_E_UNSUPPORTED, "real x transforms need a power-of-two nx in [4, 8192]");
+  const RPro rp{kind, alpha, aux};
+  switch (nx / 2) {
+#define PFCS_CASE(MM) \
+  case MM:            \
+    return real_x_m<MM, MODE_R2C_PRO>(in, out, inner, nullptr, st, rp);
     PFCS_M_CASES(PFCS_CASE)
 #undef PFCS_CASE
     default:

@@ -339,6 +339,7 @@ def free_energy_full(psi, sym: SymbolTable, grid: GridSpec) -> float:
 # representation of the hydro / multiphysics fields (multiphysics.py doc).
 
 RPW_CUBE, RPW_MUL, RPW_ADV3, RPW_CHNL, RPW_ADD3 = 0, 1, 2, 3, 4  # pfcs_real_pointwise kinds
+_R2C_PRO = __import__("os").environ.get("PFCS_R2C_PRO", "1") != "0"  # fused prologues (A/B switch)
 
 
 def _is_real(x) -> bool:
@@ -387,11 +388,22 @@ class _Real3:
             cache[key] = _Real3(shape, sym, device)
         return cache[key]
 
-    def fwd(self, x: torch.Tensor) -> torch.Tensor:
+    def fwd(self, x: torch.Tensor, kind: int | None = None, aux: torch.Tensor | None = None,
+            alpha: float = 0.0) -> torch.Tensor:
+        """F[x], or F[f(x)] with f a pfcs_real_pointwise kind (0 cube, 1 x*aux,
+        3 alpha (x^3 - x)) fused into the first (x) pass (PFCS_R2C_PRO=0:
+        the product in its own pass, bit-identical)."""
         nx, ny, nz = self.shape
         out = torch.empty(self.hshape, dtype=torch.complex128, device=x.device)
         st = nat.stream_ptr()
-        nat.call("pfcs_rfft_x", nat.ptr(x), nat.ptr(out), nx, ny * nz, st)
+        if kind is not None and not _R2C_PRO:
+            x = _rpw(kind, x, *([aux] if aux is not None else []), alpha=alpha)
+            kind = None
+        if kind is None:
+            nat.call("pfcs_rfft_x", nat.ptr(x), nat.ptr(out), nx, ny * nz, st)
+        else:
+            nat.call("pfcs_rfft_x_pro", nat.ptr(x), nat.ptr(out), nx, ny * nz, kind,
+                     nat.ptr(aux) if aux is not None else None, float(alpha), st)
         if ny > 1:
             nat.call("pfcs_fft_axis_c2c", nat.ptr(out), nat.ptr(out), self.nh, ny, nz, 1, 1, st)
         if nz > 1:
@@ -461,7 +473,7 @@ def _adv_term_r(R: _Real3, x_hat: torch.Tensor, axis: int, v_axis: torch.Tensor)
 def _density_r(R: _Real3, ph, ps, adv, sym, hp: HydroParams, flag: _StepFlag):
     nh, ny, nz = R.hshape
     kx, ky, kz = R.k
-    nl_hat = R.fwd(_rpw(RPW_CUBE, ps))
+    nl_hat = R.fwd(ps, RPW_CUBE)
     adv_hat = R.fwd(adv)
     new = torch.empty_like(ph)
     nat.call("pfcs_hydro_psi_update_to", nat.ptr(ph), nat.ptr(new), nat.ptr(nl_hat), nat.ptr(adv_hat), nh, ny, nz,
@@ -473,7 +485,7 @@ def _density_r(R: _Real3, ph, ps, adv, sym, hp: HydroParams, flag: _StepFlag):
 def _density_mu_r(R: _Real3, ps, sym) -> torch.Tensor:
     nh, ny, nz = R.hshape
     kx, ky, kz = R.k
-    nl_hat = R.fwd(_rpw(RPW_CUBE, ps))
+    nl_hat = R.fwd(ps, RPW_CUBE)
     f_hat = R.fwd(ps)
     mu = torch.empty_like(nl_hat)
     nat.call("pfcs_hydro_mu", nat.ptr(nl_hat), nat.ptr(f_hat), nat.ptr(mu), nh, ny, nz, nat.ptr(kx), nat.ptr(ky),
@@ -485,9 +497,9 @@ def _velocity_r(R: _Real3, vh, ps, axis: int, mu_hat, sym, hp: HydroParams, flag
                 muc=None, beta: float = 0.0):
     nh, ny, nz = R.hshape
     kx, ky, kz = R.k
-    force = R.fwd(_rpw(RPW_MUL, ps, R.inv(mu_hat, deriv=axis)))  # F(psi F^-1(i k mu_hat))
+    force = R.fwd(R.inv(mu_hat, deriv=axis), RPW_MUL, ps)  # F(psi F^-1(i k mu_hat))
     if beta != 0.0:
-        force_c = R.fwd(_rpw(RPW_MUL, cc, R.inv(muc, deriv=axis)))
+        force_c = R.fwd(R.inv(muc, deriv=axis), RPW_MUL, cc)
         total = torch.empty_like(force)
         nat.call("pfcs_axpy", nat.ptr(force), nat.ptr(force_c), nat.ptr(total), total.numel(), float(beta),
                  nat.stream_ptr())

@@ -331,7 +331,7 @@ def _composition_r(R: _Real3, ch, cc, v, sym, params: MultiParams, flag: _StepFl
     nh, ny, nz = R.hshape
     kx, ky, kz = R.k
     adv_hat = R.fwd(_grad_dot_r(R, ch, v))
-    f_hat = R.fwd(_rpw(RPW_CHNL, cc, alpha=params.alpha))
+    f_hat = R.fwd(cc, RPW_CHNL, alpha=params.alpha)
     new = torch.empty_like(ch)
     nat.call("pfcs_ch_update_to", nat.ptr(ch), nat.ptr(new), nat.ptr(f_hat), nat.ptr(adv_hat), nh, ny, nz, nat.ptr(kx),
              nat.ptr(ky), nat.ptr(kz), float(params.mobility), float(params.kappa), float(params.hydro.pfc.dt),
@@ -342,7 +342,7 @@ def _composition_r(R: _Real3, ch, cc, v, sym, params: MultiParams, flag: _StepFl
 def _composition_mu_r(R: _Real3, cc, ch, params: MultiParams) -> torch.Tensor:
     nh, ny, nz = R.hshape
     kx, ky, kz = R.k
-    fc_hat = R.fwd(_rpw(RPW_CHNL, cc, alpha=params.alpha))
+    fc_hat = R.fwd(cc, RPW_CHNL, alpha=params.alpha)
     muc = torch.empty_like(fc_hat)
     nat.call("pfcs_ch_mu", nat.ptr(fc_hat), nat.ptr(ch), nat.ptr(muc), nh, ny, nz, nat.ptr(kx), nat.ptr(ky),
              nat.ptr(kz), float(params.kappa), _st())

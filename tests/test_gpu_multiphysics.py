@@ -235,3 +235,45 @@ def test_r2c_rejects_full_grid_spectra(pkg):
                     v=[np.real(x).copy() for x in f.v])
     with pytest.raises(ValueError, match="x-halved"):
         serial_hydro_step(h, sym, mp.hydro)
+
+
+PRO_CHILD = r"""
+import sys, numpy as np
+sys.path.insert(0, {root!r})
+sys.path.insert(0, {tests!r})
+import paper_2603_26818_b200 as pkg
+from test_gpu_multiphysics import setup, to_real
+from paper_2603_26818_b200.multiphysics import serial_multi_step
+out = {{}}
+for beta in (0.0, 0.5):
+    grid, sym, mp, f = setup(pkg, n=32, beta=beta)
+    r = to_real(f)
+    for _ in range(3):
+        serial_multi_step(r, sym, mp)
+    for k in ("psi", "c", "psi_hat", "c_hat"):
+        out[f"{{beta}}_{{k}}"] = getattr(r, k)
+    for i in range(3):
+        out[f"{{beta}}_v{{i}}"] = r.v[i]
+np.savez({path!r}, **out)
+"""
+
+
+def test_r2c_fused_prologues_bit_identical(pkg, tmp_path):
+    """The pointwise prologues fused into the R2C x pass (psi^3, psi * g,
+    alpha (c^3 - c): pfcs_rfft_x_pro) reproduce the two-pass form
+    (pfcs_real_pointwise + pfcs_rfft_x) bit for bit."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    here = Path(__file__).resolve().parent
+    res = {}
+    for flag in ("0", "1"):
+        path = str(tmp_path / f"pro{flag}.npz")
+        env = dict(os.environ, PFCS_R2C_PRO=flag)
+        subprocess.run([sys.executable, "-c", PRO_CHILD.format(root=str(here.parent), tests=str(here), path=path)],
+                       check=True, env=env, timeout=600)
+        res[flag] = np.load(path)
+    for k in res["0"].files:
+        np.testing.assert_array_equal(res["0"][k], res["1"][k])

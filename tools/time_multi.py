@@ -1,5 +1,6 @@
-"""Time the serial multiphysics step (5 fields, 512^3 default) in isolation:
-    python tools/time_multi.py [n] [steps]"""
+"""Time the 512^3 serial R2C multiphysics step (bench.py's configs[4] line)
+on cuda:0:   python tools/time_multi.py [n] [steps]   (env switches apply)."""
+import os
 import sys
 from pathlib import Path
 
@@ -15,22 +16,20 @@ def main():
     from paper_2603_26818_b200.pfc import PfcParams
 
     n = int(sys.argv[1]) if len(sys.argv) > 1 else 512
-    steps = int(sys.argv[2]) if len(sys.argv) > 2 else 6
+    steps = int(sys.argv[2]) if len(sys.argv) > 2 else 5
+    torch.cuda.set_device(0)
     dev = torch.device("cuda", 0)
     grid = GridSpec((n,) * 3, (2 * np.pi * np.sqrt(3) * (n // 8),) * 3)
     hp = hydro.HydroParams(pfc=PfcParams(eps=-0.3, dt=0.1), rho=1.0, gamma=1.0, a0=2.0)
     mp = mpx.MultiParams(hydro=hp, mobility=1.0, kappa=1.0, alpha=1.0, beta=0.0)
     sym = make_symbols(grid, -0.3, a0=2.0)
-    gen = torch.Generator(device=dev).manual_seed(11)
-
-    def field(scale, base=0.0):
-        x = torch.rand((n,) * 3, dtype=torch.float64, device=dev, generator=gen)
-        return (base + scale * (x - 0.5)).to(torch.complex128)
-
-    psi, c = field(0.02, -0.3), field(0.2)
-    zeros = torch.zeros((n,) * 3, dtype=torch.complex128, device=dev)
-    f = mpx.MultiFields(psi_hat=hydro._fft(psi, True), psi=psi, c_hat=hydro._fft(c, True), c=c,
-                        v_hat=[zeros.clone() for _ in range(3)], v=[zeros.clone() for _ in range(3)])
+    g = torch.Generator(device=dev).manual_seed(11)
+    psi = -0.3 + 0.02 * (torch.rand((n,) * 3, dtype=torch.float64, device=dev, generator=g) - 0.5)
+    c = 0.2 * (torch.rand((n,) * 3, dtype=torch.float64, device=dev, generator=g) - 0.5)
+    R = mpx._Real3.of((n,) * 3, sym, dev)
+    z = torch.zeros_like(psi)
+    f = mpx.MultiFields(psi_hat=R.fwd(psi), psi=psi, c_hat=R.fwd(c), c=c, v_hat=[R.fwd(z) for _ in range(3)],
+                        v=[z.clone() for _ in range(3)])
     for _ in range(2):
         mpx.serial_multi_step(f, sym, mp)
     torch.cuda.synchronize()
@@ -40,7 +39,8 @@ def main():
         mpx.serial_multi_step(f, sym, mp)
     b.record()
     torch.cuda.synchronize()
-    print(f"multiphysics {n}^3 serial: {a.elapsed_time(b) / steps:.2f} ms/step")
+    print(f"multiphysics {n}^3: {a.elapsed_time(b) / steps:.3f} ms/step",
+          {k: v for k, v in os.environ.items() if k.startswith("PFCS_")})
 
 
 if __name__ == "__main__":
