@@ -23,6 +23,7 @@ step; results equal the C2C path to rounding.  numpy inputs are accepted
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass, field as dataclass_field
 
 import numpy as np
@@ -339,7 +340,7 @@ def free_energy_full(psi, sym: SymbolTable, grid: GridSpec) -> float:
 # representation of the hydro / multiphysics fields (multiphysics.py doc).
 
 RPW_CUBE, RPW_MUL, RPW_ADV3, RPW_CHNL, RPW_ADD3 = 0, 1, 2, 3, 4  # pfcs_real_pointwise kinds
-_R2C_PRO = __import__("os").environ.get("PFCS_R2C_PRO", "1") != "0"  # fused prologues (A/B switch)
+_R2C_PRO = os.environ.get("PFCS_R2C_PRO", "1") != "0"  # fused prologues (A/B switch)
 
 
 def _is_real(x) -> bool:

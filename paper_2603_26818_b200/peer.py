@@ -138,6 +138,13 @@ class _IpcFence:
             self.barrier = lambda: dist.barrier(group=hg)
         self.k = 0
 
+    def __del__(self):
+        try:
+            for ev in self.own + [e for evs in self.peers for e in evs]:
+                self.lib.pfcs_event_destroy(ctypes.c_void_p(ev))
+        except Exception:  # interpreter shutdown
+            pass
+
     def __call__(self) -> None:
         st = ctypes.c_void_p(nat.stream_ptr())
         i = self.k & 1
