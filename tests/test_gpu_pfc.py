@@ -321,3 +321,32 @@ def test_peer_default_with_non_pow2_y(pkg, n, real):
     ref = pkg.spawn_group(1, body)[0]
     got = pkg.spawn_group(2, body)[0]
     np.testing.assert_array_equal(got, ref)
+
+
+def test_local_is_read_only_and_touch_invalidates(pkg):
+    """DistField.local is a read-only host copy (an in-place edit would be
+    silently lost, so it raises); editing .dev in place + touch() makes the
+    PFC engine rebuild its prepared inverse."""
+    from paper_2603_26818_b200 import distfft, pfc
+
+    n = (16, 16, 16)
+    grid = pkg.GridSpec(n, pfc.default_domain_length(n))
+    psi0 = pfc.initial_field("constant_plus_noise", grid, seed=2, noise_amplitude=0.05)
+
+    def body(w):
+        st = make_state(pkg, w, grid, psi0, real=True)
+        with pytest.raises(ValueError):
+            st.psi_hat.local[0, 0, 0] = 1.0
+        pfc.pfc_run(st, pfc.PfcParams(), 3)  # leaves a prepared inverse of psi_hat
+        ref = make_state(pkg, w, grid, psi0, real=True)
+        pfc.pfc_run(ref, pfc.PfcParams(), 3)
+        # scale both in place: one through .dev + touch(), one by assignment
+        st.psi_hat.dev.mul_(0.5)
+        st.psi_hat.touch()
+        ref.psi_hat.local = np.asarray(ref.psi_hat.local) * 0.5
+        pfc.pfc_run(st, pfc.PfcParams(), 2)
+        pfc.pfc_run(ref, pfc.PfcParams(), 2)
+        return st.psi_hat.local.copy(), ref.psi_hat.local.copy()
+
+    a, b = pkg.spawn_group(1, body)[0]
+    np.testing.assert_array_equal(a, b)
