@@ -383,3 +383,31 @@ def test_pfc_1024_step_vs_lean_restatement(torch_cuda, pfc1024):
     torch.cuda.empty_cache()
     want = ora.pfc_step_r2c_lean(spec0.cpu().numpy(), grid.n, grid.length, -0.3, 0.1, workers=WORKERS)
     assert rel_l2(got, want) <= 1e-12
+
+
+@pytest.mark.parametrize("nx,inner", [(512, 7104), (1024, 3600), (64, 300)])
+@pytest.mark.parametrize("kind", [0, 1, 3])
+def test_rfft_x_prologue_production(torch_cuda, nx, inner, kind):
+    """pfcs_rfft_x_pro (the R2C multiphysics transforms' fused psi^3, psi*g,
+    alpha (c^3 - c)) at the production tiles (TMA path at nx 512, register
+    path at 1024, small-tile fallback at 64): bit-identical to
+    pfcs_real_pointwise followed by pfcs_rfft_x, and vs scipy <= 1e-12."""
+    import scipy.fft as sfft
+
+    torch, nat = torch_cuda, _nat()
+    rng = np.random.default_rng(nx + kind)
+    x = -0.3 + 0.2 * rng.standard_normal((nx, inner))
+    g = rng.standard_normal((nx, inner))
+    xd, gd = _to(torch, x), _to(torch, g)
+    st = nat.stream_ptr()
+    fused = torch.empty((nx // 2 + 1, inner), dtype=torch.complex128, device="cuda")
+    nat.call("pfcs_rfft_x_pro", nat.ptr(xd), nat.ptr(fused), nx, inner, kind, nat.ptr(gd) if kind == 1 else None,
+             0.7, st)
+    pw = torch.empty_like(xd)
+    nat.call("pfcs_real_pointwise", kind, nat.ptr(xd), nat.ptr(gd) if kind == 1 else None, None, None, None, None,
+             nat.ptr(pw), pw.numel(), 0.7, st)
+    two = torch.empty_like(fused)
+    nat.call("pfcs_rfft_x", nat.ptr(pw), nat.ptr(two), nx, inner, st)
+    assert torch.equal(fused, two)
+    f = {0: x * x * x, 1: x * g, 3: 0.7 * (x * (x * x) - x)}[kind]
+    assert rel_l2(fused.cpu().numpy(), sfft.rfft(f, axis=0, workers=WORKERS)) <= TOL
