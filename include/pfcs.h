@@ -233,6 +233,19 @@ int pfcs_ch_update(void* c_hat, const void* f_hat, const void* adv_hat, int64_t 
 int pfcs_ch_mu(const void* f_hat, const void* c_hat, void* out, int64_t n0, int64_t n1, int64_t n2,
                const double* kx, const double* ky, const double* kz, double kappa, void* stream);
 int pfcs_add3(const void* a, const void* b, const void* c, void* out, int64_t n, void* stream);
+/* A spectral update fused into the first (z) pass of the inverse transform
+ * that follows it (hydro.py:86-89, 103-105 and the composition update, as
+ * k_pfc_z does for PFC): reads the old state, writes the new state to
+ * state_out (may alias state_in) and the inverse z transform of the new
+ * state to zout, one pass.  kind 0 psi: aux = nl_hat, aux2 = adv_hat (or
+ * NULL), c0 = eps, c1 = dt; kind 1 velocity: aux = force, c0 = dt/rho,
+ * c1 = (dt/rho) gamma, c2 = -a0^2/2; kind 2 composition: aux = f_hat,
+ * aux2 = adv_hat, c0 = mobility, c1 = kappa, c2 = dt.  Arithmetic of
+ * pfcs_hydro_psi_update_to / pfcs_hydro_vel_update_to / pfcs_ch_update_to
+ * followed by pfcs_fft_axis_c2c(axis 2, inverse): bit-identical. */
+int pfcs_update_zinv(int kind, const void* state_in, const void* aux, const void* aux2, void* state_out, void* zout,
+                     int64_t n0, int64_t n1, int64_t n2, const double* kx, const double* ky, const double* kz,
+                     double c0, double c1, double c2, double* diag, void* stream);
 /* Real-field pointwise operators of the R2C multiphysics path (physical
  * fields real: 8-byte samples), numpy evaluation order, no FMA; all operand
  * pointers 16-byte aligned, unused ones may be NULL:

@@ -229,6 +229,45 @@ int pfcs_fft_axis_c2c(const void* in, void* out, int64_t n0, int64_t n1, int64_t
   return launch_strided_c2c((const double2*)in, (double2*)out, outer, (int)n, inner, forward != 0, S(stream));
 }
 
+int pfcs_update_zinv(int kind, const void* state_in, const void* aux, const void* aux2, void* state_out, void* zout,
+                     int64_t n0, int64_t n1, int64_t n2, const double* kx, const double* ky, const double* kz,
+                     double c0, double c1, double c2, double* diag, void* stream) {
+  if (kind < 0 || kind > 2) return fail(PFCS_E_ARG, "update kind must be 0 (psi), 1 (velocity) or 2 (composition)");
+  if (!state_in || !aux || !state_out || !zout || !kx || !ky || !kz) return fail(PFCS_E_ARG, "null argument");
+  if (zout == state_in || zout == state_out || zout == aux || (aux2 && zout == aux2))
+    return fail(PFCS_E_ARG, "zout must not alias the state or the operands");
+  if (n0 < 0 || n1 < 0 || n2 < 0) return fail(PFCS_E_ARG, "negative extent");
+  if (n0 * n1 * n2 == 0) return PFCS_OK;
+  Pro p{};
+  p.kind = PRO_UPD_PSI + kind;
+  p.aux = aux;
+  p.aux2 = kind == 1 ? nullptr : aux2;
+  p.out2 = state_out;
+  p.axis = 2;
+  p.n1 = (int)n1;
+  p.n2 = (int)n2;
+  p.kx = kx;
+  p.ky = ky;
+  p.kz = kz;
+  p.c0 = c0;
+  p.c1 = c1;
+  p.c2 = c2;
+  p.diag = diag;
+  if (n2 > 1) {
+    const int rc = launch_lines_pro((const double2*)state_in, (double2*)zout, n0 * n1, (int)n2, p, false, S(stream));
+    if (rc != 1) return rc;
+  }
+  // lengths without a fused kernel: the standalone update, then the z pass
+  int rc = kind == 0   ? pfcs_hydro_psi_update_to(state_in, state_out, aux, aux2, n0, n1, n2, kx, ky, kz, c0, c1,
+                                                  diag, stream)
+           : kind == 1 ? pfcs_hydro_vel_update_to(state_in, state_out, aux, n0, n1, n2, kx, ky, kz, c0, c1, c2,
+                                                  diag, stream)
+                       : pfcs_ch_update_to(state_in, state_out, aux, aux2, n0, n1, n2, kx, ky, kz, c0, c1, c2, diag,
+                                           stream);
+  if (rc) return rc;
+  return pfcs_fft_axis_c2c(state_out, zout, n0, n1, n2, 2, 0, stream);
+}
+
 int pfcs_fft_axis_c2c_pro(const void* in, void* out, int64_t n0, int64_t n1, int64_t n2, int axis,
                           int forward, int pro, const void* aux, int aux_axis, void* stream) {
   if (pro == PRO_NONE) return pfcs_fft_axis_c2c(in, out, n0, n1, n2, axis, forward, stream);

@@ -29,12 +29,22 @@ struct Regs1 {
 };
 
 // PRO: a pointwise prologue (pfcs_pro.cuh) applied to each loaded element
-// before the transform (plain layouts only).
+// before the transform (plain layouts only): 1 cube / cmul / deriv, 2 a
+// spectral update (PRO_UPD_*; its own instantiation so the light prologues
+// do not carry its registers).
 #ifndef PFCS_LINES_TARGET2
 #define PFCS_LINES_TARGET2 768  // register target of the 2-stage z-line kernel (B200 512^3: 0.360 -> 0.357 ms)
 #endif
-template <int N, int T, int ST, bool FWD, bool BIN, bool BOUT, bool PRO = false>
-__global__ void __launch_bounds__(T*(N / radix_R(N)), min_blocks(T*(N / radix_R(N)), ST == 2 ? PFCS_LINES_TARGET2 : 1024))
+#ifndef PFCS_UPD_ST
+#define PFCS_UPD_ST 1  // register stages of the update-fused z pass (A/B: profiles/r2_ab_kernels.txt)
+#endif
+#ifndef PFCS_UPD_TARGET
+#define PFCS_UPD_TARGET 512  // resident-thread target of the update-fused z pass
+#endif
+template <int N, int T, int ST, bool FWD, bool BIN, bool BOUT, int PRO = 0>
+__global__ void __launch_bounds__(T*(N / radix_R(N)), min_blocks(T*(N / radix_R(N)), PRO == 2 ? PFCS_UPD_TARGET
+                                                                                   : ST == 2 ? PFCS_LINES_TARGET2
+                                                                                             : 1024))
     k_lines(const double2* in, double2* out, i64 nlines, SlabSplit sin, SlabSplit sout, PeerTable tout,
             const double2* __restrict__ tw, double scale, Pro pro = Pro{}) {
   constexpr int R = radix_R(N);
@@ -66,13 +76,35 @@ __global__ void __launch_bounds__(T*(N / radix_R(N)), min_blocks(T*(N / radix_R(
   auto comp = [&](i64 tile, Regs1<R>& r) {
     const i64 l = tile * T + t;
     const int jj = opaque(j);
-    if constexpr (PRO) {  // lines run along z: (x, y) = (l / n1, l % n1)
-      const i64 lx = l / pro.n1;
-      const i64 ly = l - lx * pro.n1;
-      const i64 cl = pro.axis == 0 ? lx : ly;
+    if constexpr (PRO == 1) {  // lines run along z: (x, y) = (l / n1, l % n1)
+      if (l < nlines) {  // (a partial last tile: no aux reads / state writes past the end)
+        const i64 lx = l / pro.n1;
+        const i64 ly = l - lx * pro.n1;
+        const i64 cl = pro.axis == 0 ? lx : ly;
 #pragma unroll
-      for (int e = 0; e < R; ++e)
-        r.v[e] = apply_pro(pro, r.v[e], l * N + jj + P * e, pro.axis == 2 ? (i64)(jj + P * e) : cl);
+        for (int e = 0; e < R; ++e)
+          r.v[e] = apply_pro(pro, r.v[e], l * N + jj + P * e, pro.axis == 2 ? (i64)(jj + P * e) : cl);
+      }
+    } else if constexpr (PRO == 2) {
+      if (l < nlines) {
+        const i64 lx = l / pro.n1;
+        const i64 ly = l - lx * pro.n1;
+        const double ka = __ldg(pro.kx + lx), kb = __ldg(pro.ky + ly);
+        const double kxy = __dadd_rn(__dmul_rn(ka, ka), __dmul_rn(kb, kb));
+        const double2* A = (const double2*)pro.aux + l * N;
+        const double2* B = (const double2*)pro.aux2 + l * N;
+        double2 a[R], b[R];
+#pragma unroll
+        for (int e = 0; e < R; ++e) {  // all operand loads in flight before the first use
+          a[e] = __ldg(A + jj + P * e);
+          b[e] = pro.aux2 ? __ldg(B + jj + P * e) : make_double2(0.0, 0.0);
+        }
+#pragma unroll
+        for (int e = 0; e < R; ++e) {
+          const double kc = __ldg(pro.kz + jj + P * e);
+          r.v[e] = apply_upd(pro, r.v[e], a[e], b[e], l * N + jj + P * e, __dadd_rn(kxy, __dmul_rn(kc, kc)));
+        }
+      }
     }
     fft_line<N, FWD, 1, PFCS_LINES_TWL>(r.v, jj, sl, tw);
     if (l < nlines) {
@@ -299,11 +331,21 @@ static int lines_n(const double2* in, double2* out, i64 nlines, SlabSplitH si, S
     if (pro) {
       if (bin || bout) return fail(PFCS_E_UNSUPPORTED, "prologue on a blocked line pass");
       int grid = 0;
-      if (int rc = persistent_grid((const void*)k_lines<N, T, ST, FWD, false, false, true>, T * P, smem, ntiles,
-                                   &grid))
+      if (pro->kind >= PRO_UPD_PSI) {  // updates feed inverse transforms only
+        if constexpr (FWD) {
+          return fail(PFCS_E_UNSUPPORTED, "update prologue on a forward pass");
+        } else {
+          if (int rc = persistent_grid((const void*)k_lines<N, T, PFCS_UPD_ST, FWD, false, false, 2>, T * P, smem,
+                                       ntiles, &grid))
+            return rc;
+          k_lines<N, T, PFCS_UPD_ST, FWD, false, false, 2><<<grid, T * P, smem, st>>>(in, out, nlines, a, b, tab,
+                                                                                      tw, scale, *pro);
+          return check_launch("k_lines(update)");
+        }
+      }
+      if (int rc = persistent_grid((const void*)k_lines<N, T, ST, FWD, false, false, 1>, T * P, smem, ntiles, &grid))
         return rc;
-      k_lines<N, T, ST, FWD, false, false, true><<<grid, T * P, smem, st>>>(in, out, nlines, a, b, tab, tw, scale,
-                                                                           *pro);
+      k_lines<N, T, ST, FWD, false, false, 1><<<grid, T * P, smem, st>>>(in, out, nlines, a, b, tab, tw, scale, *pro);
       return check_launch("k_lines(pro)");
     }
     const void* f;

@@ -10,6 +10,7 @@
 // The only non-bit-reproducible factor is the Gaussian cg = exp(-a0^2 k^2/2)
 // (CUDA exp vs numpy exp differ in the last ulp on a few % of inputs).
 #include "pfcs_diag.cuh"
+#include "pfcs_hydro_math.cuh"
 #include "pfcs_internal.h"
 
 namespace pfcs {
@@ -84,19 +85,8 @@ __global__ void k_hydro_psi_update(const double2* psi_in, double2* psi_hat, cons
                                    double eps, double dt, double* diag) {
   bool bad = false;
   PFCS_FOR_ALL(n) {
-    const double k2 = k2_at(kx, ky, kz, i, n1, n2);
-    const double lap = -k2;
-    const double a = __dsub_rn(1.0, k2);
-    const double b = __dsub_rn(4.0 / 3.0, k2);
-    const double op = __dadd_rn(eps, __dmul_rn(__dmul_rn(a, a), __dmul_rn(b, b)));
-    const double rden = __drcp_rn(__dsub_rn(1.0, __dmul_rn(dt, __dmul_rn(lap, op))));
-    const double2 nl = nl_hat[i];
     const double2 ad = adv_hat ? adv_hat[i] : make_double2(0.0, 0.0);
-    const double tr = __dsub_rn(__dmul_rn(lap, nl.x), ad.x);
-    const double ti = __dsub_rn(__dmul_rn(lap, nl.y), ad.y);
-    const double2 ph = psi_in[i];
-    const double2 nw = make_double2(__dmul_rn(__dadd_rn(ph.x, __dmul_rn(dt, tr)), rden),
-                                    __dmul_rn(__dadd_rn(ph.y, __dmul_rn(dt, ti)), rden));
+    const double2 nw = psi_update(psi_in[i], nl_hat[i], ad, k2_at(kx, ky, kz, i, n1, n2), eps, dt);
     bad |= !isfinite(nw.x);  // hydro._check_finite looks at the real part (hydro.py:72-74)
     psi_hat[i] = nw;
   }
@@ -125,15 +115,8 @@ __global__ void k_hydro_vel_update(const double2* v_in, double2* v_hat, const do
                                    double c_exp, double* diag) {
   bool bad = false;
   PFCS_FOR_ALL(n) {
-    const double k2 = k2_at(kx, ky, kz, i, n1, n2);
-    const double lap = -k2;
-    const double cg = exp(__dmul_rn(c_exp, k2));
-    const double w = __dmul_rn(c_cg, cg);
-    const double rden = __drcp_rn(__dsub_rn(1.0, __dmul_rn(c_den, lap)));
     const double2 f = force ? force[i] : make_double2(0.0, 0.0);
-    const double2 v = v_in[i];
-    const double2 nw = make_double2(__dmul_rn(__dsub_rn(v.x, __dmul_rn(w, f.x)), rden),
-                                    __dmul_rn(__dsub_rn(v.y, __dmul_rn(w, f.y)), rden));
+    const double2 nw = vel_update(v_in[i], f, k2_at(kx, ky, kz, i, n1, n2), c_cg, c_den, c_exp);
     bad |= !isfinite(nw.x);
     v_hat[i] = nw;
   }
@@ -161,16 +144,8 @@ __global__ void k_ch_update(const double2* c_in, double2* c_hat, const double2* 
                             const double* __restrict__ kz, double mob, double kappa, double dt, double* diag) {
   bool bad = false;
   PFCS_FOR_ALL(n) {
-    const double lap = -k2_at(kx, ky, kz, i, n1, n2);
-    const double ml = __dmul_rn(mob, lap);
-    const double rden = __drcp_rn(__dadd_rn(1.0, __dmul_rn(__dmul_rn(dt, __dmul_rn(mob, kappa)), __dmul_rn(lap, lap))));
-    const double2 f = f_hat[i];
     const double2 ad = adv_hat ? adv_hat[i] : make_double2(0.0, 0.0);
-    const double2 ch = c_in[i];
-    const double tr = __dsub_rn(__dmul_rn(ml, f.x), ad.x);
-    const double ti = __dsub_rn(__dmul_rn(ml, f.y), ad.y);
-    const double2 nw = make_double2(__dmul_rn(__dadd_rn(ch.x, __dmul_rn(dt, tr)), rden),
-                                    __dmul_rn(__dadd_rn(ch.y, __dmul_rn(dt, ti)), rden));
+    const double2 nw = ch_update(c_in[i], f_hat[i], ad, k2_at(kx, ky, kz, i, n1, n2), mob, kappa, dt);
     bad |= !isfinite(nw.x);
     c_hat[i] = nw;
   }

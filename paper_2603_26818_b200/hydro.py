@@ -341,6 +341,7 @@ def free_energy_full(psi, sym: SymbolTable, grid: GridSpec) -> float:
 
 RPW_CUBE, RPW_MUL, RPW_ADV3, RPW_CHNL, RPW_ADD3 = 0, 1, 2, 3, 4  # pfcs_real_pointwise kinds
 _R2C_PRO = os.environ.get("PFCS_R2C_PRO", "1") != "0"  # fused prologues (A/B switch)
+_R2C_UPD = os.environ.get("PFCS_R2C_UPD", "1") != "0"  # updates fused into the next inverse (A/B switch)
 
 
 def _is_real(x) -> bool:
@@ -411,6 +412,35 @@ class _Real3:
             nat.call("pfcs_fft_axis_c2c", nat.ptr(out), nat.ptr(out), self.nh, ny, nz, 2, 1, st)
         return out
 
+    def update_inv(self, kind: int, state: torch.Tensor, aux: torch.Tensor, aux2, c: tuple,
+                   flag: "_StepFlag") -> tuple:
+        """A spectral update fused with the first (z) pass of the inverse
+        transform of its result (pfcs_update_zinv; kind 0 psi, 1 velocity,
+        2 composition): returns (new state, F^-1 of it).  PFCS_R2C_UPD=0 runs
+        the standalone update kernel and the plain inverse (bit-identical)."""
+        nx, ny, nz = self.shape
+        nh = self.nh
+        kx, ky, kz = self.k
+        st = nat.stream_ptr()
+        new = torch.empty_like(state)
+        if not _R2C_UPD:
+            name = ("pfcs_hydro_psi_update_to", "pfcs_hydro_vel_update_to", "pfcs_ch_update_to")[kind]
+            ops = [nat.ptr(state), nat.ptr(new), nat.ptr(aux)] + ([] if kind == 1 else [nat.ptr(aux2)])
+            consts = c[:2] if kind == 0 else c
+            nat.call(name, *ops, nh, ny, nz, nat.ptr(kx), nat.ptr(ky), nat.ptr(kz), *(float(v) for v in consts),
+                     nat.ptr(flag.t), st)
+            return new, self.inv(new)
+        tmp = torch.empty_like(state)
+        c3 = tuple(float(v) for v in c) + (0.0,) * (3 - len(c))
+        nat.call("pfcs_update_zinv", kind, nat.ptr(state), nat.ptr(aux), nat.ptr(aux2) if aux2 is not None else None,
+                 nat.ptr(new), nat.ptr(tmp), nh, ny, nz, nat.ptr(kx), nat.ptr(ky), nat.ptr(kz), *c3,
+                 nat.ptr(flag.t), st)
+        if ny > 1:
+            nat.call("pfcs_fft_axis_c2c", nat.ptr(tmp), nat.ptr(tmp), nh, ny, nz, 1, 0, st)
+        out = torch.empty(self.shape, dtype=torch.float64, device=state.device)
+        nat.call("pfcs_irfft_x", nat.ptr(tmp), nat.ptr(out), nx, ny * nz, st)
+        return new, out
+
     def inv(self, h: torch.Tensor, deriv: int | None = None) -> torch.Tensor:
         nx, ny, nz = self.shape
         nh = self.nh
@@ -472,15 +502,9 @@ def _adv_term_r(R: _Real3, x_hat: torch.Tensor, axis: int, v_axis: torch.Tensor)
 
 
 def _density_r(R: _Real3, ph, ps, adv, sym, hp: HydroParams, flag: _StepFlag):
-    nh, ny, nz = R.hshape
-    kx, ky, kz = R.k
     nl_hat = R.fwd(ps, RPW_CUBE)
     adv_hat = R.fwd(adv)
-    new = torch.empty_like(ph)
-    nat.call("pfcs_hydro_psi_update_to", nat.ptr(ph), nat.ptr(new), nat.ptr(nl_hat), nat.ptr(adv_hat), nh, ny, nz,
-             nat.ptr(kx), nat.ptr(ky), nat.ptr(kz), float(sym.eps), float(hp.pfc.dt), nat.ptr(flag.t),
-             nat.stream_ptr())
-    return new, R.inv(new)
+    return R.update_inv(0, ph, nl_hat, adv_hat, (float(sym.eps), float(hp.pfc.dt)), flag)
 
 
 def _density_mu_r(R: _Real3, ps, sym) -> torch.Tensor:
@@ -496,8 +520,6 @@ def _density_mu_r(R: _Real3, ps, sym) -> torch.Tensor:
 
 def _velocity_r(R: _Real3, vh, ps, axis: int, mu_hat, sym, hp: HydroParams, flag: _StepFlag, cc=None,
                 muc=None, beta: float = 0.0):
-    nh, ny, nz = R.hshape
-    kx, ky, kz = R.k
     force = R.fwd(R.inv(mu_hat, deriv=axis), RPW_MUL, ps)  # F(psi F^-1(i k mu_hat))
     if beta != 0.0:
         force_c = R.fwd(R.inv(muc, deriv=axis), RPW_MUL, cc)
@@ -506,11 +528,8 @@ def _velocity_r(R: _Real3, vh, ps, axis: int, mu_hat, sym, hp: HydroParams, flag
                  nat.stream_ptr())
         force = total
     dt, rho = float(hp.pfc.dt), float(hp.rho)
-    new = torch.empty_like(vh)
-    nat.call("pfcs_hydro_vel_update_to", nat.ptr(vh), nat.ptr(new), nat.ptr(force), nh, ny, nz, nat.ptr(kx),
-             nat.ptr(ky), nat.ptr(kz), dt / rho, (dt / rho) * float(hp.gamma), -0.5 * float(sym.a0) ** 2,
-             nat.ptr(flag.t), nat.stream_ptr())
-    return new, R.inv(new)
+    return R.update_inv(1, vh, force, None, (dt / rho, (dt / rho) * float(hp.gamma), -0.5 * float(sym.a0) ** 2),
+                        flag)
 
 
 def _serial_hydro_step_r(fields: HydroFields, sym: SymbolTable, params: HydroParams) -> HydroFields:

@@ -328,15 +328,10 @@ def parallel_multi_step(worker, st: dict, sym: SymbolTable, params: MultiParams)
 # ------------------------------------------------------------ R2C path ------
 
 def _composition_r(R: _Real3, ch, cc, v, sym, params: MultiParams, flag: _StepFlag):
-    nh, ny, nz = R.hshape
-    kx, ky, kz = R.k
     adv_hat = R.fwd(_grad_dot_r(R, ch, v))
     f_hat = R.fwd(cc, RPW_CHNL, alpha=params.alpha)
-    new = torch.empty_like(ch)
-    nat.call("pfcs_ch_update_to", nat.ptr(ch), nat.ptr(new), nat.ptr(f_hat), nat.ptr(adv_hat), nh, ny, nz, nat.ptr(kx),
-             nat.ptr(ky), nat.ptr(kz), float(params.mobility), float(params.kappa), float(params.hydro.pfc.dt),
-             nat.ptr(flag.t), _st())
-    return new, R.inv(new)
+    return R.update_inv(2, ch, f_hat, adv_hat,
+                        (float(params.mobility), float(params.kappa), float(params.hydro.pfc.dt)), flag)
 
 
 def _composition_mu_r(R: _Real3, cc, ch, params: MultiParams) -> torch.Tensor:
