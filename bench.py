@@ -379,6 +379,22 @@ def run_fft(ctx, args, out):
     ms_e2e = timed(ctx, e2e_step, max(48, args.steps), 2, drain=drain)
     torch.cuda.synchronize()
     e2e_err = float((yh[(k_step[0] - 1) % 2] - xh).norm() / xh.norm())
+
+    # the same copy pipeline with no compute: the PCIe bound of the e2e step
+    def copy_step():
+        b = k_step[0] % 2
+        k_step[0] += 1
+        with torch.cuda.stream(s_up):
+            s_up.wait_event(downloaded[b])
+            dev_in[b].copy_(xh, non_blocking=True)
+            loaded[b].record(s_up)
+        with torch.cuda.stream(s_down):
+            s_down.wait_event(loaded[b])
+            yh[b].copy_(dev_in[b], non_blocking=True)
+            downloaded[b].record(s_down)
+
+    ms_copy = timed(ctx, copy_step, max(48, args.steps), 2, drain=drain)
+    torch.cuda.synchronize()
     bpr = fft_bytes(n)
     value = bpr / (ms * 1e-3) / 1e9
     out.update({
@@ -389,6 +405,9 @@ def run_fft(ctx, args, out):
                 "h2d_bytes_per_step": int(ctx.sum_over_ranks(x.numel() * 8)),
                 "d2h_bytes_per_step": int(ctx.sum_over_ranks(x.numel() * 8)),
                 "pipeline": "H2D of step k+1 overlaps D2H of step k (separate copy streams)",
+                "copy_only_ms_per_step": round(ms_copy, 3),
+                "pcie_gbs_per_direction": round(x.numel() * 8 / (ms_copy * 1e-3) / 1e9, 2),
+                "frac_of_copy_bound": round(ms_copy / ms_e2e, 4),
                 "roundtrip_rel_l2": ctx.max_over_ranks(e2e_err)},
         "kernels": table,
         "kernels_note": KERNELS_NOTE,
