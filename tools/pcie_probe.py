@@ -30,3 +30,28 @@ for k in (1, 2, 4, 8):
         torch.cuda.synchronize()
     ms = a.elapsed_time(b)
     print(f"k={k}: 1 GiB up + 1 GiB down concurrently in {ms:.2f} ms -> {2 * 8 * n / ms / 1e6:.1f} GB/s total")
+
+# one direction at a time, and where the host memory sits relative to the GPU
+for name, fn in (("H2D only", lambda: din.copy_(hin, non_blocking=True)),
+                 ("D2H only", lambda: hout.copy_(dout, non_blocking=True))):
+    fn()
+    torch.cuda.synchronize()
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    a.record()
+    fn()
+    b.record()
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b)
+    print(f"{name}: 1 GiB in {ms:.2f} ms -> {8 * n / ms / 1e6:.1f} GB/s")
+try:
+    import glob
+    import subprocess
+
+    print(subprocess.run(["nvidia-smi", "--query-gpu=pci.bus_id,pcie.link.gen.current,pcie.link.width.current",
+                          "--format=csv,noheader"], capture_output=True, text=True).stdout.strip())
+    for p in glob.glob("/sys/bus/pci/devices/*/numa_node"):
+        pass
+    print("host NUMA nodes:", len(glob.glob("/sys/devices/system/node/node[0-9]*")))
+except Exception as exc:  # diagnostics only
+    print("topology query failed:", exc)
