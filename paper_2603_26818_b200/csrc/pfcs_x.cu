@@ -45,10 +45,18 @@ struct RPro {
   double alpha;
   const double* aux;  // kind 1: the other factor, same (nx, inner) layout
 };
-__device__ __forceinline__ double rpro_apply(const RPro& p, double x, i64 idx, bool ok) {
+// `a` = the kind-1 factor (loaded ahead of use by the caller: a product
+// prologue that loads its factor when it needs it exposes a full DRAM latency
+// per tile — 1.22 vs 0.44 ms per 512^3 launch)
+__device__ __forceinline__ double rpro_apply(const RPro& p, double x, double a) {
   if (p.kind == 0) return __dmul_rn(__dmul_rn(x, x), x);
-  if (p.kind == 1) return __dmul_rn(x, ok ? __ldg(p.aux + idx) : 0.0);
+  if (p.kind == 1) return __dmul_rn(x, a);
   return __dmul_rn(p.alpha, __dsub_rn(__dmul_rn(x, __dmul_rn(x, x)), x));
+}
+// the kind-1 factors of rows 2m and 2m+1 of column i (zero outside the grid)
+__device__ __forceinline__ double2 rpro_factor(const RPro& p, i64 m, i64 i, i64 inner, bool ok) {
+  if (p.kind != 1 || !ok) return make_double2(0.0, 0.0);
+  return make_double2(__ldg(p.aux + (2 * m) * inner + i), __ldg(p.aux + (2 * m + 1) * inner + i));
 }
 
 // values per thread of the fused cube pass (A/B experiments: -DPFCS_CUBE_R,
@@ -81,10 +89,11 @@ __host__ __device__ constexpr bool late_mirror(int mode) {
   return PFCS_MIRROR == 2 && (mode == 2 || (PFCS_MIRROR_C2R && mode == 1));
 }
 
-template <int R>
+template <int R, bool AX = false>
 struct RegsX {
   double2 v[R];
-  double2 xm;  // row M (half-spectrum Nyquist mode), used by thread j == 0
+  double2 xm;           // row M (half-spectrum Nyquist mode), used by thread j == 0
+  double2 ax[AX ? R : 1];  // MODE_R2C_PRO: the prologue's factors of rows 2m, 2m+1
 };
 
 // Extra +8 keeps row M (index PAD(M)) inside the line when the bank rule
@@ -131,8 +140,9 @@ __global__ void __launch_bounds__(T*(M / real_R(M, MODE)),
   double2* sl = smem + t * LS;
   const i64 ntiles = (inner + T - 1) / T;
   double m_abs = 0.0;
+  using Regs = RegsX<R, MODE == MODE_R2C_PRO>;
 
-  auto load = [&](i64 tile, RegsX<R>& r) {
+  auto load = [&](i64 tile, Regs& r) {
     const i64 i = tile * T + t;
     const bool ok = i < inner;
     if (is_r2c(MODE)) {
@@ -142,11 +152,7 @@ __global__ void __launch_bounds__(T*(M / real_R(M, MODE)),
         const i64 m = j + P * e;
         r.v[e] = ok ? make_double2(in[(2 * m) * inner + i], in[(2 * m + 1) * inner + i])
                     : make_double2(0.0, 0.0);
-        if constexpr (MODE == MODE_R2C_PRO) {
-          if (ok)
-            r.v[e] = make_double2(rpro_apply(rp, r.v[e].x, (2 * m) * inner + i, true),
-                                  rpro_apply(rp, r.v[e].y, (2 * m + 1) * inner + i, true));
-        }
+        if constexpr (MODE == MODE_R2C_PRO) r.ax[e] = rpro_factor(rp, m, i, inner, ok);  // applied in comp
       }
     } else {
       const double2* in = (const double2*)in_;
@@ -159,7 +165,7 @@ __global__ void __launch_bounds__(T*(M / real_R(M, MODE)),
     }
   };
 
-  auto comp = [&](i64 tile, RegsX<R>& r) {
+  auto comp = [&](i64 tile, Regs& r) {
     const unsigned tid_ = opaque_tid();
     const int t = tid_ % T;
     const int jj = tid_ / T;
@@ -167,6 +173,13 @@ __global__ void __launch_bounds__(T*(M / real_R(M, MODE)),
     const i64 i = tile * T + t;
     const bool ok = i < inner;
     double2* v = r.v;
+    if constexpr (MODE == MODE_R2C_PRO && !TMA) {
+      if (ok) {
+#pragma unroll
+        for (int e = 0; e < R; ++e)
+          v[e] = make_double2(rpro_apply(rp, v[e].x, r.ax[e].x), rpro_apply(rp, v[e].y, r.ax[e].y));
+      }
+    }
     if (!is_r2c(MODE)) {
       // Z'[k] = (X_k + conj X_{M-k}) + i W_N^{-k} (X_k - conj X_{M-k});
       // Im X_0 and Im X_M are ignored (numpy irfft convention)
@@ -278,7 +291,7 @@ __global__ void __launch_bounds__(T*(M / real_R(M, MODE)),
   };
 
   if constexpr (!TMA) {
-    reg_tile_loop<ST, RegsX<R>>(ntiles, load, comp);
+    reg_tile_loop<ST, Regs>(ntiles, load, comp);
   } else {
     unsigned long long* bars = (unsigned long long*)(smem + (size_t)T * LS);
     auto issue = [&](i64 tile, int sidx) {
@@ -299,6 +312,15 @@ __global__ void __launch_bounds__(T*(M / real_R(M, MODE)),
     __syncthreads();
     i64 tile = blockIdx.x;
     if (tid == 0 && tile < ntiles) issue(tile, 0);
+    // MODE_R2C_PRO: the product factors of the tile, loaded one tile ahead
+    double2 axn[MODE == MODE_R2C_PRO ? R : 1];
+    auto aux_ahead = [&](i64 tl) {
+      if constexpr (MODE == MODE_R2C_PRO) {
+#pragma unroll
+        for (int e = 0; e < R; ++e) axn[e] = rpro_factor(rp, j + P * e, tl * T + t, inner, tl * T + t < inner);
+      }
+    };
+    aux_ahead(tile);
     for (int it = 0; tile < ntiles; ++it, tile += gridDim.x) {
       const int sidx = it & 1;
       if (tid == 0) {
@@ -310,7 +332,7 @@ __global__ void __launch_bounds__(T*(M / real_R(M, MODE)),
       }
       mbar_wait(&bars[sidx], (unsigned)((it >> 1) & 1));
       cur = sidx ? stage1 : stage0;
-      RegsX<R> r;
+      Regs r;
       if (is_r2c(MODE)) {
         // rows 2m and 2m+1 of a T-double stage row pair sit in opposite
         // halves of the 32 banks when T = 8: odd-j threads read their odd
@@ -324,13 +346,10 @@ __global__ void __launch_bounds__(T*(M / real_R(M, MODE)),
           const double a = sd[(2 * m + sw) * T + t];
           const double b = sd[(2 * m + 1 - sw) * T + t];
           r.v[e] = sw ? make_double2(b, a) : make_double2(a, b);
-          if constexpr (MODE == MODE_R2C_PRO) {
-            const i64 i = tile * T + t;
-            const bool ok = i < inner;
-            r.v[e] = make_double2(rpro_apply(rp, r.v[e].x, (2 * m) * inner + i, ok),
-                                  rpro_apply(rp, r.v[e].y, (2 * m + 1) * inner + i, ok));
-          }
+          if constexpr (MODE == MODE_R2C_PRO)
+            r.v[e] = make_double2(rpro_apply(rp, r.v[e].x, axn[e].x), rpro_apply(rp, r.v[e].y, axn[e].y));
         }
+        if constexpr (MODE == MODE_R2C_PRO) aux_ahead(tile + gridDim.x);  // in flight during comp
       } else {
 #pragma unroll
         for (int e = 0; e < R; ++e) r.v[e] = cur[(j + P * e) * T + t];
@@ -709,7 +728,11 @@ static int real_x_m(const void* in, void* out, i64 inner, double* diag, cudaStre
       // 1024^3 4.94 -> 5.58 (64-byte real rows, one CTA per SM), so R2C keeps
       // the register pipeline from M = 512 up.
       if constexpr (XStage<M, T, MODE>::SMEM <= 227 * 1024 && (!is_r2c(MODE) || (T >= 2 && M <= 256))) {
-        if (tma_enabled() && x_tmaps<M, T, MODE>(&tm, in, inner)) {
+        // a product prologue (kind 1) streams a second real array: the
+        // register pipeline prefetches it with the tile (512^3: 0.67 ms vs
+        // 0.85 ms TMA-staged with the factor loaded one tile ahead)
+        const bool reg_product = MODE == MODE_R2C_PRO && rp.kind == 1;
+        if (!reg_product && tma_enabled() && x_tmaps<M, T, MODE>(&tm, in, inner)) {
           constexpr size_t smem = XStage<M, T, MODE>::SMEM;
           int grid = 0;
           if (int rc = persistent_grid((const void*)k_real_x<M, T, 3, MODE>, T * P, smem, ntiles, &grid)) return rc;

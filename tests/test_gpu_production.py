@@ -385,7 +385,7 @@ def test_pfc_1024_step_vs_lean_restatement(torch_cuda, pfc1024):
     assert rel_l2(got, want) <= 1e-12
 
 
-@pytest.mark.parametrize("nx,inner", [(512, 7104), (1024, 3600), (64, 300)])
+@pytest.mark.parametrize("nx,inner", [(512, 7104), (512, 7110), (1024, 3600), (1024, 3606), (64, 300)])
 @pytest.mark.parametrize("kind", [0, 1, 3])
 def test_rfft_x_prologue_production(torch_cuda, nx, inner, kind):
     """pfcs_rfft_x_pro (the R2C multiphysics transforms' fused psi^3, psi*g,

@@ -2,7 +2,7 @@
 
     python tools/prof_kernel.py <kind> [n] [reps]
 
-kind: cube_x | update_z | rfft_x | irfft_x | zlines | strided
+kind: cube_x | update_z | rfft_x | irfft_x | rfft_pro{0,1,3} | zlines | strided
 The kernel runs `reps` times (default 2: one warm launch + one to capture with
 `ncu -k regex:<kernel> -s 1 -c 1`).  Prints the average CUDA-event time of
 launches 2..reps (never a bench number when run under ncu).
@@ -44,6 +44,11 @@ def main():
             fn = lambda: nat.call("pfcs_rfft_x", nat.ptr(r), nat.ptr(a), n, n * n, st)
         else:
             fn = lambda: nat.call("pfcs_irfft_x", nat.ptr(a), nat.ptr(r), n, n * n, st)
+    elif kind.startswith("rfft_pro"):  # rfft_pro0 / rfft_pro1 / rfft_pro3: R2C x pass with a prologue
+        r = torch.randn(n * n * n, dtype=torch.float64, device="cuda")
+        aux = torch.randn_like(r)
+        pk = int(kind[-1])
+        fn = lambda: nat.call("pfcs_rfft_x_pro", nat.ptr(r), nat.ptr(a), n, n * n, pk, nat.ptr(aux), 0.5, st)
     elif kind == "zlines":
         fn = lambda: nat.call("pfcs_fft_zlines", nat.ptr(a), nat.ptr(a), nh * n, n, 1, 1, 1, st)
     elif kind == "strided":
