@@ -33,6 +33,8 @@ from __future__ import annotations
 
 import enum
 
+import warnings
+
 import numpy as np
 import torch
 
@@ -336,7 +338,13 @@ def _peer_plan(worker, g: "_Geometry"):
     plans = worker.__dict__.setdefault("_pfcs_plans", {})
     key = (g.nx, g.ny, g.nz, g.real)
     if key not in plans:
-        plans[key] = _PeerPlan(worker, g)
+        from .peer import PeerUnavailable
+
+        try:
+            plans[key] = _PeerPlan(worker, g)
+        except PeerUnavailable as exc:  # every rank: the collective path from now on
+            warnings.warn(f"fused peer exchange unavailable ({exc}); using the collective all-to-all")
+            plans[key] = None
     return plans[key]
 
 

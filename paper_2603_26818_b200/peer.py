@@ -74,30 +74,57 @@ class PeerMap:
             pass
 
 
-def map_peers(worker, buf: DeviceBuffer) -> PeerMap:
-    """Collective: device addresses of `buf` on all ranks of `worker`."""
-    lib = nat.load()
-    dev = torch.cuda.current_device()
+class PeerUnavailable(RuntimeError):
+    """Raised on EVERY rank of a group when any rank could not map a peer's
+    buffer (no P2P between the devices, no CUDA IPC in this container): the
+    callers fall back to the collective exchange, all ranks together."""
+
+
+def _map_rank(worker, buf: DeviceBuffer, lib, dev: int) -> PeerMap:
+    """This rank's side of map_peers (collective exchange of the handles or
+    addresses, then the local mapping); raises if the mapping fails."""
     if hasattr(worker, "_dist"):  # ProcessWorker: CUDA IPC handles
         h = ctypes.create_string_buffer(64)
-        nat.check(lib.pfcs_ipc_get_handle(ctypes.c_void_p(buf.ptr), ctypes.addressof(h)), "pfcs_ipc_get_handle")
-        handles = worker.all_to_all([bytes(h.raw)] * worker.size)
-        addrs, opened = [], []
+        got = lib.pfcs_ipc_get_handle(ctypes.c_void_p(buf.ptr), ctypes.addressof(h))
+        # every rank takes part in the exchange, with None if it has no handle
+        handles = worker.all_to_all([bytes(h.raw) if got == 0 else None] * worker.size)
+        nat.check(got, "pfcs_ipc_get_handle")
+        pm = PeerMap([], [])
         for r, raw in enumerate(handles):
             if r == worker.rank:
-                addrs.append(buf.ptr)
+                pm.addrs.append(buf.ptr)
                 continue
+            if raw is None:
+                raise RuntimeError(f"rank {r} has no IPC handle")
             p = ctypes.c_void_p()
             hb = ctypes.create_string_buffer(raw, 64)
             nat.check(lib.pfcs_ipc_open_handle(ctypes.addressof(hb), ctypes.byref(p)), "pfcs_ipc_open_handle")
-            addrs.append(p.value)
-            opened.append(p.value)
-        return PeerMap(addrs, opened)
+            pm.addrs.append(p.value)
+            pm._opened.append(p.value)
+        return pm
     infos = worker.all_to_all([(buf.ptr, dev)] * worker.size)
     for _, d in infos:
         if d != dev:
             nat.check(lib.pfcs_enable_peer_access(int(d)), "pfcs_enable_peer_access")
     return PeerMap([p for p, _ in infos], [])
+
+
+def map_peers(worker, buf: DeviceBuffer) -> PeerMap:
+    """Collective: device addresses of `buf` on all ranks of `worker`.
+    Raises PeerUnavailable on all ranks if any rank fails to map (the ranks
+    agree through one more all-to-all, so none is left waiting in a fused
+    exchange the others abandoned)."""
+    lib = nat.load()
+    err, pm = "", None
+    try:
+        pm = _map_rank(worker, buf, lib, torch.cuda.current_device())
+    except Exception as exc:
+        err = f"rank {worker.rank}: {exc}"
+    errs = [e for e in worker.all_to_all([err] * worker.size) if e]
+    if errs:
+        del pm  # closes any IPC mappings this rank opened
+        raise PeerUnavailable("; ".join(errs))
+    return pm
 
 
 class _IpcFence:

@@ -156,8 +156,14 @@ class _StepEngine:
               and exchange_mode() == "peer"):
             # the fused y-line scatter (pfcs_fft_lines_scatter) needs
             # power-of-two y lines <= 4096; other y extents take the collective
-            self._setup_peer()
-        else:
+            from .peer import PeerUnavailable
+
+            try:
+                self._setup_peer()
+            except PeerUnavailable as exc:  # on every rank: collective buffers instead
+                warnings.warn(f"fused peer exchange unavailable ({exc}); using the collective all-to-all")
+                self._bz = self._bx = self._maps = None
+        if not self.peer and self.G > 1:
             self.send = torch.empty(max(g.xslab_elems, 1), dtype=cdt, device=self.device)
             self.recv_z = torch.empty(max(g.zslab_elems, 1), dtype=cdt, device=self.device)
             self.recv_x = torch.empty(max(g.xslab_elems, 1), dtype=cdt, device=self.device)

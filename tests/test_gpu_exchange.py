@@ -106,3 +106,44 @@ def test_exchange_processes_ipc_bitwise(pkg, mode):
         assert peer is not None, out
         assert peer == (mode == "peer")
         np.testing.assert_array_equal(out, ref)
+
+
+@pytest.mark.parametrize("fail_rank", [0, 1])
+def test_peer_mapping_failure_falls_back_on_every_rank(pkg, monkeypatch, fail_rank):
+    """If ANY rank cannot map a peer buffer (no P2P / no CUDA IPC), every
+    rank raises PeerUnavailable together and the step engine and the
+    distributed FFT fall back to the collective exchange — same results."""
+    from paper_2603_26818_b200 import peer
+
+    real_map = peer._map_rank
+
+    def flaky(worker, buf, lib, dev):
+        pm = real_map(worker, buf, lib, dev)
+        if worker.rank == fail_rank:
+            raise RuntimeError("injected: no peer access")
+        return pm
+
+    monkeypatch.setattr(peer, "_map_rank", flaky)
+    ref = _run(pkg, 1, "peer", True)
+    with pytest.warns(UserWarning, match="fused peer exchange unavailable"):
+        got = _run_fallback(pkg, 2)
+    np.testing.assert_array_equal(got, ref)
+
+
+def _run_fallback(pkg, G, steps=12, n=(16, 32, 16)):
+    from paper_2603_26818_b200 import distfft, pfc
+
+    grid = pkg.GridSpec(n, pfc.default_domain_length(n))
+    psi0 = pfc.initial_field("constant_plus_noise", grid, seed=9, noise_amplitude=0.05)
+
+    def body(w):
+        sym = pkg.make_symbols(grid, -0.3)
+        f = distfft.scatter(psi0, w, grid, distfft.Layout.Z_SLAB, real=True)
+        st = pfc.PfcState(psi_hat=distfft.forward(f, w), grid=grid, symbols=sym, worker=w)
+        pfc.pfc_run(st, pfc.PfcParams(), steps // 2)
+        for _ in range(steps - steps // 2):
+            pfc.pfc_step(st, pfc.PfcParams())
+        assert not st._engine.peer
+        return distfft.gather(distfft.inverse(st.psi_hat, w), w)
+
+    return pkg.spawn_group(G, body)[0]
