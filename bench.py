@@ -506,10 +506,12 @@ def multi_bytes(n: int) -> float:
     cubes and alpha (c^3 - c) ride in their transforms' loads for free) =
     17R; the spectral updates / mu (psi 4S, c 4S, mu 3S, 3 x velocity 3S =
     20S), less the five state updates' re-read of the new state, which ride
-    in the z pass of their inverse transform (pfcs_update_zinv: -5S)."""
+    in the z pass of their inverse transform (pfcs_update_zinv: -5S), and
+    less one z pass (2S) per gradient — grad psi, grad c, grad mu: the x and
+    y derivatives share one inverse z pass (_Real3.grad_inv: -6S)."""
     R = 8.0 * n**3
     S = spec_bytes(n)
-    return 23 * (R + 5 * S) + 17 * R + 15 * S
+    return 23 * (R + 5 * S) + 17 * R + 9 * S
 
 
 def run_multi(ctx, args):

@@ -281,7 +281,8 @@ int pfcs_fft_axis_c2c_pro(const void* in, void* out, int64_t n0, int64_t n1, int
   const int64_t n = axis == 0 ? n0 : (axis == 1 ? n1 : n2);
   const int64_t outer = axis == 0 ? 1 : (axis == 1 ? n0 : n0 * n1);
   const int64_t inner = axis == 0 ? n1 * n2 : (axis == 1 ? n2 : 1);
-  const Pro p{pro, aux, aux_axis, (int)n1, (int)n2};
+  Pro p{pro, aux, aux_axis, (int)n1, (int)n2};
+  p.pass = axis;
   if (n > 1 && n <= 4096) {
     // fused: contiguous lines (k_lines) or the TMA-staged strided pass
     // (B200, 512^3 multiphysics step: 105 -> 95 ms with cube, product and

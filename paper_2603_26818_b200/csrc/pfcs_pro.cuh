@@ -27,6 +27,7 @@ struct Pro {
   const double *kx, *ky, *kz;
   double c0, c1, c2;  // psi: eps, dt; vel: dt/rho, (dt/rho) gamma, -a0^2/2; c: mobility, kappa, dt
   double* diag;       // non-finite flag (value 3 of a slot), or null
+  int pass;           // axis of the transform the prologue feeds (strided passes: 0 or 1)
 };
 
 // Prologue on element `idx` (flat C index of the (n0, n1, n2) grid) whose

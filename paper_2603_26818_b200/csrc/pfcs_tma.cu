@@ -83,6 +83,14 @@ __global__ void __launch_bounds__(T*(N / radix_R(N)), 1)
   __syncthreads();
   i64 tile = blockIdx.x;
   if (tid == 0 && tile < ntiles) issue(tile, 0);
+  // PRO_DERIV along the line: the multipliers of this thread's elements are
+  // the same in every tile
+  double dline[PRO ? R : 1];
+  if constexpr (PRO) {
+#pragma unroll
+    for (int e = 0; e < R; ++e)
+      dline[e] = (pro.kind == PRO_DERIV && pro.axis == pro.pass) ? __ldg((const double*)pro.aux + j + P * e) : 0.0;
+  }
   for (int it = 0; tile < ntiles; ++it, tile += gridDim.x) {
     const int s = it & 1;
     if (tid == 0) {
@@ -103,16 +111,21 @@ __global__ void __launch_bounds__(T*(N / radix_R(N)), 1)
     if constexpr (PRO) {
       if (i < inner) {
         // element (o, n, i) of the (outer, N, inner) view of the (n0, n1, n2)
-        // grid; PRO_DERIV (not on the hydro hot path here) decodes its
-        // coordinate from the flat index
+        // grid.  PRO_DERIV: the multiplier's coordinate is n itself when it
+        // runs along the line, else fixed for the thread's column — decoded
+        // once per tile (a per-element 64-bit decode made the y pass with
+        // an x / y derivative 1.5-2x slower than the plain pass)
+        if (pro.kind == PRO_DERIV) {  // i d[c] v, apply_pro's arithmetic
+          const i64 cfix = pro.pass == 1 ? (pro.axis == 0 ? o : i) : (pro.axis == 1 ? i / pro.n2 : i % pro.n2);
+          const double dfix = pro.axis == pro.pass ? 0.0 : __ldg((const double*)pro.aux + cfix);
 #pragma unroll
-        for (int e = 0; e < R; ++e) {
-          const i64 idx = (o * N + jj + P * e) * inner + i;
-          i64 c = 0;
-          if (pro.kind == PRO_DERIV)
-            c = pro.axis == 2 ? idx % pro.n2
-                              : (pro.axis == 1 ? (idx / pro.n2) % pro.n1 : idx / ((i64)pro.n2 * pro.n1));
-          v[e] = apply_pro(pro, v[e], idx, c);
+          for (int e = 0; e < R; ++e) {
+            const double dk = pro.axis == pro.pass ? dline[e] : dfix;
+            v[e] = make_double2(-__dmul_rn(dk, v[e].y), __dmul_rn(dk, v[e].x));
+          }
+        } else {
+#pragma unroll
+          for (int e = 0; e < R; ++e) v[e] = apply_pro(pro, v[e], (o * N + jj + P * e) * inner + i, 0);
         }
       }
     }

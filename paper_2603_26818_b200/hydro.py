@@ -342,6 +342,10 @@ def free_energy_full(psi, sym: SymbolTable, grid: GridSpec) -> float:
 RPW_CUBE, RPW_MUL, RPW_ADV3, RPW_CHNL, RPW_ADD3 = 0, 1, 2, 3, 4  # pfcs_real_pointwise kinds
 _R2C_PRO = os.environ.get("PFCS_R2C_PRO", "1") != "0"  # fused prologues (A/B switch)
 _R2C_UPD = os.environ.get("PFCS_R2C_UPD", "1") != "0"  # updates fused into the next inverse (A/B switch)
+# x / y derivatives share one z pass, multiplier in the y pass (A/B timing
+# switch: PFCS_R2C_GRAD=0 multiplies in each derivative's own z pass, which
+# rounds differently — not a bit-identity switch)
+_R2C_GRAD = os.environ.get("PFCS_R2C_GRAD", "1") != "0"
 
 
 def _is_real(x) -> bool:
@@ -442,6 +446,9 @@ class _Real3:
         return new, out
 
     def inv(self, h: torch.Tensor, deriv: int | None = None) -> torch.Tensor:
+        """F^-1[h], or F^-1[i d_deriv h] (grad_inv's recipe for that axis)."""
+        if deriv is not None and deriv != 2 and self.shape[1] > 1 and _R2C_GRAD:
+            return self.grad_inv(h, (deriv,))[0]
         nx, ny, nz = self.shape
         nh = self.nh
         st = nat.stream_ptr()
@@ -456,6 +463,37 @@ class _Real3:
         out = torch.empty(self.shape, dtype=torch.float64, device=h.device)
         nat.call("pfcs_irfft_x", nat.ptr(tmp), nat.ptr(out), nx, ny * nz, st)
         return out
+
+
+    def grad_inv(self, h: torch.Tensor, axes=(0, 1, 2)) -> list:
+        """[F^-1(i d_a h) for a in axes].  k_x and k_y are constant along z
+        lines, so the x and y derivatives share ONE plain inverse z pass and
+        take their multiplier in the y pass (pfcs_fft_axis_c2c_pro, axis 1);
+        the z derivative takes it in its own z pass.  A gradient costs two z
+        passes instead of three (2S less HBM traffic).  Every caller — the
+        serial steps and each rank of the role maps — forms a derivative
+        along a given axis the same way, so they stay bit-identical."""
+        nx, ny, nz = self.shape
+        nh = self.nh
+        st = nat.stream_ptr()
+        if ny == 1 or not _R2C_GRAD:
+            return [self.inv(h, deriv=a) for a in axes]
+        t0 = None
+        outs = []
+        for a in axes:
+            if a == 2:
+                outs.append(self.inv(h, deriv=2))
+                continue
+            if t0 is None:
+                t0 = torch.empty_like(h)
+                nat.call("pfcs_fft_axis_c2c", nat.ptr(h), nat.ptr(t0), nh, ny, nz, 2, 0, st)
+            tmp = torch.empty_like(h)
+            nat.call("pfcs_fft_axis_c2c_pro", nat.ptr(t0), nat.ptr(tmp), nh, ny, nz, 1, 0, 3,
+                     nat.ptr(self.d[a]), a, st)
+            out = torch.empty(self.shape, dtype=torch.float64, device=h.device)
+            nat.call("pfcs_irfft_x", nat.ptr(tmp), nat.ptr(out), nx, ny * nz, st)
+            outs.append(out)
+        return outs
 
 
 def _check_half(R: _Real3, *spectra: torch.Tensor) -> None:
@@ -492,7 +530,7 @@ class _StepFlag:
 
 def _grad_dot_r(R: _Real3, x_hat: torch.Tensor, v) -> torch.Tensor:
     """v . grad x = sum_i v_i F^-1(i d_i x_hat), real (hydro.py:83-85 order)."""
-    g = [R.inv(x_hat, deriv=i) for i in range(3)]
+    g = R.grad_inv(x_hat)
     return _rpw(RPW_ADV3, v[0], g[0], v[1], g[1], v[2], g[2])
 
 
@@ -519,10 +557,14 @@ def _density_mu_r(R: _Real3, ps, sym) -> torch.Tensor:
 
 
 def _velocity_r(R: _Real3, vh, ps, axis: int, mu_hat, sym, hp: HydroParams, flag: _StepFlag, cc=None,
-                muc=None, beta: float = 0.0):
-    force = R.fwd(R.inv(mu_hat, deriv=axis), RPW_MUL, ps)  # F(psi F^-1(i k mu_hat))
+                muc=None, beta: float = 0.0, dmu=None, dmuc=None):
+    """dmu / dmuc: F^-1(i d_axis mu_hat) (/ muc) when the caller formed the
+    whole gradient at once (R.grad_inv: the serial steps)."""
+    if dmu is None:
+        dmu = R.inv(mu_hat, deriv=axis)
+    force = R.fwd(dmu, RPW_MUL, ps)  # F(psi F^-1(i k mu_hat))
     if beta != 0.0:
-        force_c = R.fwd(R.inv(muc, deriv=axis), RPW_MUL, cc)
+        force_c = R.fwd(dmuc if dmuc is not None else R.inv(muc, deriv=axis), RPW_MUL, cc)
         total = torch.empty_like(force)
         nat.call("pfcs_axpy", nat.ptr(force), nat.ptr(force_c), nat.ptr(total), total.numel(), float(beta),
                  nat.stream_ptr())
@@ -543,7 +585,8 @@ def _serial_hydro_step_r(fields: HydroFields, sym: SymbolTable, params: HydroPar
     vs = [_rdev(v) for v in fields.v]
     psi_hat, psi = _density_r(R, ph, ps, _grad_dot_r(R, ph, vs), sym, params, flag)
     mu_hat = _density_mu_r(R, psi, sym)  # shared by the three components
-    out = [_velocity_r(R, vh[i], psi, i, mu_hat, sym, params, flag) for i in range(3)]
+    dmu = R.grad_inv(mu_hat)
+    out = [_velocity_r(R, vh[i], psi, i, mu_hat, sym, params, flag, dmu=dmu[i]) for i in range(3)]
     flag.check(fields.step_index, psi_hat, *(o[0] for o in out))
     fields.psi_hat, fields.psi = _out(psi_hat, host), _out(psi, host)
     for i in range(3):

@@ -2,7 +2,7 @@
 
     python tools/prof_kernel.py <kind> [n] [reps]
 
-kind: cube_x | update_z | rfft_x | irfft_x | rfft_pro{0,1,3} | zlines | strided
+kind: cube_x | update_z | rfft_x | irfft_x | rfft_pro{0,1,3} | deriv<axis><aux_axis> | zlines | strided
 The kernel runs `reps` times (default 2: one warm launch + one to capture with
 `ncu -k regex:<kernel> -s 1 -c 1`).  Prints the average CUDA-event time of
 launches 2..reps (never a bench number when run under ncu).
@@ -49,8 +49,16 @@ def main():
         aux = torch.randn_like(r)
         pk = int(kind[-1])
         fn = lambda: nat.call("pfcs_rfft_x_pro", nat.ptr(r), nat.ptr(a), n, n * n, pk, nat.ptr(aux), 0.5, st)
+    elif kind.startswith("deriv"):  # deriv<axis><aux_axis>: an inverse pass with the i d multiplier fused
+        ax, aa = int(kind[5]), int(kind[6])
+        d = torch.randn(n if aa else nh, dtype=torch.float64, device="cuda")
+        b = torch.empty_like(a)
+        fn = lambda: nat.call("pfcs_fft_axis_c2c_pro", nat.ptr(a), nat.ptr(b), nh, n, n, ax, 0, 3, nat.ptr(d), aa, st)
     elif kind == "zlines":
         fn = lambda: nat.call("pfcs_fft_zlines", nat.ptr(a), nat.ptr(a), nh * n, n, 1, 1, 1, st)
+    elif kind == "strided_oop":
+        b = torch.empty_like(a)
+        fn = lambda: nat.call("pfcs_fft_axis_c2c", nat.ptr(a), nat.ptr(b), nh, n, n, 1, 0, st)
     elif kind == "strided":
         fn = lambda: nat.call("pfcs_fft_axis_c2c", nat.ptr(a), nat.ptr(a), nh, n, n, 1, 1, st)
     else:
