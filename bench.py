@@ -508,10 +508,12 @@ def multi_bytes(n: int) -> float:
     20S), less the five state updates' re-read of the new state, which ride
     in the z pass of their inverse transform (pfcs_update_zinv: -5S), and
     less one z pass (2S) per gradient — grad psi, grad c, grad mu: the x and
-    y derivatives share one inverse z pass (_Real3.grad_inv: -6S)."""
+    y derivatives share one inverse z pass (_Real3.grad_inv: -6S), and less
+    the physical derivative's write and re-read in each of the three forces
+    psi F^-1(i k mu) (one fused C2R * psi R2C x pass, pfcs_xmul_x: -6R)."""
     R = 8.0 * n**3
     S = spec_bytes(n)
-    return 23 * (R + 5 * S) + 17 * R + 9 * S
+    return 23 * (R + 5 * S) + 11 * R + 9 * S
 
 
 def run_multi(ctx, args):

@@ -135,6 +135,13 @@ int pfcs_irfft_x(const void* in, double* out, int64_t nx, int64_t inner, void* s
  * bit-identical to that kernel followed by pfcs_rfft_x. */
 int pfcs_rfft_x_pro(const double* in, void* out, int64_t nx, int64_t inner, int kind, const double* aux,
                     double alpha, void* stream);
+/* The x pass of a pseudo-spectral product, in place: data (an (nx/2+1,
+ * inner) x-halved spectrum whose y and z passes are done) <- R2C(C2R(data) *
+ * aux), aux a real (nx, inner) field — the hydro force psi * F^-1(i k mu)
+ * between the inverse and forward x stages (hydro.py:98), so neither factor
+ * nor product reaches HBM.  Bit-identical to pfcs_irfft_x, then
+ * pfcs_real_pointwise kind 1 with aux, then pfcs_rfft_x. */
+int pfcs_xmul_x(void* data, const double* aux, int64_t nx, int64_t inner, void* stream);
 
 /* ---- fused PFC step kernels: pfc.pfc_step (pfc.py:96-128) ---------------
  * Diagnostics block `diag` (device, PFCS_DIAG_SLOTS x 4 doubles; the caller

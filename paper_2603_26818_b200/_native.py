@@ -64,6 +64,7 @@ _SIGS = {
     "pfcs_rfft_x": [_c_p, _c_p, _c_i64, _c_i64, _c_p],
     "pfcs_irfft_x": [_c_p, _c_p, _c_i64, _c_i64, _c_p],
     "pfcs_rfft_x_pro": [_c_p, _c_p, _c_i64, _c_i64, _c_int, _c_p, _c_d, _c_p],
+    "pfcs_xmul_x": [_c_p, _c_p, _c_i64, _c_i64, _c_p],
     "pfcs_pfc_cube_x": [_c_p, _c_i64, _c_i64, _c_int, _c_p, _c_p],
     "pfcs_pfc_update_z": [_c_p, _c_p, _c_p, _c_i64, _c_i64, _c_i64, _c_int, _c_int,
                           _c_p, _c_p, _c_p, _c_d, _c_d, _c_p, _c_p],

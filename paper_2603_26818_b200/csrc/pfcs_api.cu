@@ -178,6 +178,7 @@ int launch_real_x(const void* in, void* out, long long nx, long long inner, int 
 int launch_cube_c2c(void* data, long long nx, long long inner, double* diag, cudaStream_t st);
 int launch_rfft_x_pro(const double* in, void* out, long long nx, long long inner, int kind, const double* aux,
                       double alpha, cudaStream_t st);
+int launch_xmul(void* data, const double* aux, long long nx, long long inner, cudaStream_t st);
 int launch_pfc_z(const double2* nl, double2* psi_hat, double2* next, long long cx, long long ny,
                  long long nz, int g_in, int g_out, const double* kx, const double* ky,
                  const double* kz, double eps, double dt, double* diag, cudaStream_t st,
@@ -343,6 +344,13 @@ int pfcs_rfft_x_pro(const double* in, void* out, int64_t nx, int64_t inner, int 
                     double alpha, void* stream) {
   if (!in || !out) return fail(PFCS_E_ARG, "null argument");
   return launch_rfft_x_pro(in, out, nx, inner, kind, aux, alpha, S(stream));
+}
+
+int pfcs_xmul_x(void* data, const double* aux, int64_t nx, int64_t inner, void* stream) {
+  if (!data) return fail(PFCS_E_ARG, "null argument");
+  if (nx < 1 || inner < 0) return fail(PFCS_E_ARG, "bad shape");
+  if ((const void*)aux == data) return fail(PFCS_E_ARG, "aux must not alias data");
+  return launch_xmul(data, aux, nx, inner, S(stream));
 }
 
 int pfcs_rfft_x(const double* in, void* out, int64_t nx, int64_t inner, void* stream) {

@@ -32,7 +32,11 @@
 
 namespace pfcs {
 
-enum { MODE_R2C = 0, MODE_C2R = 1, MODE_CUBE = 2, MODE_R2C_PRO = 3 };
+enum { MODE_R2C = 0, MODE_C2R = 1, MODE_CUBE = 2, MODE_R2C_PRO = 3, MODE_XMUL = 4 };
+// MODE_XMUL: the x pass of a pseudo-spectral product, in place like the cube
+// pass: C2R -> x * aux per real sample (pfcs_real_pointwise kind 1's
+// arithmetic) -> R2C, so neither the physical factor F^-1(.) nor the
+// product reaches HBM (the hydro force psi * F^-1(i k mu), hydro.py:98).
 __host__ __device__ constexpr bool is_r2c(int mode) { return mode == MODE_R2C || mode == MODE_R2C_PRO; }
 
 // Pointwise prologue of an R2C x pass (MODE_R2C_PRO): the real sample x of
@@ -68,7 +72,7 @@ __device__ __forceinline__ double2 rpro_factor(const RPro& p, i64 m, i64 i, i64 
 #define PFCS_CUBE_TARGET 768
 #endif
 __host__ __device__ constexpr int real_R(int m, int mode) {
-  return (mode == 2 && m >= 64) ? PFCS_CUBE_R : radix_R(m);
+  return ((mode == 2 || mode == 4) && m >= 64) ? PFCS_CUBE_R : radix_R(m);
 }
 
 // Mirrored pre-step: the C2R pre-twiddle pairs X_k with X_{M-k}.  With
@@ -180,6 +184,13 @@ __global__ void __launch_bounds__(T*(M / real_R(M, MODE)),
           v[e] = make_double2(rpro_apply(rp, v[e].x, r.ax[e].x), rpro_apply(rp, v[e].y, r.ax[e].y));
       }
     }
+    // MODE_XMUL: the factors of rows 2m, 2m+1, loaded before the inverse
+    // FFT so their latency hides behind it
+    double2 xf[MODE == MODE_XMUL ? R : 1];
+    if constexpr (MODE == MODE_XMUL) {
+#pragma unroll
+      for (int e = 0; e < R; ++e) xf[e] = rpro_factor(rp, jj + P * e, i, inner, ok);
+    }
     if (!is_r2c(MODE)) {
       // Z'[k] = (X_k + conj X_{M-k}) + i W_N^{-k} (X_k - conj X_{M-k});
       // Im X_0 and Im X_M are ignored (numpy irfft convention)
@@ -247,6 +258,10 @@ __global__ void __launch_bounds__(T*(M / real_R(M, MODE)),
         // psi**3 of a real sample, x*x*x in numpy's left-to-right order
         v[e] = make_double2(__dmul_rn(__dmul_rn(a, a), a), __dmul_rn(__dmul_rn(b, b), b));
       }
+    }
+    if constexpr (MODE == MODE_XMUL) {
+#pragma unroll
+      for (int e = 0; e < R; ++e) v[e] = make_double2(__dmul_rn(v[e].x, xf[e].x), __dmul_rn(v[e].y, xf[e].y));
     }
 
     // forward M-point FFT, then the R2C split
@@ -708,14 +723,14 @@ static int real_x_m(const void* in, void* out, i64 inner, double* diag, cudaStre
   if (!twN) return PFCS_E_CUDA;
   constexpr int PM = M / real_R(M, MODE);
   const long long tiles_min = (inner + (PM >= 32 ? 1 : 32 / PM) - 1) / (PM >= 32 ? 1 : 32 / PM);
-  return with_variant_n<MODE == MODE_CUBE ? KIND_CUBER : KIND_REALX, M>(tiles_min, [&](auto var) -> int {
+  return with_variant_n<(MODE == MODE_CUBE || MODE == MODE_XMUL) ? KIND_CUBER : KIND_REALX, M>(tiles_min, [&](auto var) -> int {
     constexpr int V = decltype(var)::value;
     constexpr int P = M / real_R(M, MODE);
     // R2C/C2R at M = 256 (the 512^3 round trip) take 16 lines per tile:
     // 128-byte complex rows and real rows, one 512-thread CTA per SM (B200:
     // rfft_x 0.50 -> 0.42 ms, irfft_x 0.53 -> 0.43 ms; the cube pass stays
     // at 8 lines, 0.67 vs 0.71 ms)
-    constexpr int TX = (MODE != MODE_CUBE && M == 256) ? 1 : 0;
+    constexpr int TX = (MODE != MODE_CUBE && MODE != MODE_XMUL && M == 256) ? 1 : 0;
     constexpr int T = ((P >= 32 ? 1 : 32 / P) << (V & 3)) << TX;
     constexpr int ST = 1 + (V >> 2);
     if constexpr (T * P > 1024) {
@@ -793,6 +808,25 @@ int launch_real_x(const void* in, void* out, long long nx, long long inner, int 
       if (rc != 1) return rc;                                                         \
     }                                                                                 \
     return real_x_m<MM, MODE_CUBE>(in, out, inner, diag, st);
+    PFCS_M_CASES(PFCS_CASE)
+#undef PFCS_CASE
+    default:
+      break;
+  }
+  return fail(PFCS_E_UNSUPPORTED, "unsupported nx");
+}
+
+// x pass of a pseudo-spectral product (MODE_XMUL), in place
+int launch_xmul(void* data, const double* aux, long long nx, long long inner, cudaStream_t st) {
+  if (inner <= 0) return PFCS_OK;
+  if (!aux) return fail(PFCS_E_ARG, "x-pass product needs aux");
+  if (!is_pow2(nx) || nx < 4 || nx > 8192)
+    return fail(PFCS_E_UNSUPPORTED, "real x transforms need a power-of-two nx in [4, 8192]");
+  const RPro rp{1, 0.0, aux};
+  switch (nx / 2) {
+#define PFCS_CASE(MM) \
+  case MM:            \
+    return real_x_m<MM, MODE_XMUL>(data, data, inner, nullptr, st, rp);
     PFCS_M_CASES(PFCS_CASE)
 #undef PFCS_CASE
     default:

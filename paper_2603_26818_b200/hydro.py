@@ -346,6 +346,8 @@ _R2C_UPD = os.environ.get("PFCS_R2C_UPD", "1") != "0"  # updates fused into the 
 # switch: PFCS_R2C_GRAD=0 multiplies in each derivative's own z pass, which
 # rounds differently — not a bit-identity switch)
 _R2C_GRAD = os.environ.get("PFCS_R2C_GRAD", "1") != "0"
+# the force product in one fused x pass (_Real3.prod_grad; A/B, bit-identical)
+_R2C_XMUL = os.environ.get("PFCS_R2C_XMUL", "1") != "0"
 
 
 def _is_real(x) -> bool:
@@ -447,52 +449,79 @@ class _Real3:
 
     def inv(self, h: torch.Tensor, deriv: int | None = None) -> torch.Tensor:
         """F^-1[h], or F^-1[i d_deriv h] (grad_inv's recipe for that axis)."""
-        if deriv is not None and deriv != 2 and self.shape[1] > 1 and _R2C_GRAD:
+        if deriv is not None:
             return self.grad_inv(h, (deriv,))[0]
         nx, ny, nz = self.shape
         nh = self.nh
         st = nat.stream_ptr()
         tmp = torch.empty_like(h)
-        if deriv is not None:  # i d_axis x_hat fused into the z pass
-            nat.call("pfcs_fft_axis_c2c_pro", nat.ptr(h), nat.ptr(tmp), nh, ny, nz, 2, 0, 3,
-                     nat.ptr(self.d[deriv]), deriv, st)
-        else:
-            nat.call("pfcs_fft_axis_c2c", nat.ptr(h), nat.ptr(tmp), nh, ny, nz, 2, 0, st)
+        nat.call("pfcs_fft_axis_c2c", nat.ptr(h), nat.ptr(tmp), nh, ny, nz, 2, 0, st)
         if ny > 1:
             nat.call("pfcs_fft_axis_c2c", nat.ptr(tmp), nat.ptr(tmp), nh, ny, nz, 1, 0, st)
         out = torch.empty(self.shape, dtype=torch.float64, device=h.device)
         nat.call("pfcs_irfft_x", nat.ptr(tmp), nat.ptr(out), nx, ny * nz, st)
         return out
 
-
-    def grad_inv(self, h: torch.Tensor, axes=(0, 1, 2)) -> list:
-        """[F^-1(i d_a h) for a in axes].  k_x and k_y are constant along z
-        lines, so the x and y derivatives share ONE plain inverse z pass and
-        take their multiplier in the y pass (pfcs_fft_axis_c2c_pro, axis 1);
-        the z derivative takes it in its own z pass.  A gradient costs two z
-        passes instead of three (2S less HBM traffic).  Every caller — the
-        serial steps and each rank of the role maps — forms a derivative
-        along a given axis the same way, so they stay bit-identical."""
+    def _grad_zy(self, h: torch.Tensor, axes) -> list:
+        """The inverse z and y passes of F^-1(i d_a h) for each a in axes
+        (x-halved spectra, before the x pass).  k_x and k_y are constant
+        along z lines, so the x and y derivatives share ONE plain inverse z
+        pass and take their multiplier in the y pass (pfcs_fft_axis_c2c_pro,
+        axis 1); the z derivative takes it in its own z pass.  A gradient
+        costs two z passes instead of three (2S less HBM traffic).  Every
+        caller — the serial steps and each rank of the role maps — forms a
+        derivative along a given axis this way, so they stay bit-identical."""
         nx, ny, nz = self.shape
         nh = self.nh
         st = nat.stream_ptr()
-        if ny == 1 or not _R2C_GRAD:
-            return [self.inv(h, deriv=a) for a in axes]
-        t0 = None
-        outs = []
+        share = ny > 1 and _R2C_GRAD
+        t0, outs = None, []
         for a in axes:
-            if a == 2:
-                outs.append(self.inv(h, deriv=2))
-                continue
-            if t0 is None:
-                t0 = torch.empty_like(h)
-                nat.call("pfcs_fft_axis_c2c", nat.ptr(h), nat.ptr(t0), nh, ny, nz, 2, 0, st)
             tmp = torch.empty_like(h)
-            nat.call("pfcs_fft_axis_c2c_pro", nat.ptr(t0), nat.ptr(tmp), nh, ny, nz, 1, 0, 3,
-                     nat.ptr(self.d[a]), a, st)
+            if share and a != 2:
+                if t0 is None:
+                    t0 = torch.empty_like(h)
+                    nat.call("pfcs_fft_axis_c2c", nat.ptr(h), nat.ptr(t0), nh, ny, nz, 2, 0, st)
+                nat.call("pfcs_fft_axis_c2c_pro", nat.ptr(t0), nat.ptr(tmp), nh, ny, nz, 1, 0, 3,
+                         nat.ptr(self.d[a]), a, st)
+            else:  # i d_a fused into the z pass
+                nat.call("pfcs_fft_axis_c2c_pro", nat.ptr(h), nat.ptr(tmp), nh, ny, nz, 2, 0, 3,
+                         nat.ptr(self.d[a]), a, st)
+                if ny > 1:
+                    nat.call("pfcs_fft_axis_c2c", nat.ptr(tmp), nat.ptr(tmp), nh, ny, nz, 1, 0, st)
+            outs.append(tmp)
+        return outs
+
+    def grad_inv(self, h: torch.Tensor, axes=(0, 1, 2)) -> list:
+        """[F^-1(i d_a h) for a in axes] (real fields; see _grad_zy)."""
+        nx, ny, nz = self.shape
+        st = nat.stream_ptr()
+        outs = []
+        for tmp in self._grad_zy(h, axes):
             out = torch.empty(self.shape, dtype=torch.float64, device=h.device)
             nat.call("pfcs_irfft_x", nat.ptr(tmp), nat.ptr(out), nx, ny * nz, st)
             outs.append(out)
+        return outs
+
+    def prod_grad(self, h: torch.Tensor, aux: torch.Tensor, axes=(0, 1, 2)) -> list:
+        """[F(aux * F^-1(i d_a h)) for a in axes] — the hydro force
+        F(psi F^-1(i k mu_hat)) (hydro.py:98): the inverse z / y passes of
+        _grad_zy, ONE fused x pass (C2R, times aux, R2C: pfcs_xmul_x, the
+        physical derivative and the product never reach HBM), the forward y
+        and z passes.  Bit-identical to fwd(grad_inv(h)[a], RPW_MUL, aux)
+        (PFCS_R2C_XMUL=0 runs that form)."""
+        if not _R2C_XMUL:
+            return [self.fwd(d, RPW_MUL, aux) for d in self.grad_inv(h, axes)]
+        nx, ny, nz = self.shape
+        nh = self.nh
+        st = nat.stream_ptr()
+        outs = self._grad_zy(h, axes)
+        for tmp in outs:
+            nat.call("pfcs_xmul_x", nat.ptr(tmp), nat.ptr(aux), nx, ny * nz, st)
+            if ny > 1:
+                nat.call("pfcs_fft_axis_c2c", nat.ptr(tmp), nat.ptr(tmp), nh, ny, nz, 1, 1, st)
+            if nz > 1:
+                nat.call("pfcs_fft_axis_c2c", nat.ptr(tmp), nat.ptr(tmp), nh, ny, nz, 2, 1, st)
         return outs
 
 
@@ -557,14 +586,14 @@ def _density_mu_r(R: _Real3, ps, sym) -> torch.Tensor:
 
 
 def _velocity_r(R: _Real3, vh, ps, axis: int, mu_hat, sym, hp: HydroParams, flag: _StepFlag, cc=None,
-                muc=None, beta: float = 0.0, dmu=None, dmuc=None):
-    """dmu / dmuc: F^-1(i d_axis mu_hat) (/ muc) when the caller formed the
-    whole gradient at once (R.grad_inv: the serial steps)."""
-    if dmu is None:
-        dmu = R.inv(mu_hat, deriv=axis)
-    force = R.fwd(dmu, RPW_MUL, ps)  # F(psi F^-1(i k mu_hat))
+                muc=None, beta: float = 0.0, force=None, force_c=None):
+    """force / force_c: F(psi F^-1(i d_axis mu_hat)) (/ c, muc) when the
+    caller formed all three at once (R.prod_grad: the serial steps)."""
+    if force is None:
+        force = R.prod_grad(mu_hat, ps, (axis,))[0]  # F(psi F^-1(i k mu_hat))
     if beta != 0.0:
-        force_c = R.fwd(dmuc if dmuc is not None else R.inv(muc, deriv=axis), RPW_MUL, cc)
+        if force_c is None:
+            force_c = R.prod_grad(muc, cc, (axis,))[0]
         total = torch.empty_like(force)
         nat.call("pfcs_axpy", nat.ptr(force), nat.ptr(force_c), nat.ptr(total), total.numel(), float(beta),
                  nat.stream_ptr())
@@ -585,8 +614,8 @@ def _serial_hydro_step_r(fields: HydroFields, sym: SymbolTable, params: HydroPar
     vs = [_rdev(v) for v in fields.v]
     psi_hat, psi = _density_r(R, ph, ps, _grad_dot_r(R, ph, vs), sym, params, flag)
     mu_hat = _density_mu_r(R, psi, sym)  # shared by the three components
-    dmu = R.grad_inv(mu_hat)
-    out = [_velocity_r(R, vh[i], psi, i, mu_hat, sym, params, flag, dmu=dmu[i]) for i in range(3)]
+    forces = R.prod_grad(mu_hat, psi)
+    out = [_velocity_r(R, vh[i], psi, i, mu_hat, sym, params, flag, force=forces[i]) for i in range(3)]
     flag.check(fields.step_index, psi_hat, *(o[0] for o in out))
     fields.psi_hat, fields.psi = _out(psi_hat, host), _out(psi, host)
     for i in range(3):

@@ -357,10 +357,10 @@ def _serial_multi_step_r(fields: MultiFields, sym: SymbolTable, params: MultiPar
     c_hat, c = _composition_r(R, ch, cc, vs, sym, params, flag)
     mu_hat = _density_mu_r(R, psi, sym)
     muc = _composition_mu_r(R, c, c_hat, params) if params.beta != 0.0 else None
-    dmu = R.grad_inv(mu_hat)
-    dmuc = R.grad_inv(muc) if muc is not None else [None] * 3
-    out = [_velocity_r(R, vh[i], psi, i, mu_hat, sym, params.hydro, flag, c, muc, params.beta, dmu[i], dmuc[i])
-           for i in range(3)]
+    forces = R.prod_grad(mu_hat, psi)
+    forces_c = R.prod_grad(muc, c) if muc is not None else [None] * 3
+    out = [_velocity_r(R, vh[i], psi, i, mu_hat, sym, params.hydro, flag, c, muc, params.beta, forces[i],
+                       forces_c[i]) for i in range(3)]
     flag.check(fields.step_index, psi_hat, c_hat, *(o[0] for o in out))
     for i in range(3):
         fields.v_hat[i], fields.v[i] = _out(out[i][0], host), _out(out[i][1], host)

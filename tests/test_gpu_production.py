@@ -411,3 +411,32 @@ def test_rfft_x_prologue_production(torch_cuda, nx, inner, kind):
     assert torch.equal(fused, two)
     f = {0: x * x * x, 1: x * g, 3: 0.7 * (x * (x * x) - x)}[kind]
     assert rel_l2(fused.cpu().numpy(), sfft.rfft(f, axis=0, workers=WORKERS)) <= TOL
+
+
+@pytest.mark.parametrize("nx,inner", [(512, 7104), (512, 7110), (1024, 3600), (64, 300)])
+def test_xmul_x_production(torch_cuda, nx, inner):
+    """pfcs_xmul_x (the x pass of the force product: C2R, times a real
+    field, R2C, in place) at the production tiles: bit-identical to
+    pfcs_irfft_x + pfcs_real_pointwise kind 1 + pfcs_rfft_x, and vs scipy
+    <= 1e-12."""
+    import scipy.fft as sfft
+
+    torch, nat = torch_cuda, _nat()
+    rng = np.random.default_rng(nx + inner)
+    nh = nx // 2 + 1
+    spec = rng.standard_normal((nh, inner)) + 1j * rng.standard_normal((nh, inner))
+    g = rng.standard_normal((nx, inner))
+    gd = _to(torch, g)
+    st = nat.stream_ptr()
+    fused = _to(torch, spec)
+    nat.call("pfcs_xmul_x", nat.ptr(fused), nat.ptr(gd), nx, inner, st)
+    phys = torch.empty((nx, inner), dtype=torch.float64, device="cuda")
+    nat.call("pfcs_irfft_x", nat.ptr(_to(torch, spec)), nat.ptr(phys), nx, inner, st)
+    prod = torch.empty_like(phys)
+    nat.call("pfcs_real_pointwise", 1, nat.ptr(phys), nat.ptr(gd), None, None, None, None, nat.ptr(prod),
+             prod.numel(), 0.0, st)
+    two = torch.empty_like(fused)
+    nat.call("pfcs_rfft_x", nat.ptr(prod), nat.ptr(two), nx, inner, st)
+    assert torch.equal(fused, two)
+    want = sfft.rfft(sfft.irfft(spec, n=nx, axis=0, workers=WORKERS) * g, axis=0, workers=WORKERS)
+    assert rel_l2(fused.cpu().numpy(), want) <= TOL
