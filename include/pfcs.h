@@ -142,6 +142,17 @@ int pfcs_rfft_x_pro(const double* in, void* out, int64_t nx, int64_t inner, int 
  * nor product reaches HBM.  Bit-identical to pfcs_irfft_x, then
  * pfcs_real_pointwise kind 1 with aux, then pfcs_rfft_x. */
 int pfcs_xmul_x(void* data, const double* aux, int64_t nx, int64_t inner, void* stream);
+/* The x pass of the advection term v . grad x (hydro.py:83-85) in one pass:
+ * spec3 = the three derivative spectra i d_a x_hat after their inverse z
+ * and y passes, stacked (3, nx/2+1, inner); v0..v2 real (nx, inner); out
+ * (nx/2+1, inner) = R2C((v0 g0 + v1 g1) + v2 g2), g_a = C2R(spec3[a]) —
+ * bit-identical to three pfcs_irfft_x + pfcs_real_pointwise kind 2 +
+ * pfcs_rfft_x.  nx 256 or 512 (TMA-staged); pfcs_xdot3_supported(nx,
+ * inner) says whether this build / setting has the fused kernel
+ * (PFCS_E_UNSUPPORTED otherwise). */
+int pfcs_xdot3_supported(int64_t nx, int64_t inner);
+int pfcs_xdot3_x(const void* spec3, const double* v0, const double* v1, const double* v2, void* out, int64_t nx,
+                 int64_t inner, void* stream);
 
 /* ---- fused PFC step kernels: pfc.pfc_step (pfc.py:96-128) ---------------
  * Diagnostics block `diag` (device, PFCS_DIAG_SLOTS x 4 doubles; the caller

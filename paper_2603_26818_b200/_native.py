@@ -65,6 +65,8 @@ _SIGS = {
     "pfcs_irfft_x": [_c_p, _c_p, _c_i64, _c_i64, _c_p],
     "pfcs_rfft_x_pro": [_c_p, _c_p, _c_i64, _c_i64, _c_int, _c_p, _c_d, _c_p],
     "pfcs_xmul_x": [_c_p, _c_p, _c_i64, _c_i64, _c_p],
+    "pfcs_xdot3_supported": [_c_i64, _c_i64],
+    "pfcs_xdot3_x": [_c_p, _c_p, _c_p, _c_p, _c_p, _c_i64, _c_i64, _c_p],
     "pfcs_pfc_cube_x": [_c_p, _c_i64, _c_i64, _c_int, _c_p, _c_p],
     "pfcs_pfc_update_z": [_c_p, _c_p, _c_p, _c_i64, _c_i64, _c_i64, _c_int, _c_int,
                           _c_p, _c_p, _c_p, _c_d, _c_d, _c_p, _c_p],
@@ -156,7 +158,8 @@ launches = 0
 trace: list | None = None
 _NO_LAUNCH = {"pfcs_version", "pfcs_last_error", "pfcs_device_count", "pfcs_energy_scratch_bytes",
               "pfcs_plan_create", "pfcs_plan_destroy", "pfcs_plan_spectral_elems", "pfcs_ipc_event_create",
-              "pfcs_ipc_event_open", "pfcs_event_record", "pfcs_stream_wait_event", "pfcs_event_destroy"}
+              "pfcs_ipc_event_open", "pfcs_event_record", "pfcs_stream_wait_event", "pfcs_event_destroy",
+              "pfcs_xdot3_supported"}
 
 
 def call(name: str, *args) -> None:

@@ -179,6 +179,9 @@ int launch_cube_c2c(void* data, long long nx, long long inner, double* diag, cud
 int launch_rfft_x_pro(const double* in, void* out, long long nx, long long inner, int kind, const double* aux,
                       double alpha, cudaStream_t st);
 int launch_xmul(void* data, const double* aux, long long nx, long long inner, cudaStream_t st);
+bool xdot3_supported(long long nx, long long inner);
+int launch_xdot3(const void* spec3, const double* v0, const double* v1, const double* v2, void* out, long long nx,
+                 long long inner, cudaStream_t st);
 int launch_pfc_z(const double2* nl, double2* psi_hat, double2* next, long long cx, long long ny,
                  long long nz, int g_in, int g_out, const double* kx, const double* ky,
                  const double* kz, double eps, double dt, double* diag, cudaStream_t st,
@@ -351,6 +354,17 @@ int pfcs_xmul_x(void* data, const double* aux, int64_t nx, int64_t inner, void* 
   if (nx < 1 || inner < 0) return fail(PFCS_E_ARG, "bad shape");
   if ((const void*)aux == data) return fail(PFCS_E_ARG, "aux must not alias data");
   return launch_xmul(data, aux, nx, inner, S(stream));
+}
+
+int pfcs_xdot3_supported(int64_t nx, int64_t inner) { return xdot3_supported(nx, inner) ? 1 : 0; }
+
+int pfcs_xdot3_x(const void* spec3, const double* v0, const double* v1, const double* v2, void* out, int64_t nx,
+                 int64_t inner, void* stream) {
+  if (!spec3 || !v0 || !v1 || !v2 || !out) return fail(PFCS_E_ARG, "null argument");
+  if (out == spec3) return fail(PFCS_E_ARG, "out must not alias the derivative spectra");
+  const int rc = launch_xdot3(spec3, v0, v1, v2, out, nx, inner, S(stream));
+  if (rc == 1) return fail(PFCS_E_UNSUPPORTED, "fused advection x pass: nx 256 or 512 with TMA (pfcs_xdot3_supported)");
+  return rc;
 }
 
 int pfcs_rfft_x(const double* in, void* out, int64_t nx, int64_t inner, void* stream) {

@@ -376,6 +376,193 @@ __global__ void __launch_bounds__(T*(M / real_R(M, MODE)),
   if (MODE == MODE_CUBE) diag_block_max(diag, m_abs, 0.0, m_abs);
 }
 
+// ----------------------------------------------- advection dot product --
+// v . grad x on the R2C path in ONE x pass (hydro.py:83-85 and the
+// composition advection): the inputs are the three derivative spectra
+// i d_a x_hat after their inverse z and y passes, stacked as (3, M+1, inner);
+// per tile the kernel runs three C2R sub-passes (TMA-staged, double-buffered
+// across sub-passes) and accumulates v_a * g_a per real sample in registers
+// in pfcs_real_pointwise kind 2's order ((v0 g0 + v1 g1) + v2 g2), then the
+// R2C of the sum: the three physical derivatives and the product never
+// reach HBM.  Arithmetic of k_real_x MODE_C2R / MODE_R2C (bit-identical to
+// three pfcs_irfft_x + pfcs_real_pointwise kind 2 + pfcs_rfft_x).
+#ifndef PFCS_XDOT_MINB
+#define PFCS_XDOT_MINB 1  // CTAs per SM the register cap aims for (2: 128 registers with 284 B of spills, 2.80 vs 2.61 ms)
+#endif
+template <int M, int T>
+__global__ void __launch_bounds__(T*(M / 8), PFCS_XDOT_MINB)
+    k_xdot3(double2* out, i64 inner, const double2* __restrict__ twN, double scale,
+            const __grid_constant__ TmaPair tm, const double* __restrict__ v0, const double* __restrict__ v1,
+            const double* __restrict__ v2) {
+  pdl_wait();
+  constexpr int R = 8;
+  constexpr int P = M / R;
+  constexpr int LS = real_ls(M, T);
+  using XS = XStage<M, T, MODE_C2R>;
+  extern __shared__ unsigned char draw[];
+  unsigned char* dbase = draw + ((1024u - (smem_u32(draw) & 1023u)) & 1023u);
+  double2* stage0 = (double2*)dbase;
+  double2* stage1 = (double2*)(dbase + XS::PADDED);
+  double2* smem = (double2*)(dbase + 2 * XS::PADDED);  // FFT workspace
+  unsigned long long* bars = (unsigned long long*)(smem + (size_t)T * LS);
+  const int tid = threadIdx.x;
+  const int t = tid % T;
+  const int j = tid / T;
+  const i64 ntiles = (inner + T - 1) / T;
+
+  auto issue = [&](i64 tile, int sub, int sidx) {
+    const int i0 = (int)(tile * T);
+    unsigned char* dst = (unsigned char*)(sidx ? stage1 : stage0);
+    mbar_expect_tx(&bars[sidx], (unsigned)XS::BYTES);
+#pragma unroll
+    for (int b = 0; b < XS::NB; ++b)
+      tma_load_2d(dst + (size_t)b * XS::BR * T * 16, &tm.a, &bars[sidx], 2 * i0, sub * (M + 1) + b * XS::BR);
+    tma_load_2d(dst + (size_t)M * T * 16, &tm.b, &bars[sidx], 2 * i0, sub * (M + 1) + M);
+  };
+  if (tid == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  if (tid == 0 && blockIdx.x < ntiles) issue(blockIdx.x, 0, 0);
+  int it = 0;
+  for (i64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const i64 i = tile * T + t;
+    const bool ok = i < inner;
+    double2 acc[R];
+    const double2* cur = stage0;
+#pragma unroll 1
+    for (int sub = 0; sub < 3; ++sub, ++it) {
+      const int sidx = it & 1;
+      if (tid == 0) {
+        const i64 ntile = sub < 2 ? tile : tile + gridDim.x;
+        if (ntile < ntiles) {
+          fence_proxy_async();  // the other stage was read by every thread before the last barrier
+          issue(ntile, sub < 2 ? sub + 1 : 0, sidx ^ 1);
+        }
+      }
+      mbar_wait(&bars[sidx], (unsigned)((it >> 1) & 1));
+      cur = sidx ? stage1 : stage0;
+      const int jj = opaque(j);
+      double2* sl = smem + t * LS;
+      double2 v[R];
+#pragma unroll
+      for (int e = 0; e < R; ++e) v[e] = cur[(jj + P * e) * T + t];
+      // C2R (k_real_x MODE_C2R, mirror rows from the stage)
+      const double2 wj = __ldg(&twN[jj]);
+#pragma unroll
+      for (int e = 0; e < R; ++e) {
+        const int k = jj + P * e;
+        double2 a = v[e];
+        double2 bm = cur[(M - k) * T + t];  // row M for k = 0
+        if (k == 0) {
+          a.y = 0.0;
+          bm.y = 0.0;
+        }
+        const double2 b = make_double2(bm.x, -bm.y);
+        const double2 sm = cadd(a, b);
+        const double2 d = csub(a, b);
+        const double2 w = twiddle_k<R>(twN, wj, jj, e, P);
+        const double2 wd = make_double2(fma(d.x, w.x, d.y * w.y), fma(d.y, w.x, -d.x * w.y));
+        v[e] = make_double2(sm.x - wd.y, sm.y + wd.x);
+      }
+      fft_line<M, false, 2, PFCS_X_TWL, R>(v, jj, sl, twN);
+      // this sub-pass's velocity samples (rows 2m, 2m+1)
+      const double* vp = sub == 0 ? v0 : (sub == 1 ? v1 : v2);
+      double2 vf[R];
+#pragma unroll
+      for (int e = 0; e < R; ++e) {
+        const i64 m = jj + P * e;
+        vf[e] = ok ? make_double2(__ldg(vp + (2 * m) * inner + i), __ldg(vp + (2 * m + 1) * inner + i))
+                   : make_double2(0.0, 0.0);
+      }
+#pragma unroll
+      for (int e = 0; e < R; ++e) {
+        const double gx = v[e].x * scale, gy = v[e].y * scale;
+        if (sub == 0) {
+          acc[e] = make_double2(__dmul_rn(vf[e].x, gx), __dmul_rn(vf[e].y, gy));
+        } else {
+          acc[e] = make_double2(__dadd_rn(acc[e].x, __dmul_rn(vf[e].x, gx)),
+                                __dadd_rn(acc[e].y, __dmul_rn(vf[e].y, gy)));
+        }
+      }
+      if (sub < 2) __syncthreads();  // stage and workspace free for the next sub-pass
+    }
+    // R2C of the sum (k_real_x MODE_R2C's forward FFT and split; the last
+    // sub-pass's stage pairs Z_k with Z_{M-k}: it is refilled only after the
+    // end-of-tile barrier)
+    const int j2 = opaque(j);
+    double2* sl = smem + t * LS;
+    fft_line<M, true, 2, PFCS_X_TWL, R>(acc, j2, sl, twN);
+    const double2 wj = __ldg(&twN[j2]);
+    double2* stg = const_cast<double2*>(cur);
+#pragma unroll
+    for (int e = 0; e < R; ++e) stg[(j2 + P * e) * T + t] = acc[e];
+    __syncthreads();
+#pragma unroll
+    for (int e = 0; e < R; ++e) {
+      const int k = j2 + P * e;
+      const double2 zk = acc[e];
+      const double2 zm = stg[((M - k) & (M - 1)) * T + t];
+      double2 x;
+      if (k == 0) {
+        x = make_double2(zk.x + zk.y, 0.0);
+      } else {
+        const double2 sp = make_double2(zk.x + zm.x, zk.y - zm.y);
+        const double2 d = make_double2(zk.x - zm.x, zk.y + zm.y);
+        const double2 w = twiddle_k<R>(twN, wj, j2, e, P);
+        const double2 wd = make_double2(fma(d.x, w.x, -d.y * w.y), fma(d.x, w.y, d.y * w.x));
+        x = make_double2(0.5 * (sp.x + wd.y), 0.5 * (sp.y - wd.x));
+      }
+      if (ok) out[(i64)k * inner + i] = x;
+    }
+    if (j2 == 0 && ok) out[(i64)M * inner + i] = make_double2(acc[0].x - acc[0].y, 0.0);
+    __syncthreads();
+  }
+}
+
+template <int M>
+static int xdot3_m(const double2* spec3, const double* v0, const double* v1, const double* v2, double2* out,
+                   i64 inner, cudaStream_t st) {
+  constexpr int T = 8;  // 128-byte complex rows, as the cube pass at M = 256
+  using XS = XStage<M, T, MODE_C2R>;
+  static_assert(XS::SMEM <= 227 * 1024, "stage + workspace fit");
+  if (2 * inner >= (1LL << 31) || ((uintptr_t)spec3 & 15)) return 1;
+  const double2* twN = twiddles(2 * M);
+  if (!twN) return PFCS_E_CUDA;
+  TmaPair tm{};
+  const unsigned long long dims[2] = {(unsigned long long)(2 * inner), (unsigned long long)(3 * (M + 1))};
+  const unsigned long long str[1] = {(unsigned long long)inner * 16};
+  const unsigned box[2] = {(unsigned)(2 * T), (unsigned)XS::BR};
+  const unsigned box1[2] = {(unsigned)(2 * T), 1u};
+  if (!make_tmap(&tm.a, 2, spec3, dims, str, box) || !make_tmap(&tm.b, 2, spec3, dims, str, box1)) return 1;
+  const i64 ntiles = (inner + T - 1) / T;
+  int grid = 0;
+  auto kern = k_xdot3<M, T>;
+  if (int rc = persistent_grid((const void*)kern, T * (M / 8), XS::SMEM, ntiles, &grid)) return rc;
+  launch_pdl(kern, dim3(grid), dim3(T * (M / 8)), XS::SMEM, st, out, inner, twN, 1.0 / (double)(2 * M), tm, v0, v1,
+             v2);
+  return check_launch("k_xdot3");
+}
+
+// returns 1 when not applicable (the caller runs the three C2R passes, the
+// pointwise kernel and the R2C pass instead)
+bool xdot3_supported(long long nx, long long inner) {
+  return tma_enabled() && (nx == 256 || nx == 512) && inner >= 0 && 2 * inner < (1LL << 31);
+}
+
+int launch_xdot3(const void* spec3, const double* v0, const double* v1, const double* v2, void* out, long long nx,
+                 long long inner, cudaStream_t st) {
+  if (inner <= 0) return PFCS_OK;
+  if (!xdot3_supported(nx, inner)) return 1;
+  switch (nx) {
+    case 256: return xdot3_m<128>((const double2*)spec3, v0, v1, v2, (double2*)out, inner, st);
+    case 512: return xdot3_m<256>((const double2*)spec3, v0, v1, v2, (double2*)out, inner, st);
+    default: return 1;
+  }
+}
+
 // ------------------------------------------- line-synchronous cube pass --
 // Same arithmetic as k_real_x<M, T, 3, MODE_CUBE> (bit-identical), different
 // execution: the CTA-wide barriers of the interleaved tile made all 16 warps

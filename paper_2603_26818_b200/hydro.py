@@ -348,6 +348,8 @@ _R2C_UPD = os.environ.get("PFCS_R2C_UPD", "1") != "0"  # updates fused into the 
 _R2C_GRAD = os.environ.get("PFCS_R2C_GRAD", "1") != "0"
 # the force product in one fused x pass (_Real3.prod_grad; A/B, bit-identical)
 _R2C_XMUL = os.environ.get("PFCS_R2C_XMUL", "1") != "0"
+# the advection dot product in one fused x pass (_Real3.adv_fwd; A/B, bit-identical)
+_R2C_XDOT = os.environ.get("PFCS_R2C_XDOT", "1") != "0"
 
 
 def _is_real(x) -> bool:
@@ -462,7 +464,7 @@ class _Real3:
         nat.call("pfcs_irfft_x", nat.ptr(tmp), nat.ptr(out), nx, ny * nz, st)
         return out
 
-    def _grad_zy(self, h: torch.Tensor, axes) -> list:
+    def _grad_zy(self, h: torch.Tensor, axes, outs=None) -> list:
         """The inverse z and y passes of F^-1(i d_a h) for each a in axes
         (x-halved spectra, before the x pass).  k_x and k_y are constant
         along z lines, so the x and y derivatives share ONE plain inverse z
@@ -475,9 +477,9 @@ class _Real3:
         nh = self.nh
         st = nat.stream_ptr()
         share = ny > 1 and _R2C_GRAD
-        t0, outs = None, []
-        for a in axes:
-            tmp = torch.empty_like(h)
+        t0, given, outs = None, outs, []
+        for n_a, a in enumerate(axes):
+            tmp = given[n_a] if given is not None else torch.empty_like(h)
             if share and a != 2:
                 if t0 is None:
                     t0 = torch.empty_like(h)
@@ -502,6 +504,29 @@ class _Real3:
             nat.call("pfcs_irfft_x", nat.ptr(tmp), nat.ptr(out), nx, ny * nz, st)
             outs.append(out)
         return outs
+
+    def adv_fwd(self, x_hat: torch.Tensor, v) -> torch.Tensor:
+        """F(v . grad x) (hydro.py:83-85): _grad_zy's inverse z / y passes
+        into one stacked buffer, ONE fused x pass (pfcs_xdot3_x: the three
+        C2R, the dot product with v, the R2C — the physical derivatives and
+        the product never reach HBM), the forward y and z passes.
+        Bit-identical to fwd(_grad_dot_r(self, x_hat, v)), which runs when
+        PFCS_R2C_XDOT=0 or the shape has no fused kernel."""
+        nx, ny, nz = self.shape
+        if not (_R2C_XDOT and nat.load().pfcs_xdot3_supported(nx, ny * nz)):
+            return self.fwd(_grad_dot_r(self, x_hat, v))
+        st = nat.stream_ptr()
+        spec3 = torch.empty((3,) + self.hshape, dtype=torch.complex128, device=x_hat.device)
+        self._grad_zy(x_hat, (0, 1, 2), outs=[spec3[0], spec3[1], spec3[2]])
+        out = torch.empty(self.hshape, dtype=torch.complex128, device=x_hat.device)
+        vs = [_rdev(x) for x in v]
+        nat.call("pfcs_xdot3_x", nat.ptr(spec3), nat.ptr(vs[0]), nat.ptr(vs[1]), nat.ptr(vs[2]), nat.ptr(out),
+                 nx, ny * nz, st)
+        if ny > 1:
+            nat.call("pfcs_fft_axis_c2c", nat.ptr(out), nat.ptr(out), self.nh, ny, nz, 1, 1, st)
+        if nz > 1:
+            nat.call("pfcs_fft_axis_c2c", nat.ptr(out), nat.ptr(out), self.nh, ny, nz, 2, 1, st)
+        return out
 
     def prod_grad(self, h: torch.Tensor, aux: torch.Tensor, axes=(0, 1, 2)) -> list:
         """[F(aux * F^-1(i d_a h)) for a in axes] — the hydro force
@@ -568,9 +593,9 @@ def _adv_term_r(R: _Real3, x_hat: torch.Tensor, axis: int, v_axis: torch.Tensor)
     return _rpw(RPW_MUL, v_axis, R.inv(x_hat, deriv=axis))
 
 
-def _density_r(R: _Real3, ph, ps, adv, sym, hp: HydroParams, flag: _StepFlag):
+def _density_r(R: _Real3, ph, ps, adv_hat, sym, hp: HydroParams, flag: _StepFlag):
+    """adv_hat = F(v . grad psi) (R.adv_fwd, or R.fwd of a physical sum)."""
     nl_hat = R.fwd(ps, RPW_CUBE)
-    adv_hat = R.fwd(adv)
     return R.update_inv(0, ph, nl_hat, adv_hat, (float(sym.eps), float(hp.pfc.dt)), flag)
 
 
@@ -612,7 +637,7 @@ def _serial_hydro_step_r(fields: HydroFields, sym: SymbolTable, params: HydroPar
     vh = [_hdev(x) for x in fields.v_hat]
     _check_half(R, ph, *vh)
     vs = [_rdev(v) for v in fields.v]
-    psi_hat, psi = _density_r(R, ph, ps, _grad_dot_r(R, ph, vs), sym, params, flag)
+    psi_hat, psi = _density_r(R, ph, ps, R.adv_fwd(ph, vs), sym, params, flag)
     mu_hat = _density_mu_r(R, psi, sym)  # shared by the three components
     forces = R.prod_grad(mu_hat, psi)
     out = [_velocity_r(R, vh[i], psi, i, mu_hat, sym, params, flag, force=forces[i]) for i in range(3)]
@@ -636,7 +661,7 @@ def _parallel_hydro_step_r(worker, role_state: dict, sym: SymbolTable, params: H
     if rank == 0:
         ph = role_state["psi_hat"]
         _check_half(R, ph)
-        psi_hat, psi = _density_r(R, ph, psi0, _grad_dot_r(R, ph, role_state["v"]), sym, params, flag)
+        psi_hat, psi = _density_r(R, ph, psi0, R.adv_fwd(ph, role_state["v"]), sym, params, flag)
         flag.check(idx, psi_hat)
         role_state["psi_hat"], role_state["psi"] = psi_hat, psi
         for dst in (1, 2, 3):

@@ -53,7 +53,7 @@ from . import _native as nat
 from .grid import SymbolTable
 from .hydro import (HydroParams, TAG_PSI, V_TAGS, RPW_ADD3, RPW_CHNL, _check_half, _dev, _Diag, _Real3, _StepFlag,
                     _adv_term_r,
-                    _density_mu_r, _density_r, _fft, _fft_cmul, _fft_cube, _grad_dot_r, _hdev, _ifft_deriv, _is_real,
+                    _density_mu_r, _density_r, _fft, _fft_cmul, _fft_cube, _hdev, _ifft_deriv, _is_real,
                     _out, _raise_divergence, _rdev, _rpw, _vectors, _velocity_r)
 
 __all__ = [
@@ -328,7 +328,7 @@ def parallel_multi_step(worker, st: dict, sym: SymbolTable, params: MultiParams)
 # ------------------------------------------------------------ R2C path ------
 
 def _composition_r(R: _Real3, ch, cc, v, sym, params: MultiParams, flag: _StepFlag):
-    adv_hat = R.fwd(_grad_dot_r(R, ch, v))
+    adv_hat = R.adv_fwd(ch, v)
     f_hat = R.fwd(cc, RPW_CHNL, alpha=params.alpha)
     return R.update_inv(2, ch, f_hat, adv_hat,
                         (float(params.mobility), float(params.kappa), float(params.hydro.pfc.dt)), flag)
@@ -353,7 +353,7 @@ def _serial_multi_step_r(fields: MultiFields, sym: SymbolTable, params: MultiPar
     vh = [_hdev(x) for x in fields.v_hat]
     _check_half(R, ph, ch, *vh)
     vs = [_rdev(v) for v in fields.v]
-    psi_hat, psi = _density_r(R, ph, ps, _grad_dot_r(R, ph, vs), sym, params.hydro, flag)
+    psi_hat, psi = _density_r(R, ph, ps, R.adv_fwd(ph, vs), sym, params.hydro, flag)
     c_hat, c = _composition_r(R, ch, cc, vs, sym, params, flag)
     mu_hat = _density_mu_r(R, psi, sym)
     muc = _composition_mu_r(R, c, c_hat, params) if params.beta != 0.0 else None
@@ -388,10 +388,10 @@ def _parallel_multi_step_r(worker, st: dict, sym: SymbolTable, params: MultiPara
             for h in (5, 6, 7):
                 worker.send_tensor(h, TAG_PSIHAT, ph)
             p = [worker.recv_tensor(5 + i, ADV_TAGS[i], torch.empty_like(st["psi"])) for i in range(3)]
-            adv = _rpw(RPW_ADD3, *p)
+            adv_hat = R.fwd(_rpw(RPW_ADD3, *p))
         else:
-            adv = _grad_dot_r(R, ph, st["v"])
-        st["psi_hat"], st["psi"] = _density_r(R, ph, st["psi"], adv, sym, params.hydro, flag)
+            adv_hat = R.adv_fwd(ph, st["v"])
+        st["psi_hat"], st["psi"] = _density_r(R, ph, st["psi"], adv_hat, sym, params.hydro, flag)
         flag.check(idx, st["psi_hat"])
         for dst in (1, 2, 3):
             worker.send_tensor(dst, TAG_PSI, st["psi"])

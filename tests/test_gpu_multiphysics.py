@@ -262,8 +262,9 @@ def test_r2c_fused_prologues_bit_identical(pkg, tmp_path):
     """The pointwise prologues fused into the R2C x pass (psi^3, psi * g,
     alpha (c^3 - c): pfcs_rfft_x_pro) and the psi / velocity / composition
     updates fused into the z pass of the following inverse
-    (pfcs_update_zinv) and the force products in one fused x pass
-    (pfcs_xmul_x) reproduce the unfused form (pfcs_real_pointwise +
+    (pfcs_update_zinv), the force products and the advection dot products
+    in one fused x pass each (pfcs_xmul_x, pfcs_xdot3_x) reproduce the
+    unfused form (pfcs_real_pointwise +
     pfcs_rfft_x; the standalone update kernels + the plain inverse) bit for
     bit."""
     import os
@@ -275,7 +276,7 @@ def test_r2c_fused_prologues_bit_identical(pkg, tmp_path):
     res = {}
     for flag in ("0", "1"):
         path = str(tmp_path / f"pro{flag}.npz")
-        env = dict(os.environ, PFCS_R2C_PRO=flag, PFCS_R2C_UPD=flag, PFCS_R2C_XMUL=flag)
+        env = dict(os.environ, PFCS_R2C_PRO=flag, PFCS_R2C_UPD=flag, PFCS_R2C_XMUL=flag, PFCS_R2C_XDOT=flag)
         subprocess.run([sys.executable, "-c", PRO_CHILD.format(root=str(here.parent), tests=str(here), path=path)],
                        check=True, env=env, timeout=600)
         res[flag] = np.load(path)

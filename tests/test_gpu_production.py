@@ -440,3 +440,43 @@ def test_xmul_x_production(torch_cuda, nx, inner):
     assert torch.equal(fused, two)
     want = sfft.rfft(sfft.irfft(spec, n=nx, axis=0, workers=WORKERS) * g, axis=0, workers=WORKERS)
     assert rel_l2(fused.cpu().numpy(), want) <= TOL
+
+
+@pytest.mark.parametrize("nx,inner", [(512, 7104), (512, 7110), (256, 3000), (256, 40)])
+def test_xdot3_x_production(torch_cuda, nx, inner):
+    """pfcs_xdot3_x (the advection x pass: three C2R, (v0 g0 + v1 g1) + v2 g2,
+    R2C) at production and small tiles: bit-identical to three
+    pfcs_irfft_x + pfcs_real_pointwise kind 2 + pfcs_rfft_x, and vs scipy
+    <= 1e-12; nx without the fused kernel is reported, not run."""
+    import scipy.fft as sfft
+
+    torch, nat = torch_cuda, _nat()
+    assert nat.load().pfcs_xdot3_supported(nx, inner) == 1
+    assert nat.load().pfcs_xdot3_supported(1024, inner) == 0
+    rng = np.random.default_rng(nx * 3 + inner)
+    nh = nx // 2 + 1
+    spec = rng.standard_normal((3, nh, inner)) + 1j * rng.standard_normal((3, nh, inner))
+    vel = [rng.standard_normal((nx, inner)) for _ in range(3)]
+    vd = [_to(torch, x) for x in vel]
+    st = nat.stream_ptr()
+    sd = _to(torch, spec)
+    fused = torch.empty((nh, inner), dtype=torch.complex128, device="cuda")
+    nat.call("pfcs_xdot3_x", nat.ptr(sd), nat.ptr(vd[0]), nat.ptr(vd[1]), nat.ptr(vd[2]), nat.ptr(fused), nx, inner,
+             st)
+    g = []
+    for a in range(3):
+        ga = torch.empty((nx, inner), dtype=torch.float64, device="cuda")
+        nat.call("pfcs_irfft_x", nat.ptr(sd[a].contiguous()), nat.ptr(ga), nx, inner, st)
+        g.append(ga)
+    prod = torch.empty_like(g[0])
+    nat.call("pfcs_real_pointwise", 2, nat.ptr(vd[0]), nat.ptr(g[0]), nat.ptr(vd[1]), nat.ptr(g[1]), nat.ptr(vd[2]),
+             nat.ptr(g[2]), nat.ptr(prod), prod.numel(), 0.0, st)
+    two = torch.empty_like(fused)
+    nat.call("pfcs_rfft_x", nat.ptr(prod), nat.ptr(two), nx, inner, st)
+    assert torch.equal(fused, two)
+    phys = [sfft.irfft(spec[a], n=nx, axis=0, workers=WORKERS) for a in range(3)]
+    want = sfft.rfft((vel[0] * phys[0] + vel[1] * phys[1]) + vel[2] * phys[2], axis=0, workers=WORKERS)
+    assert rel_l2(fused.cpu().numpy(), want) <= TOL
+    with pytest.raises(Exception):
+        nat.call("pfcs_xdot3_x", nat.ptr(sd), nat.ptr(vd[0]), nat.ptr(vd[1]), nat.ptr(vd[2]), nat.ptr(fused), 1024,
+                 inner // 2, st)

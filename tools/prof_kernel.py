@@ -56,6 +56,16 @@ def main():
         fn = lambda: nat.call("pfcs_fft_axis_c2c_pro", nat.ptr(a), nat.ptr(b), nh, n, n, ax, 0, 3, nat.ptr(d), aa, st)
     elif kind == "zlines":
         fn = lambda: nat.call("pfcs_fft_zlines", nat.ptr(a), nat.ptr(a), nh * n, n, 1, 1, 1, st)
+    elif kind == "xdot3":  # fused advection x pass over three stacked derivative spectra
+        s3 = torch.empty(3 * nh * n * n, dtype=C, device="cuda")
+        s3.real.normal_()
+        s3.imag.normal_()
+        vv = [torch.randn(n * n * n, dtype=torch.float64, device="cuda") for _ in range(3)]
+        fn = lambda: nat.call("pfcs_xdot3_x", nat.ptr(s3), nat.ptr(vv[0]), nat.ptr(vv[1]), nat.ptr(vv[2]),
+                              nat.ptr(a), n, n * n, st)
+    elif kind == "xmul":
+        g = torch.randn(n * n * n, dtype=torch.float64, device="cuda")
+        fn = lambda: nat.call("pfcs_xmul_x", nat.ptr(a), nat.ptr(g), n, n * n, st)
     elif kind == "strided_oop":
         b = torch.empty_like(a)
         fn = lambda: nat.call("pfcs_fft_axis_c2c", nat.ptr(a), nat.ptr(b), nh, n, n, 1, 0, st)
