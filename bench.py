@@ -499,21 +499,29 @@ def run_pfc2d(ctx, args):
 
 
 def multi_bytes(n: int) -> float:
-    """Algorithmic HBM bytes of one serial R2C multiphysics step (beta = 0):
-    23 transforms of R + 5S; the real pointwise work — the two v . grad x
-    passes (6 reads + 1 write: 2 x 7R) and the second factor the three
-    psi * g products read inside their transforms' first pass (3 x R; the
-    cubes and alpha (c^3 - c) ride in their transforms' loads for free) =
-    17R; the spectral updates / mu (psi 4S, c 4S, mu 3S, 3 x velocity 3S =
-    20S), less the five state updates' re-read of the new state, which ride
-    in the z pass of their inverse transform (pfcs_update_zinv: -5S), and
-    less one z pass (2S) per gradient — grad psi, grad c, grad mu: the x and
-    y derivatives share one inverse z pass (_Real3.grad_inv: -6S), and less
-    the physical derivative's write and re-read in each of the three forces
-    psi F^-1(i k mu) (one fused C2R * psi R2C x pass, pfcs_xmul_x: -6R)."""
+    """Algorithmic HBM bytes of one serial R2C multiphysics step (beta = 0),
+    R = 8 n^3 (a real field), S = spec_bytes(n) (a half spectrum), as the
+    fused schedule moves them:
+      * 23 transforms of R + 5S (R + S for the x pass, 2S for y and z each)
+        = 23R + 115S;
+      * the real pointwise work of the unfused schedule, 17R: the two
+        v . grad x products (6 reads + 1 write each: 14R) and the second
+        factor psi of the three forces (3R);
+      * less what the fused x passes keep out of HBM: each force
+        (pfcs_xmul_x: C2R, * psi, R2C in one pass) the derivative's write
+        and re-read (3 x -2R), each advection (pfcs_xdot3_x: three C2R, the
+        dot product, the R2C in one pass) the three derivatives' writes and
+        re-reads, the product's write and re-read (2 x -8R: its 3R of
+        velocity reads remain);
+      * the spectral updates / mu: psi 4S, c 4S, mu 3S, 3 x velocity 3S = 20S,
+        less the five state updates' re-read of the new state (they ride in
+        the z pass of their inverse, pfcs_update_zinv: -5S);
+      * one z pass (2S) less per gradient (grad psi, grad c, grad mu: the x
+        and y derivatives share one inverse z pass, _Real3.grad_inv: -6S).
+    Total 18R + 124S."""
     R = 8.0 * n**3
     S = spec_bytes(n)
-    return 23 * (R + 5 * S) + 11 * R + 9 * S
+    return 23 * (R + 5 * S) + (17 - 6 - 16) * R + (20 - 5 - 6) * S
 
 
 def run_multi(ctx, args):
