@@ -580,8 +580,8 @@ def run_multi(ctx, args):
         alg = multi_bytes(n)
         res["roofline"] = {"bound": "hbm", "alg_bytes_per_step": alg, "achieved": round(alg / (ms * 1e-3) / 1e9, 1),
                            "peak": hbm, "unit": "GB/s", "frac": round(alg / (ms * 1e-3) / 1e9 / hbm, 4),
-                           "model": "23 R2C transforms x (R + 5S) + 17R real pointwise (fused prologues) + "
-                                    "20S spectral updates"}
+                           "model": "fused schedule, 18R + 124S per step (R a real field, S a half spectrum; "
+                                    "pass-by-pass in bench.multi_bytes)"}
         # e2e: host psi, c (pinned) in -> forward transforms -> K steps -> psi, c, v out
         hp_in = [x.cpu().pin_memory() for x in (psi, c)]
         outs = [torch.empty_like(hp_in[0]).pin_memory() for _ in range(5)]
