@@ -151,6 +151,14 @@ int pfcs_xmul_x(void* data, const double* aux, int64_t nx, int64_t inner, void* 
  * inner) says whether this build / setting has the fused kernel
  * (PFCS_E_UNSUPPORTED otherwise). */
 int pfcs_xdot3_supported(int64_t nx, int64_t inner);
+/* mu_hat of hydro_velocity_step (hydro.py:99-101) fused with the forward z
+ * passes of its operands: nl_xy, f_xy = F(psi^3) and F(psi) after their x
+ * and y passes ((n0, n1, n2) complex, z contiguous); mu = nl + op(k) f with
+ * op = eps + ((1-k2)^2)((4/3-k2)^2) — bit-identical to pfcs_fft_axis_c2c
+ * (axis 2, forward) on both, then pfcs_hydro_mu.  Other z lengths run that
+ * form (transforming nl_xy and f_xy in place). */
+int pfcs_hydro_mu_z(const void* nl_xy, const void* f_xy, void* mu, int64_t n0, int64_t n1, int64_t n2,
+                    const double* kx, const double* ky, const double* kz, double eps, void* stream);
 int pfcs_xdot3_x(const void* spec3, const double* v0, const double* v1, const double* v2, void* out, int64_t nx,
                  int64_t inner, void* stream);
 

@@ -440,6 +440,83 @@ int launch_lines_to(const double2* in, double2* out, long long nlines, int n, in
   return fail(PFCS_E_UNSUPPORTED, "unsupported line length");
 }
 
+// mu_hat of hydro_velocity_step (hydro.py:99-101) fused with the forward z
+// passes of its two operands: per z line, the x/y-transformed lines of
+// F(psi^3) and F(psi) are z-transformed in registers (the standalone forward
+// z pass's arithmetic) and combined as pfcs_hydro_mu does,
+//   mu = nl + (eps + ((1-k2)(1-k2)) ((4/3-k2)(4/3-k2))) f,
+// so neither operand spectrum reaches HBM: 2S read + S written instead of
+// two z passes (4S) and the mu pass (3S).
+#ifndef PFCS_MUZ_TARGET
+#define PFCS_MUZ_TARGET 512  // resident threads per SM the register cap aims for (two line register sets)
+#endif
+template <int N>
+__global__ void __launch_bounds__(N / radix_R(N), min_blocks(N / radix_R(N), PFCS_MUZ_TARGET))
+    k_mu_z(const double2* __restrict__ nl, const double2* __restrict__ f, double2* mu, i64 nlines, int n1,
+           const double* __restrict__ kx, const double* __restrict__ ky, const double* __restrict__ kz, double eps,
+           const double2* __restrict__ tw) {
+  pdl_wait();
+  constexpr int R = radix_R(N);
+  constexpr int P = N / R;
+  extern __shared__ double2 smem[];
+  const int j = threadIdx.x;
+  for (i64 l = blockIdx.x; l < nlines; l += gridDim.x) {
+    double2 a[R], b[R];
+#pragma unroll
+    for (int e = 0; e < R; ++e) {
+      a[e] = nl[l * N + j + P * e];
+      b[e] = f[l * N + j + P * e];
+    }
+    const int jj = opaque(j);
+    fft_line<N, true, 1, PFCS_LINES_TWL>(a, jj, smem, tw);
+    const int j2 = opaque(jj);
+    fft_line<N, true, 1, PFCS_LINES_TWL>(b, j2, smem, tw);
+    const i64 lx = l / n1;
+    const int ly = (int)(l - lx * n1);
+    const double ka = __ldg(kx + lx), kb = __ldg(ky + ly);
+    const double kxy = __dadd_rn(__dmul_rn(ka, ka), __dmul_rn(kb, kb));
+#pragma unroll
+    for (int e = 0; e < R; ++e) {
+      const int z = j2 + P * e;
+      const double kc = __ldg(kz + z);
+      const double k2 = __dadd_rn(kxy, __dmul_rn(kc, kc));
+      const double p1 = __dsub_rn(1.0, k2);
+      const double p2 = __dsub_rn(4.0 / 3.0, k2);
+      const double op = __dadd_rn(eps, __dmul_rn(__dmul_rn(p1, p1), __dmul_rn(p2, p2)));
+      mu[l * N + z] = make_double2(__dadd_rn(a[e].x, __dmul_rn(op, b[e].x)), __dadd_rn(a[e].y, __dmul_rn(op, b[e].y)));
+    }
+  }
+}
+
+template <int N>
+static int mu_z_n(const double2* nl, const double2* f, double2* mu, i64 nlines, int n1, const double* kx,
+                  const double* ky, const double* kz, double eps, cudaStream_t st) {
+  const double2* tw = twiddles(N);
+  if (!tw) return PFCS_E_CUDA;
+  constexpr int P = N / radix_R(N);
+  const size_t smem = (size_t)tile_ls(N, 1, false) * sizeof(double2);
+  int grid = 0;
+  if (int rc = persistent_grid((const void*)k_mu_z<N>, P, smem, nlines, &grid)) return rc;
+  launch_pdl(k_mu_z<N>, dim3(grid), dim3(P), smem, st, nl, f, mu, nlines, n1, kx, ky, kz, eps, tw);
+  return check_launch("k_mu_z");
+}
+
+// returns 1 when not applicable (z length not a power of two in [8, 4096])
+int launch_mu_z(const double2* nl, const double2* f, double2* mu, long long nlines, int n1, int n, const double* kx,
+                const double* ky, const double* kz, double eps, cudaStream_t st) {
+  if (nlines <= 0) return PFCS_OK;
+  switch (n) {
+#define PFCS_MU_CASE(NN) \
+  case NN:               \
+    return mu_z_n<NN>(nl, f, mu, nlines, n1, kx, ky, kz, eps, st);
+    PFCS_MU_CASE(8) PFCS_MU_CASE(16) PFCS_MU_CASE(32) PFCS_MU_CASE(64) PFCS_MU_CASE(128) PFCS_MU_CASE(256)
+    PFCS_MU_CASE(512) PFCS_MU_CASE(1024) PFCS_MU_CASE(2048) PFCS_MU_CASE(4096)
+#undef PFCS_MU_CASE
+    default:
+      return 1;
+  }
+}
+
 // Plain contiguous lines with a fused prologue; returns 1 when not
 // applicable (non-power-of-two length).
 int launch_lines_pro(const double2* in, double2* out, long long nlines, int n, const Pro& pro, bool forward,

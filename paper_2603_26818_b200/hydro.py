@@ -350,6 +350,8 @@ _R2C_GRAD = os.environ.get("PFCS_R2C_GRAD", "1") != "0"
 _R2C_XMUL = os.environ.get("PFCS_R2C_XMUL", "1") != "0"
 # the advection dot product in one fused x pass (_Real3.adv_fwd; A/B, bit-identical)
 _R2C_XDOT = os.environ.get("PFCS_R2C_XDOT", "1") != "0"
+# mu_hat with its operands' forward z passes (pfcs_hydro_mu_z; A/B, bit-identical)
+_R2C_MUZ = os.environ.get("PFCS_R2C_MUZ", "1") != "0"
 
 
 def _is_real(x) -> bool:
@@ -399,10 +401,11 @@ class _Real3:
         return cache[key]
 
     def fwd(self, x: torch.Tensor, kind: int | None = None, aux: torch.Tensor | None = None,
-            alpha: float = 0.0) -> torch.Tensor:
+            alpha: float = 0.0, z: bool = True) -> torch.Tensor:
         """F[x], or F[f(x)] with f a pfcs_real_pointwise kind (0 cube, 1 x*aux,
         3 alpha (x^3 - x)) fused into the first (x) pass (PFCS_R2C_PRO=0:
-        the product in its own pass, bit-identical)."""
+        the product in its own pass, bit-identical).  z=False stops before
+        the z pass (for a consumer that fuses it)."""
         nx, ny, nz = self.shape
         out = torch.empty(self.hshape, dtype=torch.complex128, device=x.device)
         st = nat.stream_ptr()
@@ -416,7 +419,7 @@ class _Real3:
                      nat.ptr(aux) if aux is not None else None, float(alpha), st)
         if ny > 1:
             nat.call("pfcs_fft_axis_c2c", nat.ptr(out), nat.ptr(out), self.nh, ny, nz, 1, 1, st)
-        if nz > 1:
+        if nz > 1 and z:
             nat.call("pfcs_fft_axis_c2c", nat.ptr(out), nat.ptr(out), self.nh, ny, nz, 2, 1, st)
         return out
 
@@ -600,13 +603,17 @@ def _density_r(R: _Real3, ph, ps, adv_hat, sym, hp: HydroParams, flag: _StepFlag
 
 
 def _density_mu_r(R: _Real3, ps, sym) -> torch.Tensor:
+    """mu_hat = F(psi^3) + op F(psi) (hydro.py:99-101); the two forward z
+    passes fused with the combination (pfcs_hydro_mu_z; PFCS_R2C_MUZ=0: the
+    z passes and pfcs_hydro_mu separately, bit-identical)."""
     nh, ny, nz = R.hshape
     kx, ky, kz = R.k
-    nl_hat = R.fwd(ps, RPW_CUBE)
-    f_hat = R.fwd(ps)
+    nl_hat = R.fwd(ps, RPW_CUBE, z=not _R2C_MUZ)
+    f_hat = R.fwd(ps, z=not _R2C_MUZ)
     mu = torch.empty_like(nl_hat)
-    nat.call("pfcs_hydro_mu", nat.ptr(nl_hat), nat.ptr(f_hat), nat.ptr(mu), nh, ny, nz, nat.ptr(kx), nat.ptr(ky),
-             nat.ptr(kz), float(sym.eps), nat.stream_ptr())
+    fn = "pfcs_hydro_mu_z" if _R2C_MUZ else "pfcs_hydro_mu"
+    nat.call(fn, nat.ptr(nl_hat), nat.ptr(f_hat), nat.ptr(mu), nh, ny, nz, nat.ptr(kx), nat.ptr(ky), nat.ptr(kz),
+             float(sym.eps), nat.stream_ptr())
     return mu
 
 

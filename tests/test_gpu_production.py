@@ -480,3 +480,29 @@ def test_xdot3_x_production(torch_cuda, nx, inner):
     with pytest.raises(Exception):
         nat.call("pfcs_xdot3_x", nat.ptr(sd), nat.ptr(vd[0]), nat.ptr(vd[1]), nat.ptr(vd[2]), nat.ptr(fused), 1024,
                  inner // 2, st)
+
+
+@pytest.mark.parametrize("shape", [(257, 64, 512), (9, 12, 1024), (5, 6, 12)])
+def test_hydro_mu_z(torch_cuda, shape):
+    """pfcs_hydro_mu_z (mu_hat with its operands' forward z passes fused) ==
+    two forward z passes + pfcs_hydro_mu, bit for bit (fused kernel on
+    power-of-two z; the two-pass form otherwise)."""
+    torch, nat = torch_cuda, _nat()
+    rng = np.random.default_rng(sum(shape))
+    n0, n1, n2 = shape
+    nl = _to(torch, rng.standard_normal(shape) + 1j * rng.standard_normal(shape))
+    f = _to(torch, rng.standard_normal(shape) + 1j * rng.standard_normal(shape))
+    kx, ky, kz = (_to(torch, rng.standard_normal(m)) for m in shape)
+    st = nat.stream_ptr()
+    mu = torch.empty_like(nl)
+    nl_in, f_in = nl.clone(), f.clone()  # (the two-pass fallback transforms its operands in place)
+    nat.call("pfcs_hydro_mu_z", nat.ptr(nl_in), nat.ptr(f_in), nat.ptr(mu), n0, n1, n2, nat.ptr(kx), nat.ptr(ky),
+             nat.ptr(kz), -0.3, st)
+    a, b = nl.clone(), f.clone()
+    nat.call("pfcs_fft_axis_c2c", nat.ptr(a), nat.ptr(a), n0, n1, n2, 2, 1, st)
+    nat.call("pfcs_fft_axis_c2c", nat.ptr(b), nat.ptr(b), n0, n1, n2, 2, 1, st)
+    want = torch.empty_like(nl)
+    nat.call("pfcs_hydro_mu", nat.ptr(a), nat.ptr(b), nat.ptr(want), n0, n1, n2, nat.ptr(kx), nat.ptr(ky),
+             nat.ptr(kz), -0.3, st)
+    torch.cuda.synchronize()
+    assert torch.equal(mu, want)

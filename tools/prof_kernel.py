@@ -66,6 +66,13 @@ def main():
     elif kind == "xmul":
         g = torch.randn(n * n * n, dtype=torch.float64, device="cuda")
         fn = lambda: nat.call("pfcs_xmul_x", nat.ptr(a), nat.ptr(g), n, n * n, st)
+    elif kind == "mu_z":  # mu_hat with its operands' forward z passes
+        f2 = a.clone()
+        mu = torch.empty_like(a)
+        kxv = torch.linspace(0, 1, nh, dtype=torch.float64, device="cuda")
+        kyv = torch.linspace(0, 1, n, dtype=torch.float64, device="cuda")
+        fn = lambda: nat.call("pfcs_hydro_mu_z", nat.ptr(a), nat.ptr(f2), nat.ptr(mu), nh, n, n, nat.ptr(kxv),
+                              nat.ptr(kyv), nat.ptr(kyv), -0.3, st)
     elif kind == "strided_oop":
         b = torch.empty_like(a)
         fn = lambda: nat.call("pfcs_fft_axis_c2c", nat.ptr(a), nat.ptr(b), nh, n, n, 1, 0, st)
