@@ -426,6 +426,22 @@ __global__ void __launch_bounds__(T*(M / 8), PFCS_XDOT_MINB)
   }
   __syncthreads();
   if (tid == 0 && blockIdx.x < ntiles) issue(blockIdx.x, 0, 0);
+  // velocity samples (rows 2m, 2m+1) of sub-pass `sub` of `tile`, loaded one
+  // sub-pass ahead (a load consumed right after its FFT exposed its latency:
+  // long_scoreboard was the top stall)
+  auto load_v = [&](i64 tl, int sub, double2 (&dst)[R]) {
+    const double* vp = sub == 0 ? v0 : (sub == 1 ? v1 : v2);
+    const i64 ii = tl * T + t;
+    const bool okk = tl < ntiles && ii < inner;
+#pragma unroll
+    for (int e = 0; e < R; ++e) {
+      const i64 m = j + P * e;
+      dst[e] = okk ? make_double2(__ldg(vp + (2 * m) * inner + ii), __ldg(vp + (2 * m + 1) * inner + ii))
+                   : make_double2(0.0, 0.0);
+    }
+  };
+  double2 vf[R];
+  load_v(blockIdx.x, 0, vf);
   int it = 0;
   for (i64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const i64 i = tile * T + t;
@@ -449,6 +465,9 @@ __global__ void __launch_bounds__(T*(M / 8), PFCS_XDOT_MINB)
       double2 v[R];
 #pragma unroll
       for (int e = 0; e < R; ++e) v[e] = cur[(jj + P * e) * T + t];
+      double2 vn[R];  // the next sub-pass's velocities, in flight during this one
+      if (sub < 2) load_v(tile, sub + 1, vn);
+      else load_v(tile + gridDim.x, 0, vn);
       // C2R (k_real_x MODE_C2R, mirror rows from the stage)
       const double2 wj = __ldg(&twN[jj]);
 #pragma unroll
@@ -468,15 +487,6 @@ __global__ void __launch_bounds__(T*(M / 8), PFCS_XDOT_MINB)
         v[e] = make_double2(sm.x - wd.y, sm.y + wd.x);
       }
       fft_line<M, false, 2, PFCS_X_TWL, R>(v, jj, sl, twN);
-      // this sub-pass's velocity samples (rows 2m, 2m+1)
-      const double* vp = sub == 0 ? v0 : (sub == 1 ? v1 : v2);
-      double2 vf[R];
-#pragma unroll
-      for (int e = 0; e < R; ++e) {
-        const i64 m = jj + P * e;
-        vf[e] = ok ? make_double2(__ldg(vp + (2 * m) * inner + i), __ldg(vp + (2 * m + 1) * inner + i))
-                   : make_double2(0.0, 0.0);
-      }
 #pragma unroll
       for (int e = 0; e < R; ++e) {
         const double gx = v[e].x * scale, gy = v[e].y * scale;
@@ -487,6 +497,8 @@ __global__ void __launch_bounds__(T*(M / 8), PFCS_XDOT_MINB)
                                 __dadd_rn(acc[e].y, __dmul_rn(vf[e].y, gy)));
         }
       }
+#pragma unroll
+      for (int e = 0; e < R; ++e) vf[e] = vn[e];
       if (sub < 2) __syncthreads();  // stage and workspace free for the next sub-pass
     }
     // R2C of the sum (k_real_x MODE_R2C's forward FFT and split; the last
@@ -525,7 +537,10 @@ __global__ void __launch_bounds__(T*(M / 8), PFCS_XDOT_MINB)
 template <int M>
 static int xdot3_m(const double2* spec3, const double* v0, const double* v1, const double* v2, double2* out,
                    i64 inner, cudaStream_t st) {
-  constexpr int T = 8;  // 128-byte complex rows, as the cube pass at M = 256
+#ifndef PFCS_XDOT_T
+#define PFCS_XDOT_T 8
+#endif
+  constexpr int T = PFCS_XDOT_T;  // lines per tile (8: 128-byte complex rows, as the cube pass at M = 256)
   using XS = XStage<M, T, MODE_C2R>;
   static_assert(XS::SMEM <= 227 * 1024, "stage + workspace fit");
   if (2 * inner >= (1LL << 31) || ((uintptr_t)spec3 & 15)) return 1;
