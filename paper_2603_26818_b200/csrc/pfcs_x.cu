@@ -119,9 +119,12 @@ struct XStage {
   static constexpr size_t SMEM = 2 * PADDED + (size_t)T * real_ls(M, T) * 16 + 16 + 1024;
 };
 
+#ifndef PFCS_XMUL_TARGET
+#define PFCS_XMUL_TARGET 256  // resident threads per SM of the TMA-staged product x pass (512: 128 registers, 120 B spills, 1.01 vs 0.88 ms)
+#endif
 template <int M, int T, int ST, int MODE>
 __global__ void __launch_bounds__(T*(M / real_R(M, MODE)),
-                                  min_blocks(T*(M / real_R(M, MODE)), ST == 3 ? 512 : (MODE == 2 ? PFCS_CUBE_TARGET : (ST == 2 ? 640 : 768))))
+                                  min_blocks(T*(M / real_R(M, MODE)), ST == 3 ? (MODE == MODE_XMUL ? PFCS_XMUL_TARGET : 512) : (MODE == 2 ? PFCS_CUBE_TARGET : (ST == 2 ? 640 : 768))))
     k_real_x(const void* in_, void* out_, i64 inner, const double2* __restrict__ twN, double scale,
              double* diag, const __grid_constant__ TmaPair tm, RPro rp = RPro{}) {
   pdl_wait();
@@ -144,7 +147,8 @@ __global__ void __launch_bounds__(T*(M / real_R(M, MODE)),
   double2* sl = smem + t * LS;
   const i64 ntiles = (inner + T - 1) / T;
   double m_abs = 0.0;
-  using Regs = RegsX<R, MODE == MODE_R2C_PRO>;
+  constexpr bool AXR = MODE == MODE_R2C_PRO || MODE == MODE_XMUL;  // Regs carry the product factors
+  using Regs = RegsX<R, AXR>;
 
   auto load = [&](i64 tile, Regs& r) {
     const i64 i = tile * T + t;
@@ -164,6 +168,7 @@ __global__ void __launch_bounds__(T*(M / real_R(M, MODE)),
       for (int e = 0; e < R; ++e) {
         const i64 k = j + P * e;
         r.v[e] = ok ? in[k * inner + i] : make_double2(0.0, 0.0);
+        if constexpr (MODE == MODE_XMUL) r.ax[e] = rpro_factor(rp, k, i, inner, ok);  // applied in comp
       }
       r.xm = (ok && j == 0) ? in[(i64)M * inner + i] : make_double2(0.0, 0.0);
     }
@@ -184,12 +189,12 @@ __global__ void __launch_bounds__(T*(M / real_R(M, MODE)),
           v[e] = make_double2(rpro_apply(rp, v[e].x, r.ax[e].x), rpro_apply(rp, v[e].y, r.ax[e].y));
       }
     }
-    // MODE_XMUL: the factors of rows 2m, 2m+1, loaded before the inverse
-    // FFT so their latency hides behind it
+    // MODE_XMUL: the factors of rows 2m, 2m+1 (loaded with the tile, or
+    // one tile ahead on the TMA path)
     double2 xf[MODE == MODE_XMUL ? R : 1];
     if constexpr (MODE == MODE_XMUL) {
 #pragma unroll
-      for (int e = 0; e < R; ++e) xf[e] = rpro_factor(rp, jj + P * e, i, inner, ok);
+      for (int e = 0; e < R; ++e) xf[e] = r.ax[e];
     }
     if (!is_r2c(MODE)) {
       // Z'[k] = (X_k + conj X_{M-k}) + i W_N^{-k} (X_k - conj X_{M-k});
@@ -327,10 +332,10 @@ __global__ void __launch_bounds__(T*(M / real_R(M, MODE)),
     __syncthreads();
     i64 tile = blockIdx.x;
     if (tid == 0 && tile < ntiles) issue(tile, 0);
-    // MODE_R2C_PRO: the product factors of the tile, loaded one tile ahead
-    double2 axn[MODE == MODE_R2C_PRO ? R : 1];
+    // MODE_R2C_PRO / MODE_XMUL: the product factors of the tile, loaded one tile ahead
+    double2 axn[AXR ? R : 1];
     auto aux_ahead = [&](i64 tl) {
-      if constexpr (MODE == MODE_R2C_PRO) {
+      if constexpr (AXR) {
 #pragma unroll
         for (int e = 0; e < R; ++e) axn[e] = rpro_factor(rp, j + P * e, tl * T + t, inner, tl * T + t < inner);
       }
@@ -368,6 +373,11 @@ __global__ void __launch_bounds__(T*(M / real_R(M, MODE)),
       } else {
 #pragma unroll
         for (int e = 0; e < R; ++e) r.v[e] = cur[(j + P * e) * T + t];
+        if constexpr (MODE == MODE_XMUL) {
+#pragma unroll
+          for (int e = 0; e < R; ++e) r.ax[e] = axn[e];
+          aux_ahead(tile + gridDim.x);  // in flight during comp
+        }
       }
       comp(tile, r);
       __syncthreads();
