@@ -665,18 +665,18 @@ def _parallel_hydro_step_r(worker, role_state: dict, sym: SymbolTable, params: H
     R = _Real3.of(tuple(psi0.shape), sym, psi0.device)
     flag = _StepFlag(psi0.device)
     idx = role_state["step_index"]
+    worker.bcast_groups([(0, 1, 2, 3)])  # psi -> the velocity ranks: one broadcast (hydro.py:114-116)
     if rank == 0:
         ph = role_state["psi_hat"]
         _check_half(R, ph)
         psi_hat, psi = _density_r(R, ph, psi0, R.adv_fwd(ph, role_state["v"]), sym, params, flag)
         flag.check(idx, psi_hat)
         role_state["psi_hat"], role_state["psi"] = psi_hat, psi
-        for dst in (1, 2, 3):
-            worker.send_tensor(dst, TAG_PSI, psi)
+        worker.bcast_tensor(0, (0, 1, 2, 3), TAG_PSI, t=psi)
         role_state["v"] = [worker.recv_tensor(i + 1, V_TAGS[i], torch.empty_like(psi)) for i in range(3)]
     else:
         i = rank - 1
-        psi = worker.recv_tensor(0, TAG_PSI, torch.empty_like(psi0))
+        psi = worker.bcast_tensor(0, (0, 1, 2, 3), TAG_PSI, out=torch.empty_like(psi0))
         role_state["psi"] = psi
         _check_half(R, role_state["v_hat"])
         v_hat, v = _velocity_r(R, role_state["v_hat"], psi, i, _density_mu_r(R, psi, sym), sym, params, flag)

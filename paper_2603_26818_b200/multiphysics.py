@@ -382,48 +382,49 @@ def _parallel_multi_step_r(worker, st: dict, sym: SymbolTable, params: MultiPara
     R = _Real3.of(tuple(like.shape), sym, like.device)
     _check_half(R, *(st[k] for k in ("psi_hat", "c_hat", "v_hat") if k in st))
     flag = _StepFlag(like.device)
+    # one-to-many messages as broadcasts over fixed rank sets (declared
+    # collectively, in the same order, on every rank)
+    s_psi, s_psih, s_c = (0, 1, 2, 3), (0, 5, 6, 7), (1, 2, 3, 4)
+    s_v = [(0, 1 + i, 4) + ((5 + i,) if G == 8 else ()) for i in range(3)]
+    worker.bcast_groups([s_psi, *s_v] + ([s_psih] if G == 8 else []) + ([s_c] if beta else []))
     if role == "psi":
         ph = st["psi_hat"]
         if G == 8:
-            for h in (5, 6, 7):
-                worker.send_tensor(h, TAG_PSIHAT, ph)
+            worker.bcast_tensor(0, s_psih, TAG_PSIHAT, t=ph)
             p = [worker.recv_tensor(5 + i, ADV_TAGS[i], torch.empty_like(st["psi"])) for i in range(3)]
             adv_hat = R.fwd(_rpw(RPW_ADD3, *p))
         else:
             adv_hat = R.adv_fwd(ph, st["v"])
         st["psi_hat"], st["psi"] = _density_r(R, ph, st["psi"], adv_hat, sym, params.hydro, flag)
         flag.check(idx, st["psi_hat"])
-        for dst in (1, 2, 3):
-            worker.send_tensor(dst, TAG_PSI, st["psi"])
-        st["v"] = [worker.recv_tensor(1 + i, V_TAGS[i], torch.empty_like(st["psi"])) for i in range(3)]
+        worker.bcast_tensor(0, s_psi, TAG_PSI, t=st["psi"])
+        st["v"] = [worker.bcast_tensor(1 + i, s_v[i], V_TAGS[i], out=torch.empty_like(st["psi"]))
+                   for i in range(3)]
     elif role == "c":
         st["c_hat"], st["c"] = _composition_r(R, st["c_hat"], st["c"], st["v"], sym, params, flag)
         flag.check(idx, st["c_hat"])
         if beta:
-            for dst in (1, 2, 3):
-                worker.send_tensor(dst, TAG_C, st["c"])
-                worker.send_tensor(dst, TAG_CHAT, st["c_hat"])
-        st["v"] = [worker.recv_tensor(1 + i, V_TAGS[i], torch.empty_like(st["c"])) for i in range(3)]
+            worker.bcast_tensor(4, s_c, TAG_C, t=st["c"])
+            worker.bcast_tensor(4, s_c, TAG_CHAT, t=st["c_hat"])
+        st["v"] = [worker.bcast_tensor(1 + i, s_v[i], V_TAGS[i], out=torch.empty_like(st["c"])) for i in range(3)]
     elif role.startswith("v"):
         i = int(role[1]) - 1
-        psi = worker.recv_tensor(0, TAG_PSI, torch.empty_like(st["psi"]))
+        psi = worker.bcast_tensor(0, s_psi, TAG_PSI, out=torch.empty_like(st["psi"]))
         st["psi"] = psi
         muc = None
         if beta:
-            st["c"] = worker.recv_tensor(4, TAG_C, torch.empty_like(st["c"]))
-            st["c_hat"] = worker.recv_tensor(4, TAG_CHAT, torch.empty_like(st["c_hat"]))
+            st["c"] = worker.bcast_tensor(4, s_c, TAG_C, out=torch.empty_like(st["c"]))
+            st["c_hat"] = worker.bcast_tensor(4, s_c, TAG_CHAT, out=torch.empty_like(st["c_hat"]))
             muc = _composition_mu_r(R, st["c"], st["c_hat"], params)
         mu_hat = _density_mu_r(R, psi, sym)
         st["v_hat"], st["v_own"] = _velocity_r(R, st["v_hat"], psi, i, mu_hat, sym, params.hydro, flag, st.get("c"),
                                                 muc, params.beta)
         flag.check(idx, st["v_hat"])
-        dsts = (0, 4) + ((5 + i,) if G == 8 else ())
-        for dst in dsts:
-            worker.send_tensor(dst, V_TAGS[i], st["v_own"])
+        worker.bcast_tensor(1 + i, s_v[i], V_TAGS[i], t=st["v_own"])
     else:  # advection helper (G = 8)
         i = int(role[3]) - 1
-        ph = worker.recv_tensor(0, TAG_PSIHAT, torch.empty_like(st["psi_hat"]))
+        ph = worker.bcast_tensor(0, s_psih, TAG_PSIHAT, out=torch.empty_like(st["psi_hat"]))
         worker.send_tensor(0, ADV_TAGS[i], _adv_term_r(R, ph, i, st["v_own"]))
-        st["v_own"] = worker.recv_tensor(1 + i, V_TAGS[i], torch.empty_like(st["v_own"]))
+        st["v_own"] = worker.bcast_tensor(1 + i, s_v[i], V_TAGS[i], out=torch.empty_like(st["v_own"]))
     st["step_index"] = idx + 1
     return st

@@ -273,6 +273,21 @@ class Worker:
         out.copy_(t, non_blocking=True)
         return out
 
+    def bcast_groups(self, sets: Sequence[Sequence[int]]) -> None:
+        """Declare the broadcast rank sets (collective on process groups;
+        nothing to set up in a thread group)."""
+
+    def bcast_tensor(self, root: int, ranks: Sequence[int], tag: int, t=None, out=None):
+        """``root`` sends ``t`` to every other member of ``ranks`` (all
+        members call it; receivers pass ``out``); returns the member's copy.
+        In a thread group: one reference handoff per receiver."""
+        if self.rank == root:
+            for r in ranks:
+                if r != root:
+                    self.send_tensor(r, tag, t)
+            return t
+        return self.recv_tensor(root, tag, out)
+
 
 class ProcessWorker:
     """Worker over ``torch.distributed`` (one process per GPU).
@@ -371,6 +386,42 @@ class ProcessWorker:
             cache[key] = (ProcessWorker(rows[c][1], self.device, rows[c][0]),
                           ProcessWorker(cols[r][1], self.device, cols[r][0]))
         return cache[key]
+
+    def bcast_groups(self, sets: Sequence[Sequence[int]]) -> None:
+        """Create the communicators of the broadcast rank sets (group ranks).
+        Collective: every rank of the group calls it with the same sets in
+        the same order (torch.distributed.new_group semantics); cached."""
+        cache = self.__dict__.setdefault("_bcast", {})
+        for ranks in sets:
+            key = tuple(sorted(int(r) for r in ranks))
+            if key in cache:
+                continue
+            if len(key) == self._size:
+                cache[key] = self.pg
+            else:
+                cache[key] = self._dist.new_group([self._global[r] for r in key])
+
+    def bcast_tensor(self, root: int, ranks: Sequence[int], tag: int, t=None, out=None):
+        """``root`` broadcasts ``t`` to the other members of ``ranks`` (all
+        members call it; receivers pass ``out``): one NCCL broadcast over the
+        set's communicator instead of a send per receiver, so the root's
+        link carries the field once (NCCL pipelines it through the members
+        or the switch).  The set must have been declared with
+        bcast_groups."""
+        key = tuple(sorted(int(r) for r in ranks))
+        group = self.__dict__.get("_bcast", {}).get(key, "missing")
+        if group == "missing":
+            raise TransportError(f"bcast_tensor: rank set {key} was not declared with bcast_groups")
+        buf = t.contiguous() if self.rank == root else out
+        src = self._global[root]
+        if self.backend == "nccl":
+            self._dist.broadcast(buf, src=src, group=group)
+        else:  # gloo: stage through host memory
+            host = buf.cpu() if buf.is_cuda else buf
+            self._dist.broadcast(host, src=src, group=group)
+            if host is not buf:
+                buf.copy_(host)
+        return buf
 
     def send_tensor(self, dst: int, tag: int, t) -> None:
         if self.backend == "nccl":

@@ -121,3 +121,48 @@ def test_slab_all_to_all_bookkeeping(world):
         assert isinstance(res, dict), res
         for key, (fwd_ok, inv_ok) in res.items():
             assert fwd_ok and inv_ok, key
+
+
+def _bcast(rank, world):
+    """ProcessWorker.bcast_tensor over declared rank sets (the role maps'
+    psi -> velocities and v_i -> (psi, c, helper) broadcasts), with the
+    same call order on every member, plus an undeclared set."""
+    from paper_2603_26818_b200.transport import ProcessWorker, TransportError
+
+    w = ProcessWorker()
+    sets = [(0, 1, 2, 3), (0, 1, 4), (0, 2, 4), (0, 3, 4)][: 1 if world == 4 else 4]
+    w.bcast_groups(sets)
+    got = {}
+    x = torch.full((5,), 10.0 + rank, dtype=torch.float64)
+    if rank in (0, 1, 2, 3):
+        out = w.bcast_tensor(0, (0, 1, 2, 3), 2, t=x if rank == 0 else None,
+                             out=None if rank == 0 else torch.empty(5, dtype=torch.float64))
+        got["psi"] = out.tolist()
+    if world == 5:
+        for i in range(3):
+            s = sets[1 + i]
+            if rank in s:
+                root = 1 + i
+                out = w.bcast_tensor(root, s, 4 + i, t=x if rank == root else None,
+                                     out=None if rank == root else torch.empty(5, dtype=torch.float64))
+                got[f"v{i}"] = out.tolist()
+    try:
+        w.bcast_tensor(0, (0, 3), 9, t=x, out=x)
+        got["undeclared"] = "no error"
+    except TransportError:
+        got["undeclared"] = "error"
+    return got
+
+
+@pytest.mark.parametrize("world", [4, 5])
+def test_process_worker_bcast(world):
+    res = spawn(_bcast, world)
+    for r, got in enumerate(res):
+        assert isinstance(got, dict), got
+        assert got["undeclared"] == "error"
+        if r < 4:
+            assert got["psi"] == [10.0] * 5
+        if world == 5:
+            for i in range(3):
+                if r in (0, 1 + i, 4):
+                    assert got[f"v{i}"] == [11.0 + i] * 5
