@@ -520,11 +520,14 @@ def multi_bytes(n: int) -> float:
         and y derivatives share one inverse z pass, _Real3.grad_inv: -6S);
       * mu fused with its two operands' forward z passes (pfcs_hydro_mu_z:
         2S read, S written instead of the two z passes' 4S and the mu
-        pass's 3S: -4S).
-    Total 18R + 120S."""
+        pass's 3S: -4S);
+      * the density update's F(psi^3) carried over from the previous step's
+        mu (same psi: one forward transform, R + 5S, less per step; the
+        fused mu kernel writes it, +S: -R - 4S).
+    Total 17R + 116S."""
     R = 8.0 * n**3
     S = spec_bytes(n)
-    return 23 * (R + 5 * S) + (17 - 6 - 16) * R + (20 - 5 - 6 - 4) * S
+    return 23 * (R + 5 * S) + (17 - 6 - 16 - 1) * R + (20 - 5 - 6 - 4 - 4) * S
 
 
 def run_multi(ctx, args):
@@ -583,7 +586,7 @@ def run_multi(ctx, args):
         alg = multi_bytes(n)
         res["roofline"] = {"bound": "hbm", "alg_bytes_per_step": alg, "achieved": round(alg / (ms * 1e-3) / 1e9, 1),
                            "peak": hbm, "unit": "GB/s", "frac": round(alg / (ms * 1e-3) / 1e9 / hbm, 4),
-                           "model": "fused schedule, 18R + 120S per step (R a real field, S a half spectrum; "
+                           "model": "fused schedule, 17R + 116S per step (R a real field, S a half spectrum; "
                                     "pass-by-pass in bench.multi_bytes)"}
         # e2e: host psi, c (pinned) in -> forward transforms -> K steps -> psi, c, v out
         hp_in = [x.cpu().pin_memory() for x in (psi, c)]

@@ -155,10 +155,12 @@ int pfcs_xdot3_supported(int64_t nx, int64_t inner);
  * passes of its operands: nl_xy, f_xy = F(psi^3) and F(psi) after their x
  * and y passes ((n0, n1, n2) complex, z contiguous); mu = nl + op(k) f with
  * op = eps + ((1-k2)^2)((4/3-k2)^2) — bit-identical to pfcs_fft_axis_c2c
- * (axis 2, forward) on both, then pfcs_hydro_mu.  Other z lengths run that
- * form (transforming nl_xy and f_xy in place). */
-int pfcs_hydro_mu_z(const void* nl_xy, const void* f_xy, void* mu, int64_t n0, int64_t n1, int64_t n2,
-                    const double* kx, const double* ky, const double* kz, double eps, void* stream);
+ * (axis 2, forward) on both, then pfcs_hydro_mu.  nl_out (or NULL)
+ * receives the finished F(psi^3) (the next step's density update reads the
+ * same spectrum of the same psi).  Other z lengths run the unfused form
+ * (transforming f_xy, and nl_xy when nl_out is NULL, in place). */
+int pfcs_hydro_mu_z(const void* nl_xy, const void* f_xy, void* mu, void* nl_out, int64_t n0, int64_t n1,
+                    int64_t n2, const double* kx, const double* ky, const double* kz, double eps, void* stream);
 int pfcs_xdot3_x(const void* spec3, const double* v0, const double* v1, const double* v2, void* out, int64_t nx,
                  int64_t inner, void* stream);
 

@@ -66,7 +66,7 @@ _SIGS = {
     "pfcs_rfft_x_pro": [_c_p, _c_p, _c_i64, _c_i64, _c_int, _c_p, _c_d, _c_p],
     "pfcs_xmul_x": [_c_p, _c_p, _c_i64, _c_i64, _c_p],
     "pfcs_xdot3_supported": [_c_i64, _c_i64],
-    "pfcs_hydro_mu_z": [_c_p, _c_p, _c_p, _c_i64, _c_i64, _c_i64, _c_p, _c_p, _c_p, _c_d, _c_p],
+    "pfcs_hydro_mu_z": [_c_p, _c_p, _c_p, _c_p, _c_i64, _c_i64, _c_i64, _c_p, _c_p, _c_p, _c_d, _c_p],
     "pfcs_xdot3_x": [_c_p, _c_p, _c_p, _c_p, _c_p, _c_i64, _c_i64, _c_p],
     "pfcs_pfc_cube_x": [_c_p, _c_i64, _c_i64, _c_int, _c_p, _c_p],
     "pfcs_pfc_update_z": [_c_p, _c_p, _c_p, _c_i64, _c_i64, _c_i64, _c_int, _c_int,

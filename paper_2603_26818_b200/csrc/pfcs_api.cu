@@ -180,8 +180,8 @@ int launch_rfft_x_pro(const double* in, void* out, long long nx, long long inner
                       double alpha, cudaStream_t st);
 int launch_xmul(void* data, const double* aux, long long nx, long long inner, cudaStream_t st);
 bool xdot3_supported(long long nx, long long inner);
-int launch_mu_z(const double2* nl, const double2* f, double2* mu, long long nlines, int n1, int n, const double* kx,
-                const double* ky, const double* kz, double eps, cudaStream_t st);
+int launch_mu_z(const double2* nl, const double2* f, double2* mu, double2* nl_out, long long nlines, int n1, int n,
+                const double* kx, const double* ky, const double* kz, double eps, cudaStream_t st);
 int launch_xdot3(const void* spec3, const double* v0, const double* v1, const double* v2, void* out, long long nx,
                  long long inner, cudaStream_t st);
 int launch_pfc_z(const double2* nl, double2* psi_hat, double2* next, long long cx, long long ny,
@@ -358,19 +358,21 @@ int pfcs_xmul_x(void* data, const double* aux, int64_t nx, int64_t inner, void* 
   return launch_xmul(data, aux, nx, inner, S(stream));
 }
 
-int pfcs_hydro_mu_z(const void* nl_xy, const void* f_xy, void* mu, int64_t n0, int64_t n1, int64_t n2,
-                    const double* kx, const double* ky, const double* kz, double eps, void* stream) {
+int pfcs_hydro_mu_z(const void* nl_xy, const void* f_xy, void* mu, void* nl_out, int64_t n0, int64_t n1,
+                    int64_t n2, const double* kx, const double* ky, const double* kz, double eps, void* stream) {
   if (!nl_xy || !f_xy || !mu || !kx || !ky || !kz) return fail(PFCS_E_ARG, "null argument");
-  if (mu == nl_xy || mu == f_xy) return fail(PFCS_E_ARG, "mu must not alias the operands");
+  if (mu == nl_xy || mu == f_xy || (nl_out && (nl_out == mu || nl_out == f_xy)))
+    return fail(PFCS_E_ARG, "mu / nl_out must not alias the operands or each other");
   if (n0 < 0 || n1 < 0 || n2 < 0) return fail(PFCS_E_ARG, "negative extent");
   if (n0 * n1 * n2 == 0) return PFCS_OK;
-  const int rc = launch_mu_z((const double2*)nl_xy, (const double2*)f_xy, (double2*)mu, n0 * n1, (int)n1, (int)n2,
-                             kx, ky, kz, eps, S(stream));
+  const int rc = launch_mu_z((const double2*)nl_xy, (const double2*)f_xy, (double2*)mu, (double2*)nl_out, n0 * n1,
+                             (int)n1, (int)n2, kx, ky, kz, eps, S(stream));
   if (rc != 1) return rc;
-  // other z lengths: the two forward z passes in place, then the mu pass
-  if (int r = pfcs_fft_axis_c2c(nl_xy, (void*)nl_xy, n0, n1, n2, 2, 1, stream)) return r;
+  // other z lengths: the two forward z passes, then the mu pass
+  void* nlz = nl_out ? nl_out : (void*)nl_xy;
+  if (int r = pfcs_fft_axis_c2c(nl_xy, nlz, n0, n1, n2, 2, 1, stream)) return r;
   if (int r = pfcs_fft_axis_c2c(f_xy, (void*)f_xy, n0, n1, n2, 2, 1, stream)) return r;
-  return pfcs_hydro_mu(nl_xy, f_xy, mu, n0, n1, n2, kx, ky, kz, eps, stream);
+  return pfcs_hydro_mu(nlz, f_xy, mu, n0, n1, n2, kx, ky, kz, eps, stream);
 }
 
 int pfcs_xdot3_supported(int64_t nx, int64_t inner) { return xdot3_supported(nx, inner) ? 1 : 0; }

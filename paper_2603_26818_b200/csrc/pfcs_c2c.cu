@@ -452,9 +452,9 @@ int launch_lines_to(const double2* in, double2* out, long long nlines, int n, in
 #endif
 template <int N>
 __global__ void __launch_bounds__(N / radix_R(N), min_blocks(N / radix_R(N), PFCS_MUZ_TARGET))
-    k_mu_z(const double2* __restrict__ nl, const double2* __restrict__ f, double2* mu, i64 nlines, int n1,
-           const double* __restrict__ kx, const double* __restrict__ ky, const double* __restrict__ kz, double eps,
-           const double2* __restrict__ tw) {
+    k_mu_z(const double2* __restrict__ nl, const double2* __restrict__ f, double2* mu, double2* nl_out, i64 nlines,
+           int n1, const double* __restrict__ kx, const double* __restrict__ ky, const double* __restrict__ kz,
+           double eps, const double2* __restrict__ tw) {
   pdl_wait();
   constexpr int R = radix_R(N);
   constexpr int P = N / R;
@@ -484,31 +484,32 @@ __global__ void __launch_bounds__(N / radix_R(N), min_blocks(N / radix_R(N), PFC
       const double p2 = __dsub_rn(4.0 / 3.0, k2);
       const double op = __dadd_rn(eps, __dmul_rn(__dmul_rn(p1, p1), __dmul_rn(p2, p2)));
       mu[l * N + z] = make_double2(__dadd_rn(a[e].x, __dmul_rn(op, b[e].x)), __dadd_rn(a[e].y, __dmul_rn(op, b[e].y)));
+      if (nl_out) nl_out[l * N + z] = a[e];  // F(psi^3), for the next step's density update
     }
   }
 }
 
 template <int N>
-static int mu_z_n(const double2* nl, const double2* f, double2* mu, i64 nlines, int n1, const double* kx,
-                  const double* ky, const double* kz, double eps, cudaStream_t st) {
+static int mu_z_n(const double2* nl, const double2* f, double2* mu, double2* nl_out, i64 nlines, int n1,
+                  const double* kx, const double* ky, const double* kz, double eps, cudaStream_t st) {
   const double2* tw = twiddles(N);
   if (!tw) return PFCS_E_CUDA;
   constexpr int P = N / radix_R(N);
   const size_t smem = (size_t)tile_ls(N, 1, false) * sizeof(double2);
   int grid = 0;
   if (int rc = persistent_grid((const void*)k_mu_z<N>, P, smem, nlines, &grid)) return rc;
-  launch_pdl(k_mu_z<N>, dim3(grid), dim3(P), smem, st, nl, f, mu, nlines, n1, kx, ky, kz, eps, tw);
+  launch_pdl(k_mu_z<N>, dim3(grid), dim3(P), smem, st, nl, f, mu, nl_out, nlines, n1, kx, ky, kz, eps, tw);
   return check_launch("k_mu_z");
 }
 
 // returns 1 when not applicable (z length not a power of two in [8, 4096])
-int launch_mu_z(const double2* nl, const double2* f, double2* mu, long long nlines, int n1, int n, const double* kx,
-                const double* ky, const double* kz, double eps, cudaStream_t st) {
+int launch_mu_z(const double2* nl, const double2* f, double2* mu, double2* nl_out, long long nlines, int n1, int n,
+                const double* kx, const double* ky, const double* kz, double eps, cudaStream_t st) {
   if (nlines <= 0) return PFCS_OK;
   switch (n) {
 #define PFCS_MU_CASE(NN) \
   case NN:               \
-    return mu_z_n<NN>(nl, f, mu, nlines, n1, kx, ky, kz, eps, st);
+    return mu_z_n<NN>(nl, f, mu, nl_out, nlines, n1, kx, ky, kz, eps, st);
     PFCS_MU_CASE(8) PFCS_MU_CASE(16) PFCS_MU_CASE(32) PFCS_MU_CASE(64) PFCS_MU_CASE(128) PFCS_MU_CASE(256)
     PFCS_MU_CASE(512) PFCS_MU_CASE(1024) PFCS_MU_CASE(2048) PFCS_MU_CASE(4096)
 #undef PFCS_MU_CASE

@@ -24,6 +24,7 @@ from __future__ import annotations
 
 import math
 import os
+import weakref
 from dataclasses import dataclass, field as dataclass_field
 
 import numpy as np
@@ -352,6 +353,9 @@ _R2C_XMUL = os.environ.get("PFCS_R2C_XMUL", "1") != "0"
 _R2C_XDOT = os.environ.get("PFCS_R2C_XDOT", "1") != "0"
 # mu_hat with its operands' forward z passes (pfcs_hydro_mu_z; A/B, bit-identical)
 _R2C_MUZ = os.environ.get("PFCS_R2C_MUZ", "1") != "0"
+# serial steps carry F(psi^3) from one step's mu to the next step's density
+# update (same psi, same spectrum; A/B, bit-identical)
+_CARRY_NL = os.environ.get("PFCS_R2C_CARRY", "1") != "0"
 
 
 def _is_real(x) -> bool:
@@ -596,25 +600,53 @@ def _adv_term_r(R: _Real3, x_hat: torch.Tensor, axis: int, v_axis: torch.Tensor)
     return _rpw(RPW_MUL, v_axis, R.inv(x_hat, deriv=axis))
 
 
-def _density_r(R: _Real3, ph, ps, adv_hat, sym, hp: HydroParams, flag: _StepFlag):
-    """adv_hat = F(v . grad psi) (R.adv_fwd, or R.fwd of a physical sum)."""
-    nl_hat = R.fwd(ps, RPW_CUBE)
+def _density_r(R: _Real3, ph, ps, adv_hat, sym, hp: HydroParams, flag: _StepFlag, nl_hat=None):
+    """adv_hat = F(v . grad psi) (R.adv_fwd, or R.fwd of a physical sum);
+    nl_hat = F(psi^3) when the caller has it (the previous step's mu)."""
+    if nl_hat is None:
+        nl_hat = R.fwd(ps, RPW_CUBE)
     return R.update_inv(0, ph, nl_hat, adv_hat, (float(sym.eps), float(hp.pfc.dt)), flag)
 
 
-def _density_mu_r(R: _Real3, ps, sym) -> torch.Tensor:
+def _density_mu_r(R: _Real3, ps, sym, want_nl: bool = False):
     """mu_hat = F(psi^3) + op F(psi) (hydro.py:99-101); the two forward z
     passes fused with the combination (pfcs_hydro_mu_z; PFCS_R2C_MUZ=0: the
-    z passes and pfcs_hydro_mu separately, bit-identical)."""
+    z passes and pfcs_hydro_mu separately, bit-identical).  want_nl: also
+    return F(psi^3) — the next step's density update transforms the same
+    psi**3 (hydro.py:86 after :99), so the serial steps carry it over."""
     nh, ny, nz = R.hshape
     kx, ky, kz = R.k
     nl_hat = R.fwd(ps, RPW_CUBE, z=not _R2C_MUZ)
     f_hat = R.fwd(ps, z=not _R2C_MUZ)
     mu = torch.empty_like(nl_hat)
-    fn = "pfcs_hydro_mu_z" if _R2C_MUZ else "pfcs_hydro_mu"
-    nat.call(fn, nat.ptr(nl_hat), nat.ptr(f_hat), nat.ptr(mu), nh, ny, nz, nat.ptr(kx), nat.ptr(ky), nat.ptr(kz),
-             float(sym.eps), nat.stream_ptr())
-    return mu
+    st = nat.stream_ptr()
+    if _R2C_MUZ:
+        nl_out = torch.empty_like(nl_hat) if want_nl else None
+        nat.call("pfcs_hydro_mu_z", nat.ptr(nl_hat), nat.ptr(f_hat), nat.ptr(mu), nat.ptr(nl_out), nh, ny, nz,
+                 nat.ptr(kx), nat.ptr(ky), nat.ptr(kz), float(sym.eps), st)
+    else:
+        nat.call("pfcs_hydro_mu", nat.ptr(nl_hat), nat.ptr(f_hat), nat.ptr(mu), nh, ny, nz, nat.ptr(kx),
+                 nat.ptr(ky), nat.ptr(kz), float(sym.eps), st)
+        nl_out = nl_hat
+    return (mu, nl_out) if want_nl else mu
+
+
+def _nl_carry_get(fields, ps):
+    """F(psi^3) of `ps` carried over from the previous serial step (its mu),
+    or None: valid only while fields.psi is still that step's tensor,
+    unmodified (same object, same version counter)."""
+    c = fields.__dict__.get("_pfcs_nl")
+    if c is None or not _CARRY_NL:
+        return None
+    ref, version, nl = c
+    return nl if (ref() is ps and ps._version == version) else None
+
+
+def _nl_carry_put(fields, ps, nl) -> None:
+    if isinstance(ps, torch.Tensor) and _CARRY_NL:
+        fields.__dict__["_pfcs_nl"] = (weakref.ref(ps), ps._version, nl)
+    else:
+        fields.__dict__.pop("_pfcs_nl", None)
 
 
 def _velocity_r(R: _Real3, vh, ps, axis: int, mu_hat, sym, hp: HydroParams, flag: _StepFlag, cc=None,
@@ -644,12 +676,13 @@ def _serial_hydro_step_r(fields: HydroFields, sym: SymbolTable, params: HydroPar
     vh = [_hdev(x) for x in fields.v_hat]
     _check_half(R, ph, *vh)
     vs = [_rdev(v) for v in fields.v]
-    psi_hat, psi = _density_r(R, ph, ps, R.adv_fwd(ph, vs), sym, params, flag)
-    mu_hat = _density_mu_r(R, psi, sym)  # shared by the three components
+    psi_hat, psi = _density_r(R, ph, ps, R.adv_fwd(ph, vs), sym, params, flag, _nl_carry_get(fields, ps))
+    mu_hat, nl_next = _density_mu_r(R, psi, sym, want_nl=True)  # mu shared by the three components
     forces = R.prod_grad(mu_hat, psi)
     out = [_velocity_r(R, vh[i], psi, i, mu_hat, sym, params, flag, force=forces[i]) for i in range(3)]
     flag.check(fields.step_index, psi_hat, *(o[0] for o in out))
     fields.psi_hat, fields.psi = _out(psi_hat, host), _out(psi, host)
+    _nl_carry_put(fields, fields.psi, nl_next)
     for i in range(3):
         fields.v_hat[i], fields.v[i] = _out(out[i][0], host), _out(out[i][1], host)
     fields.step_index += 1

@@ -54,7 +54,8 @@ from .grid import SymbolTable
 from .hydro import (HydroParams, TAG_PSI, V_TAGS, RPW_ADD3, RPW_CHNL, _check_half, _dev, _Diag, _Real3, _StepFlag,
                     _adv_term_r,
                     _density_mu_r, _density_r, _fft, _fft_cmul, _fft_cube, _hdev, _ifft_deriv, _is_real,
-                    _out, _raise_divergence, _rdev, _rpw, _vectors, _velocity_r)
+                    _nl_carry_get, _nl_carry_put, _out, _raise_divergence, _rdev, _rpw, _vectors,
+                    _velocity_r)
 
 __all__ = [
     "MultiParams",
@@ -353,9 +354,9 @@ def _serial_multi_step_r(fields: MultiFields, sym: SymbolTable, params: MultiPar
     vh = [_hdev(x) for x in fields.v_hat]
     _check_half(R, ph, ch, *vh)
     vs = [_rdev(v) for v in fields.v]
-    psi_hat, psi = _density_r(R, ph, ps, R.adv_fwd(ph, vs), sym, params.hydro, flag)
+    psi_hat, psi = _density_r(R, ph, ps, R.adv_fwd(ph, vs), sym, params.hydro, flag, _nl_carry_get(fields, ps))
     c_hat, c = _composition_r(R, ch, cc, vs, sym, params, flag)
-    mu_hat = _density_mu_r(R, psi, sym)
+    mu_hat, nl_next = _density_mu_r(R, psi, sym, want_nl=True)
     muc = _composition_mu_r(R, c, c_hat, params) if params.beta != 0.0 else None
     forces = R.prod_grad(mu_hat, psi)
     forces_c = R.prod_grad(muc, c) if muc is not None else [None] * 3
@@ -365,6 +366,7 @@ def _serial_multi_step_r(fields: MultiFields, sym: SymbolTable, params: MultiPar
     for i in range(3):
         fields.v_hat[i], fields.v[i] = _out(out[i][0], host), _out(out[i][1], host)
     fields.psi_hat, fields.psi = _out(psi_hat, host), _out(psi, host)
+    _nl_carry_put(fields, fields.psi, nl_next)
     fields.c_hat, fields.c = _out(c_hat, host), _out(c, host)
     fields.step_index += 1
     fields.sim_time += params.hydro.pfc.dt

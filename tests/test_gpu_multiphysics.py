@@ -244,16 +244,26 @@ sys.path.insert(0, {tests!r})
 import paper_2603_26818_b200 as pkg
 from test_gpu_multiphysics import setup, to_real
 from paper_2603_26818_b200.multiphysics import serial_multi_step
+import torch
+def dev(x):
+    return torch.from_numpy(np.ascontiguousarray(x)).cuda()
+def host(x):
+    return x.cpu().numpy() if isinstance(x, torch.Tensor) else x
 out = {{}}
 for beta in (0.0, 0.5):
     grid, sym, mp, f = setup(pkg, n=32, beta=beta)
     r = to_real(f)
-    for _ in range(3):
+    if beta == 0.0:  # device-resident fields (the carried F(psi^3) applies to those)
+        r.psi, r.c, r.psi_hat, r.c_hat = dev(r.psi), dev(r.c), dev(r.psi_hat), dev(r.c_hat)
+        r.v, r.v_hat = [dev(x) for x in r.v], [dev(x) for x in r.v_hat]
+    for k in range(4):
         serial_multi_step(r, sym, mp)
+        if k == 1 and beta == 0.0:
+            r.psi.mul_(1.0001)  # an in-place edit must invalidate the carried F(psi^3)
     for k in ("psi", "c", "psi_hat", "c_hat"):
-        out[f"{{beta}}_{{k}}"] = getattr(r, k)
+        out[f"{{beta}}_{{k}}"] = host(getattr(r, k))
     for i in range(3):
-        out[f"{{beta}}_v{{i}}"] = r.v[i]
+        out[f"{{beta}}_v{{i}}"] = host(r.v[i])
 np.savez({path!r}, **out)
 """
 
@@ -263,8 +273,9 @@ def test_r2c_fused_prologues_bit_identical(pkg, tmp_path):
     alpha (c^3 - c): pfcs_rfft_x_pro) and the psi / velocity / composition
     updates fused into the z pass of the following inverse
     (pfcs_update_zinv), the force products and the advection dot products
-    in one fused x pass each (pfcs_xmul_x, pfcs_xdot3_x) reproduce the
-    unfused form (pfcs_real_pointwise +
+    in one fused x pass each (pfcs_xmul_x, pfcs_xdot3_x), the fused mu and
+    the F(psi^3) carried from one step's mu to the next step's density update
+    (invalidated by an in-place edit of psi) reproduce the unfused form (pfcs_real_pointwise +
     pfcs_rfft_x; the standalone update kernels + the plain inverse) bit for
     bit."""
     import os
@@ -277,7 +288,7 @@ def test_r2c_fused_prologues_bit_identical(pkg, tmp_path):
     for flag in ("0", "1"):
         path = str(tmp_path / f"pro{flag}.npz")
         env = dict(os.environ, PFCS_R2C_PRO=flag, PFCS_R2C_UPD=flag, PFCS_R2C_XMUL=flag, PFCS_R2C_XDOT=flag,
-                   PFCS_R2C_MUZ=flag)
+                   PFCS_R2C_MUZ=flag, PFCS_R2C_CARRY=flag)
         subprocess.run([sys.executable, "-c", PRO_CHILD.format(root=str(here.parent), tests=str(here), path=path)],
                        check=True, env=env, timeout=600)
         res[flag] = np.load(path)

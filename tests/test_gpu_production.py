@@ -496,8 +496,9 @@ def test_hydro_mu_z(torch_cuda, shape):
     st = nat.stream_ptr()
     mu = torch.empty_like(nl)
     nl_in, f_in = nl.clone(), f.clone()  # (the two-pass fallback transforms its operands in place)
-    nat.call("pfcs_hydro_mu_z", nat.ptr(nl_in), nat.ptr(f_in), nat.ptr(mu), n0, n1, n2, nat.ptr(kx), nat.ptr(ky),
-             nat.ptr(kz), -0.3, st)
+    nl_out = torch.empty_like(nl)
+    nat.call("pfcs_hydro_mu_z", nat.ptr(nl_in), nat.ptr(f_in), nat.ptr(mu), nat.ptr(nl_out), n0, n1, n2,
+             nat.ptr(kx), nat.ptr(ky), nat.ptr(kz), -0.3, st)
     a, b = nl.clone(), f.clone()
     nat.call("pfcs_fft_axis_c2c", nat.ptr(a), nat.ptr(a), n0, n1, n2, 2, 1, st)
     nat.call("pfcs_fft_axis_c2c", nat.ptr(b), nat.ptr(b), n0, n1, n2, 2, 1, st)
@@ -506,3 +507,4 @@ def test_hydro_mu_z(torch_cuda, shape):
              nat.ptr(kz), -0.3, st)
     torch.cuda.synchronize()
     assert torch.equal(mu, want)
+    assert torch.equal(nl_out, a)  # the finished F(psi^3) the next step reuses

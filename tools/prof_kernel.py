@@ -71,7 +71,7 @@ def main():
         mu = torch.empty_like(a)
         kxv = torch.linspace(0, 1, nh, dtype=torch.float64, device="cuda")
         kyv = torch.linspace(0, 1, n, dtype=torch.float64, device="cuda")
-        fn = lambda: nat.call("pfcs_hydro_mu_z", nat.ptr(a), nat.ptr(f2), nat.ptr(mu), nh, n, n, nat.ptr(kxv),
+        fn = lambda: nat.call("pfcs_hydro_mu_z", nat.ptr(a), nat.ptr(f2), nat.ptr(mu), None, nh, n, n, nat.ptr(kxv),
                               nat.ptr(kyv), nat.ptr(kyv), -0.3, st)
     elif kind == "strided_oop":
         b = torch.empty_like(a)
