@@ -428,11 +428,14 @@ class _Real3:
         return out
 
     def update_inv(self, kind: int, state: torch.Tensor, aux: torch.Tensor, aux2, c: tuple,
-                   flag: "_StepFlag") -> tuple:
+                   flag: "_StepFlag", keep_z: bool = False) -> tuple:
         """A spectral update fused with the first (z) pass of the inverse
         transform of its result (pfcs_update_zinv; kind 0 psi, 1 velocity,
         2 composition): returns (new state, F^-1 of it).  PFCS_R2C_UPD=0 runs
-        the standalone update kernel and the plain inverse (bit-identical)."""
+        the standalone update kernel and the plain inverse (bit-identical).
+        keep_z: also return the inverse z pass of the new state (or None) —
+        the shared z pass of the next step's gradient of that state
+        (_grad_zy), so the serial steps carry it over."""
         nx, ny, nz = self.shape
         nh = self.nh
         kx, ky, kz = self.k
@@ -444,17 +447,20 @@ class _Real3:
             consts = c[:2] if kind == 0 else c
             nat.call(name, *ops, nh, ny, nz, nat.ptr(kx), nat.ptr(ky), nat.ptr(kz), *(float(v) for v in consts),
                      nat.ptr(flag.t), st)
-            return new, self.inv(new)
+            return (new, self.inv(new), None) if keep_z else (new, self.inv(new))
         tmp = torch.empty_like(state)
         c3 = tuple(float(v) for v in c) + (0.0,) * (3 - len(c))
         nat.call("pfcs_update_zinv", kind, nat.ptr(state), nat.ptr(aux), nat.ptr(aux2) if aux2 is not None else None,
                  nat.ptr(new), nat.ptr(tmp), nh, ny, nz, nat.ptr(kx), nat.ptr(ky), nat.ptr(kz), *c3,
                  nat.ptr(flag.t), st)
+        zkeep = tmp if keep_z else None
         if ny > 1:
-            nat.call("pfcs_fft_axis_c2c", nat.ptr(tmp), nat.ptr(tmp), nh, ny, nz, 1, 0, st)
+            ybuf = torch.empty_like(tmp) if keep_z else tmp  # (out of place keeps the z pass)
+            nat.call("pfcs_fft_axis_c2c", nat.ptr(tmp), nat.ptr(ybuf), nh, ny, nz, 1, 0, st)
+            tmp = ybuf
         out = torch.empty(self.shape, dtype=torch.float64, device=state.device)
         nat.call("pfcs_irfft_x", nat.ptr(tmp), nat.ptr(out), nx, ny * nz, st)
-        return new, out
+        return (new, out, zkeep) if keep_z else (new, out)
 
     def inv(self, h: torch.Tensor, deriv: int | None = None) -> torch.Tensor:
         """F^-1[h], or F^-1[i d_deriv h] (grad_inv's recipe for that axis)."""
@@ -471,7 +477,7 @@ class _Real3:
         nat.call("pfcs_irfft_x", nat.ptr(tmp), nat.ptr(out), nx, ny * nz, st)
         return out
 
-    def _grad_zy(self, h: torch.Tensor, axes, outs=None) -> list:
+    def _grad_zy(self, h: torch.Tensor, axes, outs=None, t0=None) -> list:
         """The inverse z and y passes of F^-1(i d_a h) for each a in axes
         (x-halved spectra, before the x pass).  k_x and k_y are constant
         along z lines, so the x and y derivatives share ONE plain inverse z
@@ -484,7 +490,8 @@ class _Real3:
         nh = self.nh
         st = nat.stream_ptr()
         share = ny > 1 and _R2C_GRAD
-        t0, given, outs = None, outs, []
+        t0 = t0 if share else None  # the plain inverse z pass of h, when the caller has it
+        given, outs = outs, []
         for n_a, a in enumerate(axes):
             tmp = given[n_a] if given is not None else torch.empty_like(h)
             if share and a != 2:
@@ -512,19 +519,20 @@ class _Real3:
             outs.append(out)
         return outs
 
-    def adv_fwd(self, x_hat: torch.Tensor, v) -> torch.Tensor:
+    def adv_fwd(self, x_hat: torch.Tensor, v, t0=None) -> torch.Tensor:
         """F(v . grad x) (hydro.py:83-85): _grad_zy's inverse z / y passes
         into one stacked buffer, ONE fused x pass (pfcs_xdot3_x: the three
         C2R, the dot product with v, the R2C — the physical derivatives and
         the product never reach HBM), the forward y and z passes.
         Bit-identical to fwd(_grad_dot_r(self, x_hat, v)), which runs when
-        PFCS_R2C_XDOT=0 or the shape has no fused kernel."""
+        PFCS_R2C_XDOT=0 or the shape has no fused kernel.  t0: the plain
+        inverse z pass of x_hat if the caller has it (update_inv keep_z)."""
         nx, ny, nz = self.shape
         if not (_R2C_XDOT and nat.load().pfcs_xdot3_supported(nx, ny * nz)):
             return self.fwd(_grad_dot_r(self, x_hat, v))
         st = nat.stream_ptr()
         spec3 = torch.empty((3,) + self.hshape, dtype=torch.complex128, device=x_hat.device)
-        self._grad_zy(x_hat, (0, 1, 2), outs=[spec3[0], spec3[1], spec3[2]])
+        self._grad_zy(x_hat, (0, 1, 2), outs=[spec3[0], spec3[1], spec3[2]], t0=t0)
         out = torch.empty(self.hshape, dtype=torch.complex128, device=x_hat.device)
         vs = [_rdev(x) for x in v]
         nat.call("pfcs_xdot3_x", nat.ptr(spec3), nat.ptr(vs[0]), nat.ptr(vs[1]), nat.ptr(vs[2]), nat.ptr(out),
@@ -600,12 +608,13 @@ def _adv_term_r(R: _Real3, x_hat: torch.Tensor, axis: int, v_axis: torch.Tensor)
     return _rpw(RPW_MUL, v_axis, R.inv(x_hat, deriv=axis))
 
 
-def _density_r(R: _Real3, ph, ps, adv_hat, sym, hp: HydroParams, flag: _StepFlag, nl_hat=None):
+def _density_r(R: _Real3, ph, ps, adv_hat, sym, hp: HydroParams, flag: _StepFlag, nl_hat=None,
+               keep_z: bool = False):
     """adv_hat = F(v . grad psi) (R.adv_fwd, or R.fwd of a physical sum);
     nl_hat = F(psi^3) when the caller has it (the previous step's mu)."""
     if nl_hat is None:
         nl_hat = R.fwd(ps, RPW_CUBE)
-    return R.update_inv(0, ph, nl_hat, adv_hat, (float(sym.eps), float(hp.pfc.dt)), flag)
+    return R.update_inv(0, ph, nl_hat, adv_hat, (float(sym.eps), float(hp.pfc.dt)), flag, keep_z=keep_z)
 
 
 def _density_mu_r(R: _Real3, ps, sym, want_nl: bool = False):
@@ -629,6 +638,25 @@ def _density_mu_r(R: _Real3, ps, sym, want_nl: bool = False):
                  nat.ptr(ky), nat.ptr(kz), float(sym.eps), st)
         nl_out = nl_hat
     return (mu, nl_out) if want_nl else mu
+
+
+def _z_carry_get(fields, key: str, h):
+    """The plain inverse z pass of spectrum `h` kept by the previous serial
+    step's update (update_inv keep_z), or None: valid only while `h` is
+    still that step's state tensor, unmodified."""
+    c = fields.__dict__.get("_pfcs_z", {}).get(key)
+    if c is None or not _CARRY_NL:
+        return None
+    ref, version, z = c
+    return z if (ref() is h and h._version == version) else None
+
+
+def _z_carry_put(fields, key: str, h, z) -> None:
+    d = fields.__dict__.setdefault("_pfcs_z", {})
+    if isinstance(h, torch.Tensor) and z is not None and _CARRY_NL:
+        d[key] = (weakref.ref(h), h._version, z)
+    else:
+        d.pop(key, None)
 
 
 def _nl_carry_get(fields, ps):
@@ -676,13 +704,15 @@ def _serial_hydro_step_r(fields: HydroFields, sym: SymbolTable, params: HydroPar
     vh = [_hdev(x) for x in fields.v_hat]
     _check_half(R, ph, *vh)
     vs = [_rdev(v) for v in fields.v]
-    psi_hat, psi = _density_r(R, ph, ps, R.adv_fwd(ph, vs), sym, params, flag, _nl_carry_get(fields, ps))
+    psi_hat, psi, zpsi = _density_r(R, ph, ps, R.adv_fwd(ph, vs, t0=_z_carry_get(fields, "psi", ph)), sym, params,
+                                    flag, _nl_carry_get(fields, ps), keep_z=True)
     mu_hat, nl_next = _density_mu_r(R, psi, sym, want_nl=True)  # mu shared by the three components
     forces = R.prod_grad(mu_hat, psi)
     out = [_velocity_r(R, vh[i], psi, i, mu_hat, sym, params, flag, force=forces[i]) for i in range(3)]
     flag.check(fields.step_index, psi_hat, *(o[0] for o in out))
     fields.psi_hat, fields.psi = _out(psi_hat, host), _out(psi, host)
     _nl_carry_put(fields, fields.psi, nl_next)
+    _z_carry_put(fields, "psi", fields.psi_hat, zpsi)
     for i in range(3):
         fields.v_hat[i], fields.v[i] = _out(out[i][0], host), _out(out[i][1], host)
     fields.step_index += 1

@@ -52,10 +52,9 @@ import torch
 from . import _native as nat
 from .grid import SymbolTable
 from .hydro import (HydroParams, TAG_PSI, V_TAGS, RPW_ADD3, RPW_CHNL, _check_half, _dev, _Diag, _Real3, _StepFlag,
-                    _adv_term_r,
-                    _density_mu_r, _density_r, _fft, _fft_cmul, _fft_cube, _hdev, _ifft_deriv, _is_real,
-                    _nl_carry_get, _nl_carry_put, _out, _raise_divergence, _rdev, _rpw, _vectors,
-                    _velocity_r)
+                    _adv_term_r, _density_mu_r, _density_r, _fft, _fft_cmul, _fft_cube, _hdev, _ifft_deriv,
+                    _is_real, _nl_carry_get, _nl_carry_put, _out, _raise_divergence, _rdev, _rpw, _vectors,
+                    _velocity_r, _z_carry_get, _z_carry_put)
 
 __all__ = [
     "MultiParams",
@@ -328,11 +327,14 @@ def parallel_multi_step(worker, st: dict, sym: SymbolTable, params: MultiParams)
 
 # ------------------------------------------------------------ R2C path ------
 
-def _composition_r(R: _Real3, ch, cc, v, sym, params: MultiParams, flag: _StepFlag):
-    adv_hat = R.adv_fwd(ch, v)
+def _composition_r(R: _Real3, ch, cc, v, sym, params: MultiParams, flag: _StepFlag, t0=None, keep_z=False):
+    """t0: the plain inverse z pass of ch if the caller has it; keep_z:
+    also return the new state's (update_inv)."""
+    adv_hat = R.adv_fwd(ch, v, t0=t0)
     f_hat = R.fwd(cc, RPW_CHNL, alpha=params.alpha)
     return R.update_inv(2, ch, f_hat, adv_hat,
-                        (float(params.mobility), float(params.kappa), float(params.hydro.pfc.dt)), flag)
+                        (float(params.mobility), float(params.kappa), float(params.hydro.pfc.dt)), flag,
+                        keep_z=keep_z)
 
 
 def _composition_mu_r(R: _Real3, cc, ch, params: MultiParams) -> torch.Tensor:
@@ -354,8 +356,9 @@ def _serial_multi_step_r(fields: MultiFields, sym: SymbolTable, params: MultiPar
     vh = [_hdev(x) for x in fields.v_hat]
     _check_half(R, ph, ch, *vh)
     vs = [_rdev(v) for v in fields.v]
-    psi_hat, psi = _density_r(R, ph, ps, R.adv_fwd(ph, vs), sym, params.hydro, flag, _nl_carry_get(fields, ps))
-    c_hat, c = _composition_r(R, ch, cc, vs, sym, params, flag)
+    psi_hat, psi, zpsi = _density_r(R, ph, ps, R.adv_fwd(ph, vs, t0=_z_carry_get(fields, "psi", ph)), sym,
+                                    params.hydro, flag, _nl_carry_get(fields, ps), keep_z=True)
+    c_hat, c, zc = _composition_r(R, ch, cc, vs, sym, params, flag, t0=_z_carry_get(fields, "c", ch), keep_z=True)
     mu_hat, nl_next = _density_mu_r(R, psi, sym, want_nl=True)
     muc = _composition_mu_r(R, c, c_hat, params) if params.beta != 0.0 else None
     forces = R.prod_grad(mu_hat, psi)
@@ -367,7 +370,9 @@ def _serial_multi_step_r(fields: MultiFields, sym: SymbolTable, params: MultiPar
         fields.v_hat[i], fields.v[i] = _out(out[i][0], host), _out(out[i][1], host)
     fields.psi_hat, fields.psi = _out(psi_hat, host), _out(psi, host)
     _nl_carry_put(fields, fields.psi, nl_next)
+    _z_carry_put(fields, "psi", fields.psi_hat, zpsi)
     fields.c_hat, fields.c = _out(c_hat, host), _out(c, host)
+    _z_carry_put(fields, "c", fields.c_hat, zc)
     fields.step_index += 1
     fields.sim_time += params.hydro.pfc.dt
     return fields

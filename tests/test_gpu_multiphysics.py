@@ -259,7 +259,8 @@ for beta in (0.0, 0.5):
     for k in range(4):
         serial_multi_step(r, sym, mp)
         if k == 1 and beta == 0.0:
-            r.psi.mul_(1.0001)  # an in-place edit must invalidate the carried F(psi^3)
+            r.psi.mul_(1.0001)  # in-place edits must invalidate the carried F(psi^3) ...
+            r.c_hat.mul_(1.0001)  # ... and the carried inverse z pass of c_hat
     for k in ("psi", "c", "psi_hat", "c_hat"):
         out[f"{{beta}}_{{k}}"] = host(getattr(r, k))
     for i in range(3):
@@ -275,7 +276,9 @@ def test_r2c_fused_prologues_bit_identical(pkg, tmp_path):
     (pfcs_update_zinv), the force products and the advection dot products
     in one fused x pass each (pfcs_xmul_x, pfcs_xdot3_x), the fused mu and
     the F(psi^3) carried from one step's mu to the next step's density update
-    (invalidated by an in-place edit of psi) reproduce the unfused form (pfcs_real_pointwise +
+    and the inverse z passes of psi_hat / c_hat carried from their updates to
+    the next step's gradients (all invalidated by in-place edits) reproduce
+    the unfused form (pfcs_real_pointwise +
     pfcs_rfft_x; the standalone update kernels + the plain inverse) bit for
     bit."""
     import os
