@@ -144,7 +144,6 @@ __global__ void __launch_bounds__(T*(M / real_R(M, MODE)),
   const int tid = threadIdx.x;
   const int t = tid % T;
   const int j = tid / T;
-  double2* sl = smem + t * LS;
   const i64 ntiles = (inner + T - 1) / T;
   double m_abs = 0.0;
   constexpr bool AXR = MODE == MODE_R2C_PRO || MODE == MODE_XMUL;  // Regs carry the product factors
@@ -865,7 +864,6 @@ __global__ void __launch_bounds__(T*(N / radix_R(N)), min_blocks(T*(N / radix_R(
   const int tid = threadIdx.x;
   const int t = tid % T;
   const int j = tid / T;
-  double2* sl = smem + t * LS;
   const i64 ntiles = (inner + T - 1) / T;
   double m_re = 0.0, m_im = 0.0, m_abs = 0.0;
   auto load = [&](i64 tile, RegsX<R>& r) {
