@@ -274,6 +274,16 @@ int pfcs_add3(const void* a, const void* b, const void* c, void* out, int64_t n,
 int pfcs_update_zinv(int kind, const void* state_in, const void* aux, const void* aux2, void* state_out, void* zout,
                      int64_t n0, int64_t n1, int64_t n2, const double* kx, const double* ky, const double* kz,
                      double c0, double c1, double c2, double* diag, void* stream);
+/* pfcs_update_zinv whose operands arrive before their forward z pass
+ * (flags bit 0: aux, bit 1: aux2 — after only their x and y passes): the
+ * z passes run in registers inside the update (the k_pfc_z pattern), so
+ * the operand spectra never reach HBM.  Bit-identical to
+ * pfcs_fft_axis_c2c(axis 2, forward) on the flagged operands, then
+ * pfcs_update_zinv.  Other z lengths run that form, transforming the
+ * flagged operands in place. */
+int pfcs_update_zzinv(int kind, const void* state_in, void* aux, void* aux2, void* state_out, void* zout, int64_t n0,
+                      int64_t n1, int64_t n2, const double* kx, const double* ky, const double* kz, double c0,
+                      double c1, double c2, int flags, double* diag, void* stream);
 /* Real-field pointwise operators of the R2C multiphysics path (physical
  * fields real: 8-byte samples), numpy evaluation order, no FMA; all operand
  * pointers 16-byte aligned, unused ones may be NULL:

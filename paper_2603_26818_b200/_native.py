@@ -95,6 +95,8 @@ _SIGS = {
     "pfcs_real_pointwise": [_c_int, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_i64, _c_d, _c_p],
     "pfcs_update_zinv": [_c_int, _c_p, _c_p, _c_p, _c_p, _c_p, _c_i64, _c_i64, _c_i64, _c_p, _c_p, _c_p,
                          _c_d, _c_d, _c_d, _c_p, _c_p],
+    "pfcs_update_zzinv": [_c_int, _c_p, _c_p, _c_p, _c_p, _c_p, _c_i64, _c_i64, _c_i64, _c_p, _c_p, _c_p,
+                          _c_d, _c_d, _c_d, _c_int, _c_p, _c_p],
     "pfcs_axpy": [_c_p, _c_p, _c_p, _c_i64, _c_d, _c_p],
     "pfcs_energy_sum": [_c_p, _c_i64, _c_p, _c_i64, _c_i64, _c_p, _c_p, _c_p],
     "pfcs_energy_scratch_bytes": [_c_i64],

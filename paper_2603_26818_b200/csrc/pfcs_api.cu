@@ -180,6 +180,9 @@ int launch_rfft_x_pro(const double* in, void* out, long long nx, long long inner
                       double alpha, cudaStream_t st);
 int launch_xmul(void* data, const double* aux, long long nx, long long inner, cudaStream_t st);
 bool xdot3_supported(long long nx, long long inner);
+int launch_upd_zz(const double2* state, const double2* aux, const double2* aux2, double2* state_out, double2* zout,
+                  long long nlines, int n1, int n, const double* kx, const double* ky, const double* kz, int kind,
+                  double c0, double c1, double c2, int flags, double* diag, cudaStream_t st);
 int launch_mu_z(const double2* nl, const double2* f, double2* mu, double2* nl_out, long long nlines, int n1, int n,
                 const double* kx, const double* ky, const double* kz, double eps, cudaStream_t st);
 int launch_xdot3(const void* spec3, const double* v0, const double* v1, const double* v2, void* out, long long nx,
@@ -272,6 +275,29 @@ int pfcs_update_zinv(int kind, const void* state_in, const void* aux, const void
                                            stream);
   if (rc) return rc;
   return pfcs_fft_axis_c2c(state_out, zout, n0, n1, n2, 2, 0, stream);
+}
+
+int pfcs_update_zzinv(int kind, const void* state_in, void* aux, void* aux2, void* state_out, void* zout, int64_t n0,
+                      int64_t n1, int64_t n2, const double* kx, const double* ky, const double* kz, double c0,
+                      double c1, double c2, int flags, double* diag, void* stream) {
+  if (kind < 0 || kind > 2) return fail(PFCS_E_ARG, "update kind must be 0 (psi), 1 (velocity) or 2 (composition)");
+  if (!state_in || !aux || !state_out || !zout || !kx || !ky || !kz) return fail(PFCS_E_ARG, "null argument");
+  if (zout == state_in || zout == state_out || zout == aux || (aux2 && zout == aux2))
+    return fail(PFCS_E_ARG, "zout must not alias the state or the operands");
+  if (n0 < 0 || n1 < 0 || n2 < 0) return fail(PFCS_E_ARG, "negative extent");
+  if (n0 * n1 * n2 == 0) return PFCS_OK;
+  if (kind == 1) aux2 = nullptr;
+  const int rc = launch_upd_zz((const double2*)state_in, (const double2*)aux, (const double2*)aux2,
+                               (double2*)state_out, (double2*)zout, n0 * n1, (int)n1, (int)n2, kx, ky, kz, kind, c0,
+                               c1, c2, flags, diag, S(stream));
+  if (rc != 1) return rc;
+  // other z lengths: the operands' forward z passes in place, then the update + inverse z
+  if (flags & 1)
+    if (int r = pfcs_fft_axis_c2c(aux, aux, n0, n1, n2, 2, 1, stream)) return r;
+  if (aux2 && (flags & 2))
+    if (int r = pfcs_fft_axis_c2c(aux2, aux2, n0, n1, n2, 2, 1, stream)) return r;
+  return pfcs_update_zinv(kind, state_in, aux, aux2, state_out, zout, n0, n1, n2, kx, ky, kz, c0, c1, c2, diag,
+                          stream);
 }
 
 int pfcs_fft_axis_c2c_pro(const void* in, void* out, int64_t n0, int64_t n1, int64_t n2, int axis,

@@ -17,6 +17,7 @@
 //                 row of the tile is one T*16-byte coalesced segment.
 //  * k_dft      : direct O(N^2) DFT for non-power-of-two N (the reference
 //                 accepts any N, SPEC sizes 1..16 and primes).
+#include "pfcs_diag.cuh"
 #include "pfcs_fft.cuh"
 #include "pfcs_internal.h"
 #include "pfcs_pro.cuh"
@@ -513,6 +514,102 @@ int launch_mu_z(const double2* nl, const double2* f, double2* mu, double2* nl_ou
     PFCS_MU_CASE(8) PFCS_MU_CASE(16) PFCS_MU_CASE(32) PFCS_MU_CASE(64) PFCS_MU_CASE(128) PFCS_MU_CASE(256)
     PFCS_MU_CASE(512) PFCS_MU_CASE(1024) PFCS_MU_CASE(2048) PFCS_MU_CASE(4096)
 #undef PFCS_MU_CASE
+    default:
+      return 1;
+  }
+}
+
+// A spectral update with the forward z passes of its operands AND the
+// inverse z pass of its result, per z line (the k_pfc_z pattern for the
+// hydro / multiphysics updates): operands that arrive after only their x and
+// y passes (flags bit 0: aux, bit 1: aux2) are z-transformed in registers
+// (the standalone forward z pass's arithmetic), the old state is updated as
+// pfcs_update_zinv does (pfcs_hydro_math.cuh), the new state is stored and
+// its inverse z transform written to zout — bit-identical to the forward z
+// passes, then pfcs_update_zinv.  Neither operand spectrum reaches HBM.
+#ifndef PFCS_UPDZ_TARGET
+#define PFCS_UPDZ_TARGET 512  // resident threads per SM the register cap aims for (three line register sets)
+#endif
+template <int N>
+__global__ void __launch_bounds__(N / radix_R(N), min_blocks(N / radix_R(N), PFCS_UPDZ_TARGET))
+    k_upd_zz(const double2* __restrict__ state, const double2* __restrict__ aux, const double2* __restrict__ aux2,
+             double2* state_out, double2* zout, i64 nlines, int n1, const double* __restrict__ kx,
+             const double* __restrict__ ky, const double* __restrict__ kz, int kind, double c0, double c1, double c2,
+             int flags, double* diag, const double2* __restrict__ tw, double scale) {
+  pdl_wait();
+  constexpr int R = radix_R(N);
+  constexpr int P = N / R;
+  extern __shared__ double2 smem[];
+  const int j = threadIdx.x;
+  bool bad = false;
+  for (i64 l = blockIdx.x; l < nlines; l += gridDim.x) {
+    double2 a[R], b[R];
+#pragma unroll
+    for (int e = 0; e < R; ++e) a[e] = aux[l * N + j + P * e];
+    int jj = opaque(j);
+    if (flags & 1) fft_line<N, true, 1, PFCS_LINES_TWL>(a, jj, smem, tw);
+    if (aux2) {
+#pragma unroll
+      for (int e = 0; e < R; ++e) b[e] = aux2[l * N + jj + P * e];
+      jj = opaque(jj);
+      if (flags & 2) fft_line<N, true, 1, PFCS_LINES_TWL>(b, jj, smem, tw);
+    } else {
+#pragma unroll
+      for (int e = 0; e < R; ++e) b[e] = make_double2(0.0, 0.0);
+    }
+    const i64 lx = l / n1;
+    const int ly = (int)(l - lx * n1);
+    const double ka = __ldg(kx + lx), kb = __ldg(ky + ly);
+    const double kxy = __dadd_rn(__dmul_rn(ka, ka), __dmul_rn(kb, kb));
+    double2 v[R];
+#pragma unroll
+    for (int e = 0; e < R; ++e) {
+      const int z = jj + P * e;
+      const double kc = __ldg(kz + z);
+      const double k2 = __dadd_rn(kxy, __dmul_rn(kc, kc));
+      const double2 old = state[l * N + z];
+      const double2 nw = kind == 0   ? psi_update(old, a[e], b[e], k2, c0, c1)
+                         : kind == 1 ? vel_update(old, a[e], k2, c0, c1, c2)
+                                     : ch_update(old, a[e], b[e], k2, c0, c1, c2);
+      bad |= !isfinite(nw.x);
+      state_out[l * N + z] = nw;
+      v[e] = nw;
+    }
+    const int j3 = opaque(jj);
+    fft_line<N, false, 1, PFCS_LINES_TWL>(v, j3, smem, tw);
+#pragma unroll
+    for (int e = 0; e < R; ++e) zout[l * N + j3 + P * e] = make_double2(v[e].x * scale, v[e].y * scale);
+  }
+  diag_flag_nonfinite(diag, bad);
+}
+
+template <int N>
+static int upd_zz_n(const double2* state, const double2* aux, const double2* aux2, double2* state_out, double2* zout,
+                    i64 nlines, int n1, const double* kx, const double* ky, const double* kz, int kind, double c0,
+                    double c1, double c2, int flags, double* diag, cudaStream_t st) {
+  const double2* tw = twiddles(N);
+  if (!tw) return PFCS_E_CUDA;
+  constexpr int P = N / radix_R(N);
+  const size_t smem = (size_t)tile_ls(N, 1, false) * sizeof(double2);
+  int grid = 0;
+  if (int rc = persistent_grid((const void*)k_upd_zz<N>, P, smem, nlines, &grid)) return rc;
+  launch_pdl(k_upd_zz<N>, dim3(grid), dim3(P), smem, st, state, aux, aux2, state_out, zout, nlines, n1, kx, ky, kz,
+             kind, c0, c1, c2, flags, diag, tw, 1.0 / (double)N);
+  return check_launch("k_upd_zz");
+}
+
+// returns 1 when not applicable (z length not a power of two in [8, 4096])
+int launch_upd_zz(const double2* state, const double2* aux, const double2* aux2, double2* state_out, double2* zout,
+                  long long nlines, int n1, int n, const double* kx, const double* ky, const double* kz, int kind,
+                  double c0, double c1, double c2, int flags, double* diag, cudaStream_t st) {
+  if (nlines <= 0) return PFCS_OK;
+  switch (n) {
+#define PFCS_UZ_CASE(NN) \
+  case NN:               \
+    return upd_zz_n<NN>(state, aux, aux2, state_out, zout, nlines, n1, kx, ky, kz, kind, c0, c1, c2, flags, diag, st);
+    PFCS_UZ_CASE(8) PFCS_UZ_CASE(16) PFCS_UZ_CASE(32) PFCS_UZ_CASE(64) PFCS_UZ_CASE(128) PFCS_UZ_CASE(256)
+    PFCS_UZ_CASE(512) PFCS_UZ_CASE(1024) PFCS_UZ_CASE(2048) PFCS_UZ_CASE(4096)
+#undef PFCS_UZ_CASE
     default:
       return 1;
   }

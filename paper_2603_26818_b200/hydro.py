@@ -356,6 +356,9 @@ _R2C_MUZ = os.environ.get("PFCS_R2C_MUZ", "1") != "0"
 # serial steps carry F(psi^3) from one step's mu to the next step's density
 # update (same psi, same spectrum; A/B, bit-identical)
 _CARRY_NL = os.environ.get("PFCS_R2C_CARRY", "1") != "0"
+# updates take their operands before the forward z pass and run it
+# (pfcs_update_zzinv; A/B, bit-identical)
+_R2C_ZZ = os.environ.get("PFCS_R2C_ZZ", "1") != "0"
 
 
 def _is_real(x) -> bool:
@@ -428,19 +431,28 @@ class _Real3:
         return out
 
     def update_inv(self, kind: int, state: torch.Tensor, aux: torch.Tensor, aux2, c: tuple,
-                   flag: "_StepFlag", keep_z: bool = False) -> tuple:
+                   flag: "_StepFlag", keep_z: bool = False, pre_z=(False, False)) -> tuple:
         """A spectral update fused with the first (z) pass of the inverse
         transform of its result (pfcs_update_zinv; kind 0 psi, 1 velocity,
         2 composition): returns (new state, F^-1 of it).  PFCS_R2C_UPD=0 runs
         the standalone update kernel and the plain inverse (bit-identical).
         keep_z: also return the inverse z pass of the new state (or None) —
         the shared z pass of the next step's gradient of that state
-        (_grad_zy), so the serial steps carry it over."""
+        (_grad_zy), so the serial steps carry it over.  pre_z: (aux, aux2)
+        arrive before their forward z pass (fwd(..., z=False)); the update
+        runs it in registers (pfcs_update_zzinv; PFCS_R2C_ZZ=0: the z passes
+        in place first — bit-identical)."""
         nx, ny, nz = self.shape
         nh = self.nh
         kx, ky, kz = self.k
         st = nat.stream_ptr()
         new = torch.empty_like(state)
+        pre_z = (bool(pre_z[0]), bool(pre_z[1]) and aux2 is not None)
+        fuse_zz = any(pre_z) and _R2C_ZZ and _R2C_UPD and nz > 1
+        if any(pre_z) and not fuse_zz and nz > 1:
+            for t, pz in ((aux, pre_z[0]), (aux2, pre_z[1])):
+                if pz:
+                    nat.call("pfcs_fft_axis_c2c", nat.ptr(t), nat.ptr(t), nh, ny, nz, 2, 1, st)
         if not _R2C_UPD:
             name = ("pfcs_hydro_psi_update_to", "pfcs_hydro_vel_update_to", "pfcs_ch_update_to")[kind]
             ops = [nat.ptr(state), nat.ptr(new), nat.ptr(aux)] + ([] if kind == 1 else [nat.ptr(aux2)])
@@ -450,9 +462,15 @@ class _Real3:
             return (new, self.inv(new), None) if keep_z else (new, self.inv(new))
         tmp = torch.empty_like(state)
         c3 = tuple(float(v) for v in c) + (0.0,) * (3 - len(c))
-        nat.call("pfcs_update_zinv", kind, nat.ptr(state), nat.ptr(aux), nat.ptr(aux2) if aux2 is not None else None,
-                 nat.ptr(new), nat.ptr(tmp), nh, ny, nz, nat.ptr(kx), nat.ptr(ky), nat.ptr(kz), *c3,
-                 nat.ptr(flag.t), st)
+        if fuse_zz:
+            nat.call("pfcs_update_zzinv", kind, nat.ptr(state), nat.ptr(aux),
+                     nat.ptr(aux2) if aux2 is not None else None, nat.ptr(new), nat.ptr(tmp), nh, ny, nz,
+                     nat.ptr(kx), nat.ptr(ky), nat.ptr(kz), *c3, int(pre_z[0]) | (2 * int(pre_z[1])),
+                     nat.ptr(flag.t), st)
+        else:
+            nat.call("pfcs_update_zinv", kind, nat.ptr(state), nat.ptr(aux),
+                     nat.ptr(aux2) if aux2 is not None else None, nat.ptr(new), nat.ptr(tmp), nh, ny, nz,
+                     nat.ptr(kx), nat.ptr(ky), nat.ptr(kz), *c3, nat.ptr(flag.t), st)
         zkeep = tmp if keep_z else None
         if ny > 1:
             ybuf = torch.empty_like(tmp) if keep_z else tmp  # (out of place keeps the z pass)
@@ -519,7 +537,7 @@ class _Real3:
             outs.append(out)
         return outs
 
-    def adv_fwd(self, x_hat: torch.Tensor, v, t0=None) -> torch.Tensor:
+    def adv_fwd(self, x_hat: torch.Tensor, v, t0=None, z: bool = True) -> torch.Tensor:
         """F(v . grad x) (hydro.py:83-85): _grad_zy's inverse z / y passes
         into one stacked buffer, ONE fused x pass (pfcs_xdot3_x: the three
         C2R, the dot product with v, the R2C — the physical derivatives and
@@ -529,7 +547,7 @@ class _Real3:
         inverse z pass of x_hat if the caller has it (update_inv keep_z)."""
         nx, ny, nz = self.shape
         if not (_R2C_XDOT and nat.load().pfcs_xdot3_supported(nx, ny * nz)):
-            return self.fwd(_grad_dot_r(self, x_hat, v))
+            return self.fwd(_grad_dot_r(self, x_hat, v), z=z)
         st = nat.stream_ptr()
         spec3 = torch.empty((3,) + self.hshape, dtype=torch.complex128, device=x_hat.device)
         self._grad_zy(x_hat, (0, 1, 2), outs=[spec3[0], spec3[1], spec3[2]], t0=t0)
@@ -539,11 +557,11 @@ class _Real3:
                  nx, ny * nz, st)
         if ny > 1:
             nat.call("pfcs_fft_axis_c2c", nat.ptr(out), nat.ptr(out), self.nh, ny, nz, 1, 1, st)
-        if nz > 1:
+        if nz > 1 and z:
             nat.call("pfcs_fft_axis_c2c", nat.ptr(out), nat.ptr(out), self.nh, ny, nz, 2, 1, st)
         return out
 
-    def prod_grad(self, h: torch.Tensor, aux: torch.Tensor, axes=(0, 1, 2)) -> list:
+    def prod_grad(self, h: torch.Tensor, aux: torch.Tensor, axes=(0, 1, 2), z: bool = True) -> list:
         """[F(aux * F^-1(i d_a h)) for a in axes] — the hydro force
         F(psi F^-1(i k mu_hat)) (hydro.py:98): the inverse z / y passes of
         _grad_zy, ONE fused x pass (C2R, times aux, R2C: pfcs_xmul_x, the
@@ -551,7 +569,7 @@ class _Real3:
         and z passes.  Bit-identical to fwd(grad_inv(h)[a], RPW_MUL, aux)
         (PFCS_R2C_XMUL=0 runs that form)."""
         if not _R2C_XMUL:
-            return [self.fwd(d, RPW_MUL, aux) for d in self.grad_inv(h, axes)]
+            return [self.fwd(d, RPW_MUL, aux, z=z) for d in self.grad_inv(h, axes)]
         nx, ny, nz = self.shape
         nh = self.nh
         st = nat.stream_ptr()
@@ -560,7 +578,7 @@ class _Real3:
             nat.call("pfcs_xmul_x", nat.ptr(tmp), nat.ptr(aux), nx, ny * nz, st)
             if ny > 1:
                 nat.call("pfcs_fft_axis_c2c", nat.ptr(tmp), nat.ptr(tmp), nh, ny, nz, 1, 1, st)
-            if nz > 1:
+            if nz > 1 and z:
                 nat.call("pfcs_fft_axis_c2c", nat.ptr(tmp), nat.ptr(tmp), nh, ny, nz, 2, 1, st)
         return outs
 
@@ -609,12 +627,16 @@ def _adv_term_r(R: _Real3, x_hat: torch.Tensor, axis: int, v_axis: torch.Tensor)
 
 
 def _density_r(R: _Real3, ph, ps, adv_hat, sym, hp: HydroParams, flag: _StepFlag, nl_hat=None,
-               keep_z: bool = False):
-    """adv_hat = F(v . grad psi) (R.adv_fwd, or R.fwd of a physical sum);
-    nl_hat = F(psi^3) when the caller has it (the previous step's mu)."""
+               keep_z: bool = False, adv_pre_z: bool = False):
+    """adv_hat = F(v . grad psi) (R.adv_fwd, or R.fwd of a physical sum;
+    adv_pre_z: before its forward z pass); nl_hat = F(psi^3) when the caller
+    has it (the previous step's mu), else transformed here up to its z pass,
+    which the update runs (update_inv pre_z)."""
+    nl_pre_z = nl_hat is None
     if nl_hat is None:
-        nl_hat = R.fwd(ps, RPW_CUBE)
-    return R.update_inv(0, ph, nl_hat, adv_hat, (float(sym.eps), float(hp.pfc.dt)), flag, keep_z=keep_z)
+        nl_hat = R.fwd(ps, RPW_CUBE, z=False)
+    return R.update_inv(0, ph, nl_hat, adv_hat, (float(sym.eps), float(hp.pfc.dt)), flag, keep_z=keep_z,
+                        pre_z=(nl_pre_z, adv_pre_z))
 
 
 def _density_mu_r(R: _Real3, ps, sym, want_nl: bool = False):
@@ -679,20 +701,21 @@ def _nl_carry_put(fields, ps, nl) -> None:
 
 def _velocity_r(R: _Real3, vh, ps, axis: int, mu_hat, sym, hp: HydroParams, flag: _StepFlag, cc=None,
                 muc=None, beta: float = 0.0, force=None, force_c=None):
-    """force / force_c: F(psi F^-1(i d_axis mu_hat)) (/ c, muc) when the
-    caller formed all three at once (R.prod_grad: the serial steps)."""
+    """force / force_c: F(psi F^-1(i d_axis mu_hat)) (/ c, muc) BEFORE their
+    forward z pass (prod_grad z=False), when the caller formed all three at
+    once (the serial steps); the update runs that z pass (pre_z)."""
     if force is None:
-        force = R.prod_grad(mu_hat, ps, (axis,))[0]  # F(psi F^-1(i k mu_hat))
+        force = R.prod_grad(mu_hat, ps, (axis,), z=False)[0]  # F(psi F^-1(i k mu_hat)), up to z
     if beta != 0.0:
         if force_c is None:
-            force_c = R.prod_grad(muc, cc, (axis,))[0]
+            force_c = R.prod_grad(muc, cc, (axis,), z=False)[0]
         total = torch.empty_like(force)
         nat.call("pfcs_axpy", nat.ptr(force), nat.ptr(force_c), nat.ptr(total), total.numel(), float(beta),
                  nat.stream_ptr())
         force = total
     dt, rho = float(hp.pfc.dt), float(hp.rho)
     return R.update_inv(1, vh, force, None, (dt / rho, (dt / rho) * float(hp.gamma), -0.5 * float(sym.a0) ** 2),
-                        flag)
+                        flag, pre_z=(True, False))
 
 
 def _serial_hydro_step_r(fields: HydroFields, sym: SymbolTable, params: HydroParams) -> HydroFields:
@@ -704,10 +727,10 @@ def _serial_hydro_step_r(fields: HydroFields, sym: SymbolTable, params: HydroPar
     vh = [_hdev(x) for x in fields.v_hat]
     _check_half(R, ph, *vh)
     vs = [_rdev(v) for v in fields.v]
-    psi_hat, psi, zpsi = _density_r(R, ph, ps, R.adv_fwd(ph, vs, t0=_z_carry_get(fields, "psi", ph)), sym, params,
-                                    flag, _nl_carry_get(fields, ps), keep_z=True)
+    psi_hat, psi, zpsi = _density_r(R, ph, ps, R.adv_fwd(ph, vs, t0=_z_carry_get(fields, "psi", ph), z=False), sym,
+                                    params, flag, _nl_carry_get(fields, ps), keep_z=True, adv_pre_z=True)
     mu_hat, nl_next = _density_mu_r(R, psi, sym, want_nl=True)  # mu shared by the three components
-    forces = R.prod_grad(mu_hat, psi)
+    forces = R.prod_grad(mu_hat, psi, z=False)
     out = [_velocity_r(R, vh[i], psi, i, mu_hat, sym, params, flag, force=forces[i]) for i in range(3)]
     flag.check(fields.step_index, psi_hat, *(o[0] for o in out))
     fields.psi_hat, fields.psi = _out(psi_hat, host), _out(psi, host)
@@ -732,7 +755,8 @@ def _parallel_hydro_step_r(worker, role_state: dict, sym: SymbolTable, params: H
     if rank == 0:
         ph = role_state["psi_hat"]
         _check_half(R, ph)
-        psi_hat, psi = _density_r(R, ph, psi0, R.adv_fwd(ph, role_state["v"]), sym, params, flag)
+        psi_hat, psi = _density_r(R, ph, psi0, R.adv_fwd(ph, role_state["v"], z=False), sym, params, flag,
+                                  adv_pre_z=True)
         flag.check(idx, psi_hat)
         role_state["psi_hat"], role_state["psi"] = psi_hat, psi
         worker.bcast_tensor(0, (0, 1, 2, 3), TAG_PSI, t=psi)

@@ -330,11 +330,11 @@ def parallel_multi_step(worker, st: dict, sym: SymbolTable, params: MultiParams)
 def _composition_r(R: _Real3, ch, cc, v, sym, params: MultiParams, flag: _StepFlag, t0=None, keep_z=False):
     """t0: the plain inverse z pass of ch if the caller has it; keep_z:
     also return the new state's (update_inv)."""
-    adv_hat = R.adv_fwd(ch, v, t0=t0)
-    f_hat = R.fwd(cc, RPW_CHNL, alpha=params.alpha)
+    adv_hat = R.adv_fwd(ch, v, t0=t0, z=False)
+    f_hat = R.fwd(cc, RPW_CHNL, alpha=params.alpha, z=False)
     return R.update_inv(2, ch, f_hat, adv_hat,
                         (float(params.mobility), float(params.kappa), float(params.hydro.pfc.dt)), flag,
-                        keep_z=keep_z)
+                        keep_z=keep_z, pre_z=(True, True))
 
 
 def _composition_mu_r(R: _Real3, cc, ch, params: MultiParams) -> torch.Tensor:
@@ -356,13 +356,13 @@ def _serial_multi_step_r(fields: MultiFields, sym: SymbolTable, params: MultiPar
     vh = [_hdev(x) for x in fields.v_hat]
     _check_half(R, ph, ch, *vh)
     vs = [_rdev(v) for v in fields.v]
-    psi_hat, psi, zpsi = _density_r(R, ph, ps, R.adv_fwd(ph, vs, t0=_z_carry_get(fields, "psi", ph)), sym,
-                                    params.hydro, flag, _nl_carry_get(fields, ps), keep_z=True)
+    psi_hat, psi, zpsi = _density_r(R, ph, ps, R.adv_fwd(ph, vs, t0=_z_carry_get(fields, "psi", ph), z=False), sym,
+                                    params.hydro, flag, _nl_carry_get(fields, ps), keep_z=True, adv_pre_z=True)
     c_hat, c, zc = _composition_r(R, ch, cc, vs, sym, params, flag, t0=_z_carry_get(fields, "c", ch), keep_z=True)
     mu_hat, nl_next = _density_mu_r(R, psi, sym, want_nl=True)
     muc = _composition_mu_r(R, c, c_hat, params) if params.beta != 0.0 else None
-    forces = R.prod_grad(mu_hat, psi)
-    forces_c = R.prod_grad(muc, c) if muc is not None else [None] * 3
+    forces = R.prod_grad(mu_hat, psi, z=False)
+    forces_c = R.prod_grad(muc, c, z=False) if muc is not None else [None] * 3
     out = [_velocity_r(R, vh[i], psi, i, mu_hat, sym, params.hydro, flag, c, muc, params.beta, forces[i],
                        forces_c[i]) for i in range(3)]
     flag.check(fields.step_index, psi_hat, c_hat, *(o[0] for o in out))
@@ -399,10 +399,10 @@ def _parallel_multi_step_r(worker, st: dict, sym: SymbolTable, params: MultiPara
         if G == 8:
             worker.bcast_tensor(0, s_psih, TAG_PSIHAT, t=ph)
             p = [worker.recv_tensor(5 + i, ADV_TAGS[i], torch.empty_like(st["psi"])) for i in range(3)]
-            adv_hat = R.fwd(_rpw(RPW_ADD3, *p))
+            adv_hat = R.fwd(_rpw(RPW_ADD3, *p), z=False)
         else:
-            adv_hat = R.adv_fwd(ph, st["v"])
-        st["psi_hat"], st["psi"] = _density_r(R, ph, st["psi"], adv_hat, sym, params.hydro, flag)
+            adv_hat = R.adv_fwd(ph, st["v"], z=False)
+        st["psi_hat"], st["psi"] = _density_r(R, ph, st["psi"], adv_hat, sym, params.hydro, flag, adv_pre_z=True)
         flag.check(idx, st["psi_hat"])
         worker.bcast_tensor(0, s_psi, TAG_PSI, t=st["psi"])
         st["v"] = [worker.bcast_tensor(1 + i, s_v[i], V_TAGS[i], out=torch.empty_like(st["psi"]))

@@ -119,3 +119,41 @@ def test_update_zinv_argument_errors(nat):
         nat.call("pfcs_update_zinv", 3, nat.ptr(x), nat.ptr(x), None, nat.ptr(x), nat.ptr(x.clone()), 4, 4, 8, *args)
     with pytest.raises(Exception):  # zout aliasing the state
         nat.call("pfcs_update_zinv", 1, nat.ptr(x), nat.ptr(x.clone()), None, nat.ptr(x), nat.ptr(x), 4, 4, 8, *args)
+
+
+@pytest.mark.parametrize("shape", [(9, 16, 512), (5, 12, 64), (6, 10, 9)])
+@pytest.mark.parametrize("kind,flags", [(0, 1), (0, 2), (0, 3), (1, 1), (2, 3)])
+def test_update_zzinv_bit_identical(nat, shape, kind, flags):
+    """pfcs_update_zzinv (operands before their forward z pass, the z
+    passes run inside the update) == the forward z passes, then
+    pfcs_update_zinv — bit for bit; fused on power-of-two z, the in-place
+    fallback otherwise."""
+    import torch
+
+    rng = np.random.default_rng(11 * kind + flags + sum(shape))
+    n0, n1, n2 = shape
+
+    def cplx():
+        return torch.from_numpy(rng.standard_normal(shape) + 1j * rng.standard_normal(shape)).cuda()
+
+    st = nat.stream_ptr()
+    state, aux, aux2 = cplx(), cplx(), cplx()
+    kx, ky, kz = (torch.from_numpy(rng.standard_normal(m)).cuda() for m in shape)
+    c = {0: (-0.3, 0.1, 0.0), 1: (0.1, 0.07, -2.0), 2: (1.0, 0.8, 0.1)}[kind]
+    a_w, b_w = aux.clone(), aux2.clone()
+    if flags & 1:
+        nat.call("pfcs_fft_axis_c2c", nat.ptr(a_w), nat.ptr(a_w), n0, n1, n2, 2, 1, st)
+    if flags & 2:
+        nat.call("pfcs_fft_axis_c2c", nat.ptr(b_w), nat.ptr(b_w), n0, n1, n2, 2, 1, st)
+    new_w, z_w = torch.empty_like(state), torch.empty_like(state)
+    flag_w = torch.zeros(4096, dtype=torch.float64, device="cuda")
+    nat.call("pfcs_update_zinv", kind, nat.ptr(state), nat.ptr(a_w), nat.ptr(b_w), nat.ptr(new_w), nat.ptr(z_w),
+             n0, n1, n2, nat.ptr(kx), nat.ptr(ky), nat.ptr(kz), *c, nat.ptr(flag_w), st)
+    a_g, b_g = aux.clone(), aux2.clone()
+    new_g, z_g = torch.empty_like(state), torch.empty_like(state)
+    flag_g = torch.zeros_like(flag_w)
+    nat.call("pfcs_update_zzinv", kind, nat.ptr(state), nat.ptr(a_g), nat.ptr(b_g), nat.ptr(new_g), nat.ptr(z_g),
+             n0, n1, n2, nat.ptr(kx), nat.ptr(ky), nat.ptr(kz), *c, flags, nat.ptr(flag_g), st)
+    torch.cuda.synchronize()
+    assert torch.equal(new_g, new_w)
+    assert torch.equal(z_g, z_w)
