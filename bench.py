@@ -530,11 +530,14 @@ def multi_bytes(n: int) -> float:
       * the updates take their operands before the forward z pass and run
         it in registers (pfcs_update_zzinv: each such operand's z-pass
         write and re-read, 2S — psi: adv; c: f and adv; v_1..3: the force:
-        -12S).
-    Total 17R + 100S."""
+        -12S);
+      * grad mu's first inverse z passes run inside the mu kernel
+        (pfcs_hydro_mu_zgrad: mu_hat is never stored nor re-read by the
+        two z passes: -3S).
+    Total 17R + 97S."""
     R = 8.0 * n**3
     S = spec_bytes(n)
-    return 23 * (R + 5 * S) + (17 - 6 - 16 - 1) * R + (20 - 5 - 6 - 4 - 4 - 4 - 12) * S
+    return 23 * (R + 5 * S) + (17 - 6 - 16 - 1) * R + (20 - 5 - 6 - 4 - 4 - 4 - 12 - 3) * S
 
 
 def run_multi(ctx, args):
@@ -593,7 +596,7 @@ def run_multi(ctx, args):
         alg = multi_bytes(n)
         res["roofline"] = {"bound": "hbm", "alg_bytes_per_step": alg, "achieved": round(alg / (ms * 1e-3) / 1e9, 1),
                            "peak": hbm, "unit": "GB/s", "frac": round(alg / (ms * 1e-3) / 1e9 / hbm, 4),
-                           "model": "fused schedule, 17R + 100S per step (R a real field, S a half spectrum; "
+                           "model": "fused schedule, 17R + 97S per step (R a real field, S a half spectrum; "
                                     "pass-by-pass in bench.multi_bytes)"}
         # e2e: host psi, c (pinned) in -> forward transforms -> K steps -> psi, c, v out
         hp_in = [x.cpu().pin_memory() for x in (psi, c)]

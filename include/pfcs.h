@@ -161,6 +161,16 @@ int pfcs_xdot3_supported(int64_t nx, int64_t inner);
  * (transforming f_xy, and nl_xy when nl_out is NULL, in place). */
 int pfcs_hydro_mu_z(const void* nl_xy, const void* f_xy, void* mu, void* nl_out, int64_t n0, int64_t n1,
                     int64_t n2, const double* kx, const double* ky, const double* kz, double eps, void* stream);
+/* pfcs_hydro_mu_z that also runs the first inverse z passes of grad mu
+ * (the x / y derivatives' shared plain pass -> t0_out, the z derivative's
+ * pass with the i k_z multiplier dz -> tz_out; either may be NULL), so
+ * mu_hat itself need not be stored (mu may be NULL).  Bit-identical to
+ * pfcs_hydro_mu_z followed by pfcs_fft_axis_c2c(mu, t0, axis 2, inverse) and
+ * pfcs_fft_axis_c2c_pro(mu, tz, axis 2, inverse, derivative dz, 2).  Power-of-
+ * two z lengths in [8, 4096] only (PFCS_E_UNSUPPORTED otherwise). */
+int pfcs_hydro_mu_zgrad(const void* nl_xy, const void* f_xy, void* mu, void* nl_out, void* t0_out, void* tz_out,
+                        const double* dz, int64_t n0, int64_t n1, int64_t n2, const double* kx, const double* ky,
+                        const double* kz, double eps, void* stream);
 int pfcs_xdot3_x(const void* spec3, const double* v0, const double* v1, const double* v2, void* out, int64_t nx,
                  int64_t inner, void* stream);
 

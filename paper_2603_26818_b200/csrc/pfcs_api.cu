@@ -184,7 +184,8 @@ int launch_upd_zz(const double2* state, const double2* aux, const double2* aux2,
                   long long nlines, int n1, int n, const double* kx, const double* ky, const double* kz, int kind,
                   double c0, double c1, double c2, int flags, double* diag, cudaStream_t st);
 int launch_mu_z(const double2* nl, const double2* f, double2* mu, double2* nl_out, long long nlines, int n1, int n,
-                const double* kx, const double* ky, const double* kz, double eps, cudaStream_t st);
+                const double* kx, const double* ky, const double* kz, double eps, cudaStream_t st, double2* t0_out,
+                double2* tz_out, const double* dz);
 int launch_xdot3(const void* spec3, const double* v0, const double* v1, const double* v2, void* out, long long nx,
                  long long inner, cudaStream_t st);
 int launch_pfc_z(const double2* nl, double2* psi_hat, double2* next, long long cx, long long ny,
@@ -386,14 +387,28 @@ int pfcs_xmul_x(void* data, const double* aux, int64_t nx, int64_t inner, void* 
 
 int pfcs_hydro_mu_z(const void* nl_xy, const void* f_xy, void* mu, void* nl_out, int64_t n0, int64_t n1,
                     int64_t n2, const double* kx, const double* ky, const double* kz, double eps, void* stream) {
-  if (!nl_xy || !f_xy || !mu || !kx || !ky || !kz) return fail(PFCS_E_ARG, "null argument");
-  if (mu == nl_xy || mu == f_xy || (nl_out && (nl_out == mu || nl_out == f_xy)))
-    return fail(PFCS_E_ARG, "mu / nl_out must not alias the operands or each other");
+  return pfcs_hydro_mu_zgrad(nl_xy, f_xy, mu, nl_out, nullptr, nullptr, nullptr, n0, n1, n2, kx, ky, kz, eps, stream);
+}
+
+int pfcs_hydro_mu_zgrad(const void* nl_xy, const void* f_xy, void* mu, void* nl_out, void* t0_out, void* tz_out,
+                        const double* dz, int64_t n0, int64_t n1, int64_t n2, const double* kx, const double* ky,
+                        const double* kz, double eps, void* stream) {
+  if (!nl_xy || !f_xy || !kx || !ky || !kz) return fail(PFCS_E_ARG, "null argument");
+  if (!mu && !t0_out && !tz_out) return fail(PFCS_E_ARG, "no output");
+  if (tz_out && !dz) return fail(PFCS_E_ARG, "tz_out needs the derivative vector dz");
+  const void* outs[4] = {mu, nl_out, t0_out, tz_out};
+  for (int i = 0; i < 4; ++i) {
+    if (outs[i] && (outs[i] == nl_xy || outs[i] == f_xy)) return fail(PFCS_E_ARG, "an output aliases an operand");
+    for (int k = 0; k < i; ++k)
+      if (outs[i] && outs[i] == outs[k]) return fail(PFCS_E_ARG, "outputs alias each other");
+  }
   if (n0 < 0 || n1 < 0 || n2 < 0) return fail(PFCS_E_ARG, "negative extent");
   if (n0 * n1 * n2 == 0) return PFCS_OK;
   const int rc = launch_mu_z((const double2*)nl_xy, (const double2*)f_xy, (double2*)mu, (double2*)nl_out, n0 * n1,
-                             (int)n1, (int)n2, kx, ky, kz, eps, S(stream));
+                             (int)n1, (int)n2, kx, ky, kz, eps, S(stream), (double2*)t0_out, (double2*)tz_out, dz);
   if (rc != 1) return rc;
+  if (t0_out || tz_out || !mu)
+    return fail(PFCS_E_UNSUPPORTED, "mu_hat with its gradient's z passes needs a power-of-two z length in [8, 4096]");
   // other z lengths: the two forward z passes, then the mu pass
   void* nlz = nl_out ? nl_out : (void*)nl_xy;
   if (int r = pfcs_fft_axis_c2c(nl_xy, nlz, n0, n1, n2, 2, 1, stream)) return r;

@@ -455,7 +455,8 @@ template <int N>
 __global__ void __launch_bounds__(N / radix_R(N), min_blocks(N / radix_R(N), PFCS_MUZ_TARGET))
     k_mu_z(const double2* __restrict__ nl, const double2* __restrict__ f, double2* mu, double2* nl_out, i64 nlines,
            int n1, const double* __restrict__ kx, const double* __restrict__ ky, const double* __restrict__ kz,
-           double eps, const double2* __restrict__ tw) {
+           double eps, const double2* __restrict__ tw, double2* t0_out, double2* tz_out,
+           const double* __restrict__ dz, double scale) {
   pdl_wait();
   constexpr int R = radix_R(N);
   constexpr int P = N / R;
@@ -484,33 +485,61 @@ __global__ void __launch_bounds__(N / radix_R(N), min_blocks(N / radix_R(N), PFC
       const double p1 = __dsub_rn(1.0, k2);
       const double p2 = __dsub_rn(4.0 / 3.0, k2);
       const double op = __dadd_rn(eps, __dmul_rn(__dmul_rn(p1, p1), __dmul_rn(p2, p2)));
-      mu[l * N + z] = make_double2(__dadd_rn(a[e].x, __dmul_rn(op, b[e].x)), __dadd_rn(a[e].y, __dmul_rn(op, b[e].y)));
+      const double2 m = make_double2(__dadd_rn(a[e].x, __dmul_rn(op, b[e].x)), __dadd_rn(a[e].y, __dmul_rn(op, b[e].y)));
+      if (mu) mu[l * N + z] = m;
       if (nl_out) nl_out[l * N + z] = a[e];  // F(psi^3), for the next step's density update
+      b[e] = m;
+    }
+    // the inverse z passes grad mu starts with (_Real3._grad_zy): plain (the
+    // x / y derivatives' shared pass) and with the i k_z multiplier
+    // (pfcs_fft_axis_c2c_pro's derivative prologue), so mu_hat itself need
+    // not reach HBM
+    if (t0_out) {
+#pragma unroll
+      for (int e = 0; e < R; ++e) a[e] = b[e];
+      const int j3 = opaque(j2);
+      fft_line<N, false, 1, PFCS_LINES_TWL>(a, j3, smem, tw);
+#pragma unroll
+      for (int e = 0; e < R; ++e) t0_out[l * N + j3 + P * e] = make_double2(a[e].x * scale, a[e].y * scale);
+    }
+    if (tz_out) {
+      const int j4 = opaque(j2);
+#pragma unroll
+      for (int e = 0; e < R; ++e) {
+        const double dk = __ldg(dz + j4 + P * e);
+        b[e] = make_double2(-__dmul_rn(dk, b[e].y), __dmul_rn(dk, b[e].x));
+      }
+      fft_line<N, false, 1, PFCS_LINES_TWL>(b, j4, smem, tw);
+#pragma unroll
+      for (int e = 0; e < R; ++e) tz_out[l * N + j4 + P * e] = make_double2(b[e].x * scale, b[e].y * scale);
     }
   }
 }
 
 template <int N>
 static int mu_z_n(const double2* nl, const double2* f, double2* mu, double2* nl_out, i64 nlines, int n1,
-                  const double* kx, const double* ky, const double* kz, double eps, cudaStream_t st) {
+                  const double* kx, const double* ky, const double* kz, double eps, cudaStream_t st,
+                  double2* t0_out, double2* tz_out, const double* dz) {
   const double2* tw = twiddles(N);
   if (!tw) return PFCS_E_CUDA;
   constexpr int P = N / radix_R(N);
   const size_t smem = (size_t)tile_ls(N, 1, false) * sizeof(double2);
   int grid = 0;
   if (int rc = persistent_grid((const void*)k_mu_z<N>, P, smem, nlines, &grid)) return rc;
-  launch_pdl(k_mu_z<N>, dim3(grid), dim3(P), smem, st, nl, f, mu, nl_out, nlines, n1, kx, ky, kz, eps, tw);
+  launch_pdl(k_mu_z<N>, dim3(grid), dim3(P), smem, st, nl, f, mu, nl_out, nlines, n1, kx, ky, kz, eps, tw, t0_out,
+             tz_out, dz, 1.0 / (double)N);
   return check_launch("k_mu_z");
 }
 
 // returns 1 when not applicable (z length not a power of two in [8, 4096])
 int launch_mu_z(const double2* nl, const double2* f, double2* mu, double2* nl_out, long long nlines, int n1, int n,
-                const double* kx, const double* ky, const double* kz, double eps, cudaStream_t st) {
+                const double* kx, const double* ky, const double* kz, double eps, cudaStream_t st, double2* t0_out,
+                double2* tz_out, const double* dz) {
   if (nlines <= 0) return PFCS_OK;
   switch (n) {
 #define PFCS_MU_CASE(NN) \
   case NN:               \
-    return mu_z_n<NN>(nl, f, mu, nl_out, nlines, n1, kx, ky, kz, eps, st);
+    return mu_z_n<NN>(nl, f, mu, nl_out, nlines, n1, kx, ky, kz, eps, st, t0_out, tz_out, dz);
     PFCS_MU_CASE(8) PFCS_MU_CASE(16) PFCS_MU_CASE(32) PFCS_MU_CASE(64) PFCS_MU_CASE(128) PFCS_MU_CASE(256)
     PFCS_MU_CASE(512) PFCS_MU_CASE(1024) PFCS_MU_CASE(2048) PFCS_MU_CASE(4096)
 #undef PFCS_MU_CASE

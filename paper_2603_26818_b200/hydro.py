@@ -353,6 +353,8 @@ _R2C_XMUL = os.environ.get("PFCS_R2C_XMUL", "1") != "0"
 _R2C_XDOT = os.environ.get("PFCS_R2C_XDOT", "1") != "0"
 # mu_hat with its operands' forward z passes (pfcs_hydro_mu_z; A/B, bit-identical)
 _R2C_MUZ = os.environ.get("PFCS_R2C_MUZ", "1") != "0"
+# ... and grad mu's first inverse z passes inside it (pfcs_hydro_mu_zgrad; A/B, bit-identical)
+_R2C_MUZG = os.environ.get("PFCS_R2C_MUZG", "1") != "0"
 # serial steps carry F(psi^3) from one step's mu to the next step's density
 # update (same psi, same spectrum; A/B, bit-identical)
 _CARRY_NL = os.environ.get("PFCS_R2C_CARRY", "1") != "0"
@@ -495,7 +497,7 @@ class _Real3:
         nat.call("pfcs_irfft_x", nat.ptr(tmp), nat.ptr(out), nx, ny * nz, st)
         return out
 
-    def _grad_zy(self, h: torch.Tensor, axes, outs=None, t0=None) -> list:
+    def _grad_zy(self, h: torch.Tensor, axes, outs=None, t0=None, tz=None) -> list:
         """The inverse z and y passes of F^-1(i d_a h) for each a in axes
         (x-halved spectra, before the x pass).  k_x and k_y are constant
         along z lines, so the x and y derivatives share ONE plain inverse z
@@ -509,15 +511,18 @@ class _Real3:
         st = nat.stream_ptr()
         share = ny > 1 and _R2C_GRAD
         t0 = t0 if share else None  # the plain inverse z pass of h, when the caller has it
+        like = h if h is not None else (t0 if t0 is not None else tz)  # (h is None when t0 / tz cover the axes)
         given, outs = outs, []
         for n_a, a in enumerate(axes):
-            tmp = given[n_a] if given is not None else torch.empty_like(h)
+            tmp = given[n_a] if given is not None else torch.empty_like(like)
             if share and a != 2:
                 if t0 is None:
                     t0 = torch.empty_like(h)
                     nat.call("pfcs_fft_axis_c2c", nat.ptr(h), nat.ptr(t0), nh, ny, nz, 2, 0, st)
                 nat.call("pfcs_fft_axis_c2c_pro", nat.ptr(t0), nat.ptr(tmp), nh, ny, nz, 1, 0, 3,
                          nat.ptr(self.d[a]), a, st)
+            elif tz is not None and share:  # the caller ran the z pass with i d_z (pfcs_hydro_mu_zgrad)
+                nat.call("pfcs_fft_axis_c2c", nat.ptr(tz), nat.ptr(tmp), nh, ny, nz, 1, 0, st)
             else:  # i d_a fused into the z pass
                 nat.call("pfcs_fft_axis_c2c_pro", nat.ptr(h), nat.ptr(tmp), nh, ny, nz, 2, 0, 3,
                          nat.ptr(self.d[a]), a, st)
@@ -561,19 +566,27 @@ class _Real3:
             nat.call("pfcs_fft_axis_c2c", nat.ptr(out), nat.ptr(out), self.nh, ny, nz, 2, 1, st)
         return out
 
-    def prod_grad(self, h: torch.Tensor, aux: torch.Tensor, axes=(0, 1, 2), z: bool = True) -> list:
+    def prod_grad(self, h: torch.Tensor, aux: torch.Tensor, axes=(0, 1, 2), z: bool = True, zpre=None) -> list:
         """[F(aux * F^-1(i d_a h)) for a in axes] — the hydro force
         F(psi F^-1(i k mu_hat)) (hydro.py:98): the inverse z / y passes of
         _grad_zy, ONE fused x pass (C2R, times aux, R2C: pfcs_xmul_x, the
         physical derivative and the product never reach HBM), the forward y
         and z passes.  Bit-identical to fwd(grad_inv(h)[a], RPW_MUL, aux)
-        (PFCS_R2C_XMUL=0 runs that form)."""
-        if not _R2C_XMUL:
-            return [self.fwd(d, RPW_MUL, aux, z=z) for d in self.grad_inv(h, axes)]
+        (PFCS_R2C_XMUL=0 runs that form).  zpre: {"t0", "tz"} — the
+        gradient's first inverse z passes when the caller ran them
+        (_density_mu_r grad_axes); h may then be None."""
+        zpre = zpre or {}
         nx, ny, nz = self.shape
         nh = self.nh
         st = nat.stream_ptr()
-        outs = self._grad_zy(h, axes)
+        outs = self._grad_zy(h, axes, t0=zpre.get("t0"), tz=zpre.get("tz"))
+        if not _R2C_XMUL:
+            res = []
+            for tmp in outs:
+                d = torch.empty(self.shape, dtype=torch.float64, device=tmp.device)
+                nat.call("pfcs_irfft_x", nat.ptr(tmp), nat.ptr(d), nx, ny * nz, st)
+                res.append(self.fwd(d, RPW_MUL, aux, z=z))
+            return res
         for tmp in outs:
             nat.call("pfcs_xmul_x", nat.ptr(tmp), nat.ptr(aux), nx, ny * nz, st)
             if ny > 1:
@@ -639,7 +652,7 @@ def _density_r(R: _Real3, ph, ps, adv_hat, sym, hp: HydroParams, flag: _StepFlag
                         pre_z=(nl_pre_z, adv_pre_z))
 
 
-def _density_mu_r(R: _Real3, ps, sym, want_nl: bool = False):
+def _density_mu_r(R: _Real3, ps, sym, want_nl: bool = False, grad_axes=None):
     """mu_hat = F(psi^3) + op F(psi) (hydro.py:99-101); the two forward z
     passes fused with the combination (pfcs_hydro_mu_z; PFCS_R2C_MUZ=0: the
     z passes and pfcs_hydro_mu separately, bit-identical).  want_nl: also
@@ -649,8 +662,18 @@ def _density_mu_r(R: _Real3, ps, sym, want_nl: bool = False):
     kx, ky, kz = R.k
     nl_hat = R.fwd(ps, RPW_CUBE, z=not _R2C_MUZ)
     f_hat = R.fwd(ps, z=not _R2C_MUZ)
-    mu = torch.empty_like(nl_hat)
     st = nat.stream_ptr()
+    if grad_axes and _R2C_MUZ and _R2C_MUZG and _R2C_GRAD and ny > 1 and 8 <= nz <= 4096 and nz & (nz - 1) == 0:
+        # mu_hat never stored: the kernel runs grad mu's first inverse z passes
+        # (the plain one for d_x / d_y, the i k_z one for d_z) — pfcs_hydro_mu_zgrad
+        t0 = torch.empty_like(nl_hat) if any(a != 2 for a in grad_axes) else None
+        tz = torch.empty_like(nl_hat) if 2 in grad_axes else None
+        nl_out = torch.empty_like(nl_hat) if want_nl else None
+        nat.call("pfcs_hydro_mu_zgrad", nat.ptr(nl_hat), nat.ptr(f_hat), None, nat.ptr(nl_out), nat.ptr(t0),
+                 nat.ptr(tz), nat.ptr(R.d[2]), nh, ny, nz, nat.ptr(kx), nat.ptr(ky), nat.ptr(kz), float(sym.eps), st)
+        zpre = {"t0": t0, "tz": tz}
+        return (None, nl_out, zpre) if want_nl else (None, zpre)
+    mu = torch.empty_like(nl_hat)
     if _R2C_MUZ:
         nl_out = torch.empty_like(nl_hat) if want_nl else None
         nat.call("pfcs_hydro_mu_z", nat.ptr(nl_hat), nat.ptr(f_hat), nat.ptr(mu), nat.ptr(nl_out), nh, ny, nz,
@@ -659,6 +682,8 @@ def _density_mu_r(R: _Real3, ps, sym, want_nl: bool = False):
         nat.call("pfcs_hydro_mu", nat.ptr(nl_hat), nat.ptr(f_hat), nat.ptr(mu), nh, ny, nz, nat.ptr(kx),
                  nat.ptr(ky), nat.ptr(kz), float(sym.eps), st)
         nl_out = nl_hat
+    if grad_axes:
+        return (mu, nl_out, None) if want_nl else (mu, None)
     return (mu, nl_out) if want_nl else mu
 
 
@@ -700,12 +725,12 @@ def _nl_carry_put(fields, ps, nl) -> None:
 
 
 def _velocity_r(R: _Real3, vh, ps, axis: int, mu_hat, sym, hp: HydroParams, flag: _StepFlag, cc=None,
-                muc=None, beta: float = 0.0, force=None, force_c=None):
+                muc=None, beta: float = 0.0, force=None, force_c=None, zpre=None):
     """force / force_c: F(psi F^-1(i d_axis mu_hat)) (/ c, muc) BEFORE their
     forward z pass (prod_grad z=False), when the caller formed all three at
     once (the serial steps); the update runs that z pass (pre_z)."""
     if force is None:
-        force = R.prod_grad(mu_hat, ps, (axis,), z=False)[0]  # F(psi F^-1(i k mu_hat)), up to z
+        force = R.prod_grad(mu_hat, ps, (axis,), z=False, zpre=zpre)[0]  # F(psi F^-1(i k mu_hat)), up to z
     if beta != 0.0:
         if force_c is None:
             force_c = R.prod_grad(muc, cc, (axis,), z=False)[0]
@@ -729,8 +754,8 @@ def _serial_hydro_step_r(fields: HydroFields, sym: SymbolTable, params: HydroPar
     vs = [_rdev(v) for v in fields.v]
     psi_hat, psi, zpsi = _density_r(R, ph, ps, R.adv_fwd(ph, vs, t0=_z_carry_get(fields, "psi", ph), z=False), sym,
                                     params, flag, _nl_carry_get(fields, ps), keep_z=True, adv_pre_z=True)
-    mu_hat, nl_next = _density_mu_r(R, psi, sym, want_nl=True)  # mu shared by the three components
-    forces = R.prod_grad(mu_hat, psi, z=False)
+    mu_hat, nl_next, zmu = _density_mu_r(R, psi, sym, want_nl=True, grad_axes=(0, 1, 2))  # shared by v_1..3
+    forces = R.prod_grad(mu_hat, psi, z=False, zpre=zmu)
     out = [_velocity_r(R, vh[i], psi, i, mu_hat, sym, params, flag, force=forces[i]) for i in range(3)]
     flag.check(fields.step_index, psi_hat, *(o[0] for o in out))
     fields.psi_hat, fields.psi = _out(psi_hat, host), _out(psi, host)
@@ -766,7 +791,8 @@ def _parallel_hydro_step_r(worker, role_state: dict, sym: SymbolTable, params: H
         psi = worker.bcast_tensor(0, (0, 1, 2, 3), TAG_PSI, out=torch.empty_like(psi0))
         role_state["psi"] = psi
         _check_half(R, role_state["v_hat"])
-        v_hat, v = _velocity_r(R, role_state["v_hat"], psi, i, _density_mu_r(R, psi, sym), sym, params, flag)
+        mu_hat, zmu = _density_mu_r(R, psi, sym, grad_axes=(i,))
+        v_hat, v = _velocity_r(R, role_state["v_hat"], psi, i, mu_hat, sym, params, flag, zpre=zmu)
         flag.check(idx, v_hat)
         role_state["v_hat"], role_state["v_own"] = v_hat, v
         worker.send_tensor(0, V_TAGS[i], v)

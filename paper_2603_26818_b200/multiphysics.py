@@ -359,9 +359,9 @@ def _serial_multi_step_r(fields: MultiFields, sym: SymbolTable, params: MultiPar
     psi_hat, psi, zpsi = _density_r(R, ph, ps, R.adv_fwd(ph, vs, t0=_z_carry_get(fields, "psi", ph), z=False), sym,
                                     params.hydro, flag, _nl_carry_get(fields, ps), keep_z=True, adv_pre_z=True)
     c_hat, c, zc = _composition_r(R, ch, cc, vs, sym, params, flag, t0=_z_carry_get(fields, "c", ch), keep_z=True)
-    mu_hat, nl_next = _density_mu_r(R, psi, sym, want_nl=True)
+    mu_hat, nl_next, zmu = _density_mu_r(R, psi, sym, want_nl=True, grad_axes=(0, 1, 2))
     muc = _composition_mu_r(R, c, c_hat, params) if params.beta != 0.0 else None
-    forces = R.prod_grad(mu_hat, psi, z=False)
+    forces = R.prod_grad(mu_hat, psi, z=False, zpre=zmu)
     forces_c = R.prod_grad(muc, c, z=False) if muc is not None else [None] * 3
     out = [_velocity_r(R, vh[i], psi, i, mu_hat, sym, params.hydro, flag, c, muc, params.beta, forces[i],
                        forces_c[i]) for i in range(3)]
@@ -423,9 +423,9 @@ def _parallel_multi_step_r(worker, st: dict, sym: SymbolTable, params: MultiPara
             st["c"] = worker.bcast_tensor(4, s_c, TAG_C, out=torch.empty_like(st["c"]))
             st["c_hat"] = worker.bcast_tensor(4, s_c, TAG_CHAT, out=torch.empty_like(st["c_hat"]))
             muc = _composition_mu_r(R, st["c"], st["c_hat"], params)
-        mu_hat = _density_mu_r(R, psi, sym)
+        mu_hat, zmu = _density_mu_r(R, psi, sym, grad_axes=(i,))
         st["v_hat"], st["v_own"] = _velocity_r(R, st["v_hat"], psi, i, mu_hat, sym, params.hydro, flag, st.get("c"),
-                                                muc, params.beta)
+                                                muc, params.beta, zpre=zmu)
         flag.check(idx, st["v_hat"])
         worker.bcast_tensor(1 + i, s_v[i], V_TAGS[i], t=st["v_own"])
     else:  # advection helper (G = 8)

@@ -291,7 +291,8 @@ def test_r2c_fused_prologues_bit_identical(pkg, tmp_path):
     for flag in ("0", "1"):
         path = str(tmp_path / f"pro{flag}.npz")
         env = dict(os.environ, PFCS_R2C_PRO=flag, PFCS_R2C_UPD=flag, PFCS_R2C_XMUL=flag, PFCS_R2C_XDOT=flag,
-                   PFCS_R2C_MUZ=flag, PFCS_R2C_CARRY=flag, PFCS_R2C_ZZ=flag)
+                   PFCS_R2C_MUZ=flag, PFCS_R2C_CARRY=flag, PFCS_R2C_ZZ=flag,
+                   PFCS_R2C_MUZG=flag)
         subprocess.run([sys.executable, "-c", PRO_CHILD.format(root=str(here.parent), tests=str(here), path=path)],
                        check=True, env=env, timeout=600)
         res[flag] = np.load(path)

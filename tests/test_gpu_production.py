@@ -508,3 +508,28 @@ def test_hydro_mu_z(torch_cuda, shape):
     torch.cuda.synchronize()
     assert torch.equal(mu, want)
     assert torch.equal(nl_out, a)  # the finished F(psi^3) the next step reuses
+
+
+@pytest.mark.parametrize("shape", [(257, 64, 512), (9, 12, 1024), (5, 6, 16)])
+def test_hydro_mu_zgrad(torch_cuda, shape):
+    """pfcs_hydro_mu_zgrad (mu_hat with grad mu's first inverse z passes:
+    plain and with i k_z) == pfcs_hydro_mu_z + pfcs_fft_axis_c2c (inverse z)
+    + pfcs_fft_axis_c2c_pro (inverse z, derivative prologue), bit for bit."""
+    torch, nat = torch_cuda, _nat()
+    rng = np.random.default_rng(3 + sum(shape))
+    n0, n1, n2 = shape
+    nl = _to(torch, rng.standard_normal(shape) + 1j * rng.standard_normal(shape))
+    f = _to(torch, rng.standard_normal(shape) + 1j * rng.standard_normal(shape))
+    kx, ky, kz, dz = (_to(torch, rng.standard_normal(m)) for m in (n0, n1, n2, n2))
+    st = nat.stream_ptr()
+    mu, nlo = torch.empty_like(nl), torch.empty_like(nl)
+    nat.call("pfcs_hydro_mu_z", nat.ptr(nl), nat.ptr(f), nat.ptr(mu), nat.ptr(nlo), n0, n1, n2, nat.ptr(kx),
+             nat.ptr(ky), nat.ptr(kz), -0.3, st)
+    t0_w, tz_w = torch.empty_like(nl), torch.empty_like(nl)
+    nat.call("pfcs_fft_axis_c2c", nat.ptr(mu), nat.ptr(t0_w), n0, n1, n2, 2, 0, st)
+    nat.call("pfcs_fft_axis_c2c_pro", nat.ptr(mu), nat.ptr(tz_w), n0, n1, n2, 2, 0, 3, nat.ptr(dz), 2, st)
+    t0, tz, nlo2 = torch.empty_like(nl), torch.empty_like(nl), torch.empty_like(nl)
+    nat.call("pfcs_hydro_mu_zgrad", nat.ptr(nl), nat.ptr(f), None, nat.ptr(nlo2), nat.ptr(t0), nat.ptr(tz), nat.ptr(dz),
+             n0, n1, n2, nat.ptr(kx), nat.ptr(ky), nat.ptr(kz), -0.3, st)
+    torch.cuda.synchronize()
+    assert torch.equal(t0, t0_w) and torch.equal(tz, tz_w) and torch.equal(nlo2, nlo)
