@@ -1049,6 +1049,10 @@ def main():
                       "l2": "inputs (1 GiB per field at 512^3) exceed the 126 MB L2; no flush needed"}}
     with ClockSampler(ctx.device.index) as clk:
         table = run_fft(ctx, args, out)
+        # (before the PFC lines: after a 137 GB 2048^3 run the 512^3
+        # multiphysics step measured 41 instead of 27 ms on the same box,
+        # after the 1024^3 line 28.6)
+        multi = None if args.no_multi else run_multi(ctx, args)
         pfc_res = None if args.no_pfc else run_pfc(ctx, args)
         # configs[3] grid (2048^3) when it is comfortably in this run's reach:
         # at N >= 4 GPUs (slab, <= ~70 GB peak per rank incl. the exchange
@@ -1074,7 +1078,6 @@ def main():
             pencil = _guard(lambda: run_pfc_pencil(ctx, args, args.pfc_big_n, max(3, args.steps // 4)))
             torch.cuda.empty_cache()
         pfc2d = None if args.no_pfc else run_pfc2d(ctx, args)
-        multi = None if args.no_multi else run_multi(ctx, args)
         exch = run_exchange(ctx, args) if ctx.world > 1 and not args.no_pfc else None
         yard = _guard(lambda: run_yardstick(ctx, args)) if ctx.world == 1 else None
     out["clocks"] = clk.summary()
