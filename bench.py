@@ -533,11 +533,14 @@ def multi_bytes(n: int) -> float:
         -12S);
       * grad mu's first inverse z passes run inside the mu kernel
         (pfcs_hydro_mu_zgrad: mu_hat is never stored nor re-read by the
-        two z passes: -3S).
-    Total 17R + 97S."""
+        two z passes: -3S);
+      * the x derivative of grad psi / grad c takes its i k_x in the
+        advection x pass (pfcs_xdot3_x dx), so it starts from the update's
+        kept y pass instead of a y pass of its own (-2 x 2S).
+    Total 17R + 93S."""
     R = 8.0 * n**3
     S = spec_bytes(n)
-    return 23 * (R + 5 * S) + (17 - 6 - 16 - 1) * R + (20 - 5 - 6 - 4 - 4 - 4 - 12 - 3) * S
+    return 23 * (R + 5 * S) + (17 - 6 - 16 - 1) * R + (20 - 5 - 6 - 4 - 4 - 4 - 12 - 3 - 4) * S
 
 
 def run_multi(ctx, args):
@@ -596,7 +599,7 @@ def run_multi(ctx, args):
         alg = multi_bytes(n)
         res["roofline"] = {"bound": "hbm", "alg_bytes_per_step": alg, "achieved": round(alg / (ms * 1e-3) / 1e9, 1),
                            "peak": hbm, "unit": "GB/s", "frac": round(alg / (ms * 1e-3) / 1e9 / hbm, 4),
-                           "model": "fused schedule, 17R + 97S per step (R a real field, S a half spectrum; "
+                           "model": "fused schedule, 17R + 93S per step (R a real field, S a half spectrum; "
                                     "pass-by-pass in bench.multi_bytes)"}
         # e2e: host psi, c (pinned) in -> forward transforms -> K steps -> psi, c, v out
         hp_in = [x.cpu().pin_memory() for x in (psi, c)]

@@ -143,13 +143,15 @@ int pfcs_rfft_x_pro(const double* in, void* out, int64_t nx, int64_t inner, int 
  * pfcs_real_pointwise kind 1 with aux, then pfcs_rfft_x. */
 int pfcs_xmul_x(void* data, const double* aux, int64_t nx, int64_t inner, void* stream);
 /* The x pass of the advection term v . grad x (hydro.py:83-85) in one pass:
- * spec3 = the three derivative spectra i d_a x_hat after their inverse z
- * and y passes, stacked (3, nx/2+1, inner); v0..v2 real (nx, inner); out
- * (nx/2+1, inner) = R2C((v0 g0 + v1 g1) + v2 g2), g_a = C2R(spec3[a]) —
+ * s0, s1, s2 = the three derivative spectra i d_a x_hat after their inverse
+ * z and y passes ((nx/2+1, inner) each); v0..v2 real (nx, inner); out
+ * (nx/2+1, inner) = R2C((v0 g0 + v1 g1) + v2 g2), g_a = C2R(s_a) —
  * bit-identical to three pfcs_irfft_x + pfcs_real_pointwise kind 2 +
- * pfcs_rfft_x.  nx 256 or 512 (TMA-staged); pfcs_xdot3_supported(nx,
- * inner) says whether this build / setting has the fused kernel
- * (PFCS_E_UNSUPPORTED otherwise). */
+ * pfcs_rfft_x.  dx (or NULL): s0 is the plain transform and its i d_x
+ * multiplier (a function of the x mode only) is applied to the loaded modes
+ * first, as pfcs_mul_deriv(axis 0) would.  nx 256 or 512 (TMA-staged);
+ * pfcs_xdot3_supported(nx, inner) says whether this build / setting has the
+ * fused kernel (PFCS_E_UNSUPPORTED otherwise). */
 int pfcs_xdot3_supported(int64_t nx, int64_t inner);
 /* mu_hat of hydro_velocity_step (hydro.py:99-101) fused with the forward z
  * passes of its operands: nl_xy, f_xy = F(psi^3) and F(psi) after their x
@@ -171,8 +173,8 @@ int pfcs_hydro_mu_z(const void* nl_xy, const void* f_xy, void* mu, void* nl_out,
 int pfcs_hydro_mu_zgrad(const void* nl_xy, const void* f_xy, void* mu, void* nl_out, void* t0_out, void* tz_out,
                         const double* dz, int64_t n0, int64_t n1, int64_t n2, const double* kx, const double* ky,
                         const double* kz, double eps, void* stream);
-int pfcs_xdot3_x(const void* spec3, const double* v0, const double* v1, const double* v2, void* out, int64_t nx,
-                 int64_t inner, void* stream);
+int pfcs_xdot3_x(const void* s0, const void* s1, const void* s2, const double* v0, const double* v1,
+                 const double* v2, void* out, int64_t nx, int64_t inner, const double* dx, void* stream);
 
 /* ---- fused PFC step kernels: pfc.pfc_step (pfc.py:96-128) ---------------
  * Diagnostics block `diag` (device, PFCS_DIAG_SLOTS x 4 doubles; the caller

@@ -69,7 +69,7 @@ _SIGS = {
     "pfcs_hydro_mu_z": [_c_p, _c_p, _c_p, _c_p, _c_i64, _c_i64, _c_i64, _c_p, _c_p, _c_p, _c_d, _c_p],
     "pfcs_hydro_mu_zgrad": [_c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_i64, _c_i64, _c_i64, _c_p, _c_p, _c_p, _c_d,
                             _c_p],
-    "pfcs_xdot3_x": [_c_p, _c_p, _c_p, _c_p, _c_p, _c_i64, _c_i64, _c_p],
+    "pfcs_xdot3_x": [_c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_i64, _c_i64, _c_p, _c_p],
     "pfcs_pfc_cube_x": [_c_p, _c_i64, _c_i64, _c_int, _c_p, _c_p],
     "pfcs_pfc_update_z": [_c_p, _c_p, _c_p, _c_i64, _c_i64, _c_i64, _c_int, _c_int,
                           _c_p, _c_p, _c_p, _c_d, _c_d, _c_p, _c_p],

@@ -186,8 +186,8 @@ int launch_upd_zz(const double2* state, const double2* aux, const double2* aux2,
 int launch_mu_z(const double2* nl, const double2* f, double2* mu, double2* nl_out, long long nlines, int n1, int n,
                 const double* kx, const double* ky, const double* kz, double eps, cudaStream_t st, double2* t0_out,
                 double2* tz_out, const double* dz);
-int launch_xdot3(const void* spec3, const double* v0, const double* v1, const double* v2, void* out, long long nx,
-                 long long inner, cudaStream_t st);
+int launch_xdot3(const void* const* spec, const double* v0, const double* v1, const double* v2, void* out,
+                 long long nx, long long inner, const double* dx, cudaStream_t st);
 int launch_pfc_z(const double2* nl, double2* psi_hat, double2* next, long long cx, long long ny,
                  long long nz, int g_in, int g_out, const double* kx, const double* ky,
                  const double* kz, double eps, double dt, double* diag, cudaStream_t st,
@@ -418,11 +418,12 @@ int pfcs_hydro_mu_zgrad(const void* nl_xy, const void* f_xy, void* mu, void* nl_
 
 int pfcs_xdot3_supported(int64_t nx, int64_t inner) { return xdot3_supported(nx, inner) ? 1 : 0; }
 
-int pfcs_xdot3_x(const void* spec3, const double* v0, const double* v1, const double* v2, void* out, int64_t nx,
-                 int64_t inner, void* stream) {
-  if (!spec3 || !v0 || !v1 || !v2 || !out) return fail(PFCS_E_ARG, "null argument");
-  if (out == spec3) return fail(PFCS_E_ARG, "out must not alias the derivative spectra");
-  const int rc = launch_xdot3(spec3, v0, v1, v2, out, nx, inner, S(stream));
+int pfcs_xdot3_x(const void* s0, const void* s1, const void* s2, const double* v0, const double* v1,
+                 const double* v2, void* out, int64_t nx, int64_t inner, const double* dx, void* stream) {
+  if (!s0 || !s1 || !s2 || !v0 || !v1 || !v2 || !out) return fail(PFCS_E_ARG, "null argument");
+  if (out == s0 || out == s1 || out == s2) return fail(PFCS_E_ARG, "out must not alias the derivative spectra");
+  const void* spec[3] = {s0, s1, s2};
+  const int rc = launch_xdot3(spec, v0, v1, v2, out, nx, inner, dx, S(stream));
   if (rc == 1) return fail(PFCS_E_UNSUPPORTED, "fused advection x pass: nx 256 or 512 with TMA (pfcs_xdot3_supported)");
   return rc;
 }

@@ -388,7 +388,10 @@ __global__ void __launch_bounds__(T*(M / real_R(M, MODE)),
 // ----------------------------------------------- advection dot product --
 // v . grad x on the R2C path in ONE x pass (hydro.py:83-85 and the
 // composition advection): the inputs are the three derivative spectra
-// i d_a x_hat after their inverse z and y passes, stacked as (3, M+1, inner);
+// i d_a x_hat after their inverse z and y passes (three (M+1, inner) arrays;
+// with dx, the first is the plain inverse z / y transform of x_hat and its
+// i d_x multiplier — constant along y and z lines — is applied here, to the
+// loaded modes, as pfcs_mul_deriv would);
 // per tile the kernel runs three C2R sub-passes (TMA-staged, double-buffered
 // across sub-passes) and accumulates v_a * g_a per real sample in registers
 // in pfcs_real_pointwise kind 2's order ((v0 g0 + v1 g1) + v2 g2), then the
@@ -401,8 +404,9 @@ __global__ void __launch_bounds__(T*(M / real_R(M, MODE)),
 template <int M, int T>
 __global__ void __launch_bounds__(T*(M / 8), PFCS_XDOT_MINB)
     k_xdot3(double2* out, i64 inner, const double2* __restrict__ twN, double scale,
-            const __grid_constant__ TmaPair tm, const double* __restrict__ v0, const double* __restrict__ v1,
-            const double* __restrict__ v2) {
+            const __grid_constant__ TmaPair tm0, const __grid_constant__ TmaPair tm1,
+            const __grid_constant__ TmaPair tm2, const double* __restrict__ v0, const double* __restrict__ v1,
+            const double* __restrict__ v2, const double* __restrict__ dx) {
   pdl_wait();
   constexpr int R = 8;
   constexpr int P = M / R;
@@ -421,12 +425,13 @@ __global__ void __launch_bounds__(T*(M / 8), PFCS_XDOT_MINB)
 
   auto issue = [&](i64 tile, int sub, int sidx) {
     const int i0 = (int)(tile * T);
+    const TmaPair* tm = sub == 0 ? &tm0 : (sub == 1 ? &tm1 : &tm2);
     unsigned char* dst = (unsigned char*)(sidx ? stage1 : stage0);
     mbar_expect_tx(&bars[sidx], (unsigned)XS::BYTES);
 #pragma unroll
     for (int b = 0; b < XS::NB; ++b)
-      tma_load_2d(dst + (size_t)b * XS::BR * T * 16, &tm.a, &bars[sidx], 2 * i0, sub * (M + 1) + b * XS::BR);
-    tma_load_2d(dst + (size_t)M * T * 16, &tm.b, &bars[sidx], 2 * i0, sub * (M + 1) + M);
+      tma_load_2d(dst + (size_t)b * XS::BR * T * 16, &tm->a, &bars[sidx], 2 * i0, b * XS::BR);
+    tma_load_2d(dst + (size_t)M * T * 16, &tm->b, &bars[sidx], 2 * i0, M);
   };
   if (tid == 0) {
     mbar_init(&bars[0], 1);
@@ -484,6 +489,11 @@ __global__ void __launch_bounds__(T*(M / 8), PFCS_XDOT_MINB)
         const int k = jj + P * e;
         double2 a = v[e];
         double2 bm = cur[(M - k) * T + t];  // row M for k = 0
+        if (sub == 0 && dx) {  // i d_x[k] (pfcs_mul_deriv's arithmetic) on both paired modes
+          const double dk = __ldg(dx + k), dm = __ldg(dx + (M - k));
+          a = make_double2(-__dmul_rn(dk, a.y), __dmul_rn(dk, a.x));
+          bm = make_double2(-__dmul_rn(dm, bm.y), __dmul_rn(dm, bm.x));
+        }
         if (k == 0) {
           a.y = 0.0;
           bm.y = 0.0;
@@ -544,29 +554,33 @@ __global__ void __launch_bounds__(T*(M / 8), PFCS_XDOT_MINB)
 }
 
 template <int M>
-static int xdot3_m(const double2* spec3, const double* v0, const double* v1, const double* v2, double2* out,
-                   i64 inner, cudaStream_t st) {
+static int xdot3_m(const double2* const* spec, const double* v0, const double* v1, const double* v2, double2* out,
+                   i64 inner, const double* dx, cudaStream_t st) {
 #ifndef PFCS_XDOT_T
 #define PFCS_XDOT_T 8
 #endif
   constexpr int T = PFCS_XDOT_T;  // lines per tile (8: 128-byte complex rows, as the cube pass at M = 256)
   using XS = XStage<M, T, MODE_C2R>;
   static_assert(XS::SMEM <= 227 * 1024, "stage + workspace fit");
-  if (2 * inner >= (1LL << 31) || ((uintptr_t)spec3 & 15)) return 1;
+  if (2 * inner >= (1LL << 31)) return 1;
   const double2* twN = twiddles(2 * M);
   if (!twN) return PFCS_E_CUDA;
-  TmaPair tm{};
-  const unsigned long long dims[2] = {(unsigned long long)(2 * inner), (unsigned long long)(3 * (M + 1))};
+  TmaPair tm[3] = {};
+  const unsigned long long dims[2] = {(unsigned long long)(2 * inner), (unsigned long long)(M + 1)};
   const unsigned long long str[1] = {(unsigned long long)inner * 16};
   const unsigned box[2] = {(unsigned)(2 * T), (unsigned)XS::BR};
   const unsigned box1[2] = {(unsigned)(2 * T), 1u};
-  if (!make_tmap(&tm.a, 2, spec3, dims, str, box) || !make_tmap(&tm.b, 2, spec3, dims, str, box1)) return 1;
+  for (int a = 0; a < 3; ++a) {
+    if (((uintptr_t)spec[a] & 15) || !make_tmap(&tm[a].a, 2, spec[a], dims, str, box) ||
+        !make_tmap(&tm[a].b, 2, spec[a], dims, str, box1))
+      return 1;
+  }
   const i64 ntiles = (inner + T - 1) / T;
   int grid = 0;
   auto kern = k_xdot3<M, T>;
   if (int rc = persistent_grid((const void*)kern, T * (M / 8), XS::SMEM, ntiles, &grid)) return rc;
-  launch_pdl(kern, dim3(grid), dim3(T * (M / 8)), XS::SMEM, st, out, inner, twN, 1.0 / (double)(2 * M), tm, v0, v1,
-             v2);
+  launch_pdl(kern, dim3(grid), dim3(T * (M / 8)), XS::SMEM, st, out, inner, twN, 1.0 / (double)(2 * M), tm[0], tm[1],
+             tm[2], v0, v1, v2, dx);
   return check_launch("k_xdot3");
 }
 
@@ -576,13 +590,14 @@ bool xdot3_supported(long long nx, long long inner) {
   return tma_enabled() && (nx == 256 || nx == 512) && inner >= 0 && 2 * inner < (1LL << 31);
 }
 
-int launch_xdot3(const void* spec3, const double* v0, const double* v1, const double* v2, void* out, long long nx,
-                 long long inner, cudaStream_t st) {
+int launch_xdot3(const void* const* spec, const double* v0, const double* v1, const double* v2, void* out,
+                 long long nx, long long inner, const double* dx, cudaStream_t st) {
   if (inner <= 0) return PFCS_OK;
   if (!xdot3_supported(nx, inner)) return 1;
+  const double2* s[3] = {(const double2*)spec[0], (const double2*)spec[1], (const double2*)spec[2]};
   switch (nx) {
-    case 256: return xdot3_m<128>((const double2*)spec3, v0, v1, v2, (double2*)out, inner, st);
-    case 512: return xdot3_m<256>((const double2*)spec3, v0, v1, v2, (double2*)out, inner, st);
+    case 256: return xdot3_m<128>(s, v0, v1, v2, (double2*)out, inner, dx, st);
+    case 512: return xdot3_m<256>(s, v0, v1, v2, (double2*)out, inner, dx, st);
     default: return 1;
   }
 }

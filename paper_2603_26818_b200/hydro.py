@@ -438,9 +438,10 @@ class _Real3:
         transform of its result (pfcs_update_zinv; kind 0 psi, 1 velocity,
         2 composition): returns (new state, F^-1 of it).  PFCS_R2C_UPD=0 runs
         the standalone update kernel and the plain inverse (bit-identical).
-        keep_z: also return the inverse z pass of the new state (or None) —
-        the shared z pass of the next step's gradient of that state
-        (_grad_zy), so the serial steps carry it over.  pre_z: (aux, aux2)
+        keep_z: also return {"z": the inverse z pass, "y": its y pass} of
+        the new state (or None) — the next step's gradient of that state
+        starts from them (_grad_zy, adv_fwd), so the serial steps carry them
+        over.  pre_z: (aux, aux2)
         arrive before their forward z pass (fwd(..., z=False)); the update
         runs it in registers (pfcs_update_zzinv; PFCS_R2C_ZZ=0: the z passes
         in place first — bit-identical)."""
@@ -473,14 +474,16 @@ class _Real3:
             nat.call("pfcs_update_zinv", kind, nat.ptr(state), nat.ptr(aux),
                      nat.ptr(aux2) if aux2 is not None else None, nat.ptr(new), nat.ptr(tmp), nh, ny, nz,
                      nat.ptr(kx), nat.ptr(ky), nat.ptr(kz), *c3, nat.ptr(flag.t), st)
-        zkeep = tmp if keep_z else None
+        keep = {"z": tmp, "y": None} if keep_z else None
         if ny > 1:
             ybuf = torch.empty_like(tmp) if keep_z else tmp  # (out of place keeps the z pass)
             nat.call("pfcs_fft_axis_c2c", nat.ptr(tmp), nat.ptr(ybuf), nh, ny, nz, 1, 0, st)
             tmp = ybuf
+            if keep_z:
+                keep["y"] = ybuf  # the C2R below only reads it
         out = torch.empty(self.shape, dtype=torch.float64, device=state.device)
         nat.call("pfcs_irfft_x", nat.ptr(tmp), nat.ptr(out), nx, ny * nz, st)
-        return (new, out, zkeep) if keep_z else (new, out)
+        return (new, out, keep) if keep_z else (new, out)
 
     def inv(self, h: torch.Tensor, deriv: int | None = None) -> torch.Tensor:
         """F^-1[h], or F^-1[i d_deriv h] (grad_inv's recipe for that axis)."""
@@ -497,7 +500,7 @@ class _Real3:
         nat.call("pfcs_irfft_x", nat.ptr(tmp), nat.ptr(out), nx, ny * nz, st)
         return out
 
-    def _grad_zy(self, h: torch.Tensor, axes, outs=None, t0=None, tz=None) -> list:
+    def _grad_zy(self, h: torch.Tensor, axes, outs=None, t0=None, tz=None, x_at_x: bool = False) -> list:
         """The inverse z and y passes of F^-1(i d_a h) for each a in axes
         (x-halved spectra, before the x pass).  k_x and k_y are constant
         along z lines, so the x and y derivatives share ONE plain inverse z
@@ -505,7 +508,10 @@ class _Real3:
         axis 1); the z derivative takes it in its own z pass.  A gradient
         costs two z passes instead of three (2S less HBM traffic).  Every
         caller — the serial steps and each rank of the role maps — forms a
-        derivative along a given axis this way, so they stay bit-identical."""
+        derivative along a given axis this way, so they stay bit-identical.
+        x_at_x: the x derivative's output is the plain y pass of the shared z
+        pass — its i d_x (a function of the x mode only) is applied at the
+        x stage by the caller (the advection recipe: grad_inv, adv_fwd)."""
         nx, ny, nz = self.shape
         nh = self.nh
         st = nat.stream_ptr()
@@ -519,8 +525,11 @@ class _Real3:
                 if t0 is None:
                     t0 = torch.empty_like(h)
                     nat.call("pfcs_fft_axis_c2c", nat.ptr(h), nat.ptr(t0), nh, ny, nz, 2, 0, st)
-                nat.call("pfcs_fft_axis_c2c_pro", nat.ptr(t0), nat.ptr(tmp), nh, ny, nz, 1, 0, 3,
-                         nat.ptr(self.d[a]), a, st)
+                if a == 0 and x_at_x:
+                    nat.call("pfcs_fft_axis_c2c", nat.ptr(t0), nat.ptr(tmp), nh, ny, nz, 1, 0, st)
+                else:
+                    nat.call("pfcs_fft_axis_c2c_pro", nat.ptr(t0), nat.ptr(tmp), nh, ny, nz, 1, 0, 3,
+                             nat.ptr(self.d[a]), a, st)
             elif tz is not None and share:  # the caller ran the z pass with i d_z (pfcs_hydro_mu_zgrad)
                 nat.call("pfcs_fft_axis_c2c", nat.ptr(tz), nat.ptr(tmp), nh, ny, nz, 1, 0, st)
             else:  # i d_a fused into the z pass
@@ -532,34 +541,46 @@ class _Real3:
         return outs
 
     def grad_inv(self, h: torch.Tensor, axes=(0, 1, 2)) -> list:
-        """[F^-1(i d_a h) for a in axes] (real fields; see _grad_zy)."""
+        """[F^-1(i d_a h) for a in axes] (real fields) in the advection
+        recipe (_grad_zy x_at_x: the x derivative's multiplier at the x
+        stage, here as pfcs_mul_deriv before the C2R)."""
         nx, ny, nz = self.shape
+        nh = self.nh
         st = nat.stream_ptr()
+        share = ny > 1 and _R2C_GRAD
         outs = []
-        for tmp in self._grad_zy(h, axes):
+        for a, tmp in zip(axes, self._grad_zy(h, axes, x_at_x=True)):
+            if a == 0 and share:
+                nat.call("pfcs_mul_deriv", nat.ptr(tmp), nat.ptr(tmp), nh, ny, nz, nat.ptr(self.d[0]), 0, st)
             out = torch.empty(self.shape, dtype=torch.float64, device=h.device)
             nat.call("pfcs_irfft_x", nat.ptr(tmp), nat.ptr(out), nx, ny * nz, st)
             outs.append(out)
         return outs
 
-    def adv_fwd(self, x_hat: torch.Tensor, v, t0=None, z: bool = True) -> torch.Tensor:
+    def adv_fwd(self, x_hat: torch.Tensor, v, t0=None, z: bool = True, y0=None) -> torch.Tensor:
         """F(v . grad x) (hydro.py:83-85): _grad_zy's inverse z / y passes
         into one stacked buffer, ONE fused x pass (pfcs_xdot3_x: the three
         C2R, the dot product with v, the R2C — the physical derivatives and
         the product never reach HBM), the forward y and z passes.
         Bit-identical to fwd(_grad_dot_r(self, x_hat, v)), which runs when
-        PFCS_R2C_XDOT=0 or the shape has no fused kernel.  t0: the plain
-        inverse z pass of x_hat if the caller has it (update_inv keep_z)."""
+        PFCS_R2C_XDOT=0 or the shape has no fused kernel.  t0 / y0: the
+        plain inverse z pass / z and y passes of x_hat if the caller has them
+        (update_inv keep_z) — the x derivative takes its i d_x in the x pass
+        (_grad_zy x_at_x), so with y0 it needs no pass of its own."""
         nx, ny, nz = self.shape
         if not (_R2C_XDOT and nat.load().pfcs_xdot3_supported(nx, ny * nz)):
             return self.fwd(_grad_dot_r(self, x_hat, v), z=z)
         st = nat.stream_ptr()
-        spec3 = torch.empty((3,) + self.hshape, dtype=torch.complex128, device=x_hat.device)
-        self._grad_zy(x_hat, (0, 1, 2), outs=[spec3[0], spec3[1], spec3[2]], t0=t0)
+        share = ny > 1 and _R2C_GRAD
+        if share and y0 is not None:
+            specs = [y0] + self._grad_zy(x_hat, (1, 2), t0=t0)
+        else:
+            specs = self._grad_zy(x_hat, (0, 1, 2), t0=t0, x_at_x=True)
         out = torch.empty(self.hshape, dtype=torch.complex128, device=x_hat.device)
         vs = [_rdev(x) for x in v]
-        nat.call("pfcs_xdot3_x", nat.ptr(spec3), nat.ptr(vs[0]), nat.ptr(vs[1]), nat.ptr(vs[2]), nat.ptr(out),
-                 nx, ny * nz, st)
+        nat.call("pfcs_xdot3_x", nat.ptr(specs[0]), nat.ptr(specs[1]), nat.ptr(specs[2]), nat.ptr(vs[0]),
+                 nat.ptr(vs[1]), nat.ptr(vs[2]), nat.ptr(out), nx, ny * nz,
+                 nat.ptr(self.d[0]) if share else None, st)
         if ny > 1:
             nat.call("pfcs_fft_axis_c2c", nat.ptr(out), nat.ptr(out), self.nh, ny, nz, 1, 1, st)
         if nz > 1 and z:
@@ -752,7 +773,8 @@ def _serial_hydro_step_r(fields: HydroFields, sym: SymbolTable, params: HydroPar
     vh = [_hdev(x) for x in fields.v_hat]
     _check_half(R, ph, *vh)
     vs = [_rdev(v) for v in fields.v]
-    psi_hat, psi, zpsi = _density_r(R, ph, ps, R.adv_fwd(ph, vs, t0=_z_carry_get(fields, "psi", ph), z=False), sym,
+    kpsi = _z_carry_get(fields, "psi", ph) or {}
+    psi_hat, psi, zpsi = _density_r(R, ph, ps, R.adv_fwd(ph, vs, t0=kpsi.get("z"), y0=kpsi.get("y"), z=False), sym,
                                     params, flag, _nl_carry_get(fields, ps), keep_z=True, adv_pre_z=True)
     mu_hat, nl_next, zmu = _density_mu_r(R, psi, sym, want_nl=True, grad_axes=(0, 1, 2))  # shared by v_1..3
     forces = R.prod_grad(mu_hat, psi, z=False, zpre=zmu)

@@ -327,10 +327,11 @@ def parallel_multi_step(worker, st: dict, sym: SymbolTable, params: MultiParams)
 
 # ------------------------------------------------------------ R2C path ------
 
-def _composition_r(R: _Real3, ch, cc, v, sym, params: MultiParams, flag: _StepFlag, t0=None, keep_z=False):
-    """t0: the plain inverse z pass of ch if the caller has it; keep_z:
-    also return the new state's (update_inv)."""
-    adv_hat = R.adv_fwd(ch, v, t0=t0, z=False)
+def _composition_r(R: _Real3, ch, cc, v, sym, params: MultiParams, flag: _StepFlag, t0=None, keep_z=False,
+                   y0=None):
+    """t0 / y0: the plain inverse z / z + y passes of ch if the caller has
+    them; keep_z: also return the new state's (update_inv)."""
+    adv_hat = R.adv_fwd(ch, v, t0=t0, y0=y0, z=False)
     f_hat = R.fwd(cc, RPW_CHNL, alpha=params.alpha, z=False)
     return R.update_inv(2, ch, f_hat, adv_hat,
                         (float(params.mobility), float(params.kappa), float(params.hydro.pfc.dt)), flag,
@@ -356,9 +357,11 @@ def _serial_multi_step_r(fields: MultiFields, sym: SymbolTable, params: MultiPar
     vh = [_hdev(x) for x in fields.v_hat]
     _check_half(R, ph, ch, *vh)
     vs = [_rdev(v) for v in fields.v]
-    psi_hat, psi, zpsi = _density_r(R, ph, ps, R.adv_fwd(ph, vs, t0=_z_carry_get(fields, "psi", ph), z=False), sym,
+    kpsi = _z_carry_get(fields, "psi", ph) or {}
+    kc = _z_carry_get(fields, "c", ch) or {}
+    psi_hat, psi, zpsi = _density_r(R, ph, ps, R.adv_fwd(ph, vs, t0=kpsi.get("z"), y0=kpsi.get("y"), z=False), sym,
                                     params.hydro, flag, _nl_carry_get(fields, ps), keep_z=True, adv_pre_z=True)
-    c_hat, c, zc = _composition_r(R, ch, cc, vs, sym, params, flag, t0=_z_carry_get(fields, "c", ch), keep_z=True)
+    c_hat, c, zc = _composition_r(R, ch, cc, vs, sym, params, flag, t0=kc.get("z"), y0=kc.get("y"), keep_z=True)
     mu_hat, nl_next, zmu = _density_mu_r(R, psi, sym, want_nl=True, grad_axes=(0, 1, 2))
     muc = _composition_mu_r(R, c, c_hat, params) if params.beta != 0.0 else None
     forces = R.prod_grad(mu_hat, psi, z=False, zpre=zmu)

@@ -21,7 +21,7 @@ def test_byte_models_match_survey():
     assert bench.spec_bytes(n) == S
     assert bench.fft_bytes(n) == 2 * (R + 5 * S)          # one forward + one inverse, R2C
     assert bench.pfc_bytes(n) == 10 * S                   # fused PFC step
-    assert bench.multi_bytes(n) == 17 * R + 97 * S
+    assert bench.multi_bytes(n) == 17 * R + 93 * S
 
 
 def test_combined_roofline_single_gpu_is_hbm_only():

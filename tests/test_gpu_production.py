@@ -443,30 +443,37 @@ def test_xmul_x_production(torch_cuda, nx, inner):
 
 
 @pytest.mark.parametrize("nx,inner", [(512, 7104), (512, 7110), (256, 3000), (256, 40)])
-def test_xdot3_x_production(torch_cuda, nx, inner):
+@pytest.mark.parametrize("with_dx", [False, True])
+def test_xdot3_x_production(torch_cuda, nx, inner, with_dx):
     """pfcs_xdot3_x (the advection x pass: three C2R, (v0 g0 + v1 g1) + v2 g2,
     R2C) at production and small tiles: bit-identical to three
-    pfcs_irfft_x + pfcs_real_pointwise kind 2 + pfcs_rfft_x, and vs scipy
-    <= 1e-12; nx without the fused kernel is reported, not run."""
+    pfcs_irfft_x + pfcs_real_pointwise kind 2 + pfcs_rfft_x (with dx: after
+    pfcs_mul_deriv(axis 0) on the first spectrum), and vs scipy <= 1e-12;
+    nx without the fused kernel is reported, not run."""
     import scipy.fft as sfft
 
     torch, nat = torch_cuda, _nat()
     assert nat.load().pfcs_xdot3_supported(nx, inner) == 1
     assert nat.load().pfcs_xdot3_supported(1024, inner) == 0
-    rng = np.random.default_rng(nx * 3 + inner)
+    rng = np.random.default_rng(nx * 3 + inner + with_dx)
     nh = nx // 2 + 1
     spec = rng.standard_normal((3, nh, inner)) + 1j * rng.standard_normal((3, nh, inner))
     vel = [rng.standard_normal((nx, inner)) for _ in range(3)]
+    dxv = rng.standard_normal(nh)
     vd = [_to(torch, x) for x in vel]
+    dxd = _to(torch, dxv)
     st = nat.stream_ptr()
-    sd = _to(torch, spec)
+    sd = [_to(torch, spec[a]) for a in range(3)]
     fused = torch.empty((nh, inner), dtype=torch.complex128, device="cuda")
-    nat.call("pfcs_xdot3_x", nat.ptr(sd), nat.ptr(vd[0]), nat.ptr(vd[1]), nat.ptr(vd[2]), nat.ptr(fused), nx, inner,
-             st)
+    nat.call("pfcs_xdot3_x", nat.ptr(sd[0]), nat.ptr(sd[1]), nat.ptr(sd[2]), nat.ptr(vd[0]), nat.ptr(vd[1]),
+             nat.ptr(vd[2]), nat.ptr(fused), nx, inner, nat.ptr(dxd) if with_dx else None, st)
+    s0 = sd[0].clone()
+    if with_dx:
+        nat.call("pfcs_mul_deriv", nat.ptr(s0), nat.ptr(s0), nh, inner, 1, nat.ptr(dxd), 0, st)
     g = []
-    for a in range(3):
+    for a, sa in enumerate([s0, sd[1], sd[2]]):
         ga = torch.empty((nx, inner), dtype=torch.float64, device="cuda")
-        nat.call("pfcs_irfft_x", nat.ptr(sd[a].contiguous()), nat.ptr(ga), nx, inner, st)
+        nat.call("pfcs_irfft_x", nat.ptr(sa), nat.ptr(ga), nx, inner, st)
         g.append(ga)
     prod = torch.empty_like(g[0])
     nat.call("pfcs_real_pointwise", 2, nat.ptr(vd[0]), nat.ptr(g[0]), nat.ptr(vd[1]), nat.ptr(g[1]), nat.ptr(vd[2]),
@@ -474,13 +481,13 @@ def test_xdot3_x_production(torch_cuda, nx, inner):
     two = torch.empty_like(fused)
     nat.call("pfcs_rfft_x", nat.ptr(prod), nat.ptr(two), nx, inner, st)
     assert torch.equal(fused, two)
-    phys = [sfft.irfft(spec[a], n=nx, axis=0, workers=WORKERS) for a in range(3)]
+    s0h = spec[0] * (1j * dxv[:, None]) if with_dx else spec[0]
+    phys = [sfft.irfft(x, n=nx, axis=0, workers=WORKERS) for x in (s0h, spec[1], spec[2])]
     want = sfft.rfft((vel[0] * phys[0] + vel[1] * phys[1]) + vel[2] * phys[2], axis=0, workers=WORKERS)
     assert rel_l2(fused.cpu().numpy(), want) <= TOL
     with pytest.raises(Exception):
-        nat.call("pfcs_xdot3_x", nat.ptr(sd), nat.ptr(vd[0]), nat.ptr(vd[1]), nat.ptr(vd[2]), nat.ptr(fused), 1024,
-                 inner // 2, st)
-
+        nat.call("pfcs_xdot3_x", nat.ptr(sd[0]), nat.ptr(sd[1]), nat.ptr(sd[2]), nat.ptr(vd[0]), nat.ptr(vd[1]),
+                 nat.ptr(vd[2]), nat.ptr(fused), 1024, inner // 2, None, st)
 
 @pytest.mark.parametrize("shape", [(257, 64, 512), (9, 12, 1024), (5, 6, 12)])
 def test_hydro_mu_z(torch_cuda, shape):

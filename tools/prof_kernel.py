@@ -61,8 +61,9 @@ def main():
         s3.real.normal_()
         s3.imag.normal_()
         vv = [torch.randn(n * n * n, dtype=torch.float64, device="cuda") for _ in range(3)]
-        fn = lambda: nat.call("pfcs_xdot3_x", nat.ptr(s3), nat.ptr(vv[0]), nat.ptr(vv[1]), nat.ptr(vv[2]),
-                              nat.ptr(a), n, n * n, st)
+        s3v = s3.view(3, -1)
+        fn = lambda: nat.call("pfcs_xdot3_x", nat.ptr(s3v[0]), nat.ptr(s3v[1]), nat.ptr(s3v[2]), nat.ptr(vv[0]),
+                              nat.ptr(vv[1]), nat.ptr(vv[2]), nat.ptr(a), n, n * n, None, st)
     elif kind == "xmul":
         g = torch.randn(n * n * n, dtype=torch.float64, device="cuda")
         fn = lambda: nat.call("pfcs_xmul_x", nat.ptr(a), nat.ptr(g), n, n * n, st)
