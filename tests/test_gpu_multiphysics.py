@@ -298,3 +298,62 @@ def test_r2c_fused_prologues_bit_identical(pkg, tmp_path):
         res[flag] = np.load(path)
     for k in res["0"].files:
         np.testing.assert_array_equal(res["0"][k], res["1"][k])
+
+
+@pytest.mark.parametrize("G", [5, 8])
+def test_r2c_production_fused_serial_equals_role_maps(pkg, G):
+    """At 256^3 — where the fused advection / force x passes, the fused mu
+    and the carries all take part (n = 16 runs their fallbacks) — the serial
+    step on device fields (carries active) and the G = 5 / 8 role maps
+    (no carries; G = 8 helpers form d_x x with pfcs_mul_deriv before a plain
+    C2R) agree bit for bit after 3 steps."""
+    import torch
+
+    from paper_2603_26818_b200.multiphysics import ROLES, initial_role_state, parallel_multi_step, serial_multi_step
+
+    grid, sym, mp, f0 = setup(pkg, n=256)
+    f = to_real(f0)
+    d = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()  # noqa: E731
+    ref = to_real(f0)
+    ref.psi, ref.c, ref.psi_hat, ref.c_hat = d(ref.psi), d(ref.c), d(ref.psi_hat), d(ref.c_hat)
+    ref.v, ref.v_hat = [d(x) for x in ref.v], [d(x) for x in ref.v_hat]
+    for _ in range(3):
+        serial_multi_step(ref, sym, mp)
+    want = {"psi": ref.psi.cpu().numpy(), "c": ref.c.cpu().numpy(), "v": [x.cpu().numpy() for x in ref.v]}
+    del ref
+    torch.cuda.empty_cache()
+
+    def body(w):
+        st = initial_role_state(w.rank, G, f)
+        for _ in range(3):
+            parallel_multi_step(w, st, sym, mp)
+        role = ROLES[G][w.rank]
+        key = {"psi": "psi", "c": "c"}.get(role, "v_own")
+        return role, st[key].cpu().numpy()
+
+    for role, val in pkg.spawn_group(G, body):
+        if role in ("psi", "c"):
+            np.testing.assert_array_equal(val, want[role])
+        elif role.startswith("v"):
+            np.testing.assert_array_equal(val, want["v"][int(role[1]) - 1])
+        else:
+            np.testing.assert_array_equal(val, want["v"][int(role[3]) - 1])
+
+
+def test_r2c_production_one_step_vs_oracle(pkg):
+    """One 256^3 serial step with every fused kernel of the production
+    schedule (advection / force x passes, fused mu + grad mu z passes,
+    updates with operand z passes) vs the complex oracle restatement."""
+    import ref_numpy as ora
+    from paper_2603_26818_b200.multiphysics import serial_multi_step
+
+    grid, sym, mp, f = setup(pkg, n=256)
+    o = {"psi_hat": f.psi_hat, "psi": f.psi, "c_hat": f.c_hat, "c": f.c, "v_hat": list(f.v_hat), "v": list(f.v)}
+    r = to_real(f)
+    osym = ora.symbols(grid.n, grid.length, EPS, a0=2.0)
+    serial_multi_step(r, sym, mp)
+    ora.multi_step(o, osym, 0.1, 1.0, 1.0, 0.7, 0.5, 1.0, 0.0)
+    assert rel_inf(r.psi, o["psi"].real) <= 1e-12
+    assert rel_inf(r.c, o["c"].real) <= 1e-12
+    for i in range(3):
+        assert rel_inf(r.v[i], o["v"][i].real) <= 1e-9
