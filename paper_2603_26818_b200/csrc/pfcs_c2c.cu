@@ -557,7 +557,7 @@ int launch_mu_z(const double2* nl, const double2* f, double2* mu, double2* nl_ou
 // its inverse z transform written to zout — bit-identical to the forward z
 // passes, then pfcs_update_zinv.  Neither operand spectrum reaches HBM.
 #ifndef PFCS_UPDZ_TARGET
-#define PFCS_UPDZ_TARGET 640  // resident threads per SM the register cap aims for (512: 116 registers, 640: 94, 0 spills, -0.35 ms per 512^3 multiphysics step)
+#define PFCS_UPDZ_TARGET 512  // resident threads per SM the register cap aims for (all operands loaded up front: 122 registers)
 #endif
 template <int N>
 __global__ void __launch_bounds__(N / radix_R(N), min_blocks(N / radix_R(N), PFCS_UPDZ_TARGET))
@@ -573,18 +573,18 @@ __global__ void __launch_bounds__(N / radix_R(N), min_blocks(N / radix_R(N), PFC
   bool bad = false;
   for (i64 l = blockIdx.x; l < nlines; l += gridDim.x) {
     double2 a[R], b[R];
+    double2 s0[R];
 #pragma unroll
-    for (int e = 0; e < R; ++e) a[e] = aux[l * N + j + P * e];
+    for (int e = 0; e < R; ++e) {  // every operand of the line in flight before the first FFT
+      a[e] = aux[l * N + j + P * e];
+      b[e] = aux2 ? aux2[l * N + j + P * e] : make_double2(0.0, 0.0);
+      s0[e] = state[l * N + j + P * e];
+    }
     int jj = opaque(j);
     if (flags & 1) fft_line<N, true, 1, PFCS_LINES_TWL>(a, jj, smem, tw);
-    if (aux2) {
-#pragma unroll
-      for (int e = 0; e < R; ++e) b[e] = aux2[l * N + jj + P * e];
+    if (aux2 && (flags & 2)) {
       jj = opaque(jj);
-      if (flags & 2) fft_line<N, true, 1, PFCS_LINES_TWL>(b, jj, smem, tw);
-    } else {
-#pragma unroll
-      for (int e = 0; e < R; ++e) b[e] = make_double2(0.0, 0.0);
+      fft_line<N, true, 1, PFCS_LINES_TWL>(b, jj, smem, tw);
     }
     const i64 lx = l / n1;
     const int ly = (int)(l - lx * n1);
@@ -596,7 +596,7 @@ __global__ void __launch_bounds__(N / radix_R(N), min_blocks(N / radix_R(N), PFC
       const int z = jj + P * e;
       const double kc = __ldg(kz + z);
       const double k2 = __dadd_rn(kxy, __dmul_rn(kc, kc));
-      const double2 old = state[l * N + z];
+      const double2 old = s0[e];
       const double2 nw = kind == 0   ? psi_update(old, a[e], b[e], k2, c0, c1)
                          : kind == 1 ? vel_update(old, a[e], k2, c0, c1, c2)
                                      : ch_update(old, a[e], b[e], k2, c0, c1, c2);
