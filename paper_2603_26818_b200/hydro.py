@@ -708,11 +708,17 @@ def _density_mu_r(R: _Real3, ps, sym, want_nl: bool = False, grad_axes=None):
     return (mu, nl_out) if want_nl else mu
 
 
+def _carry_slots(holder) -> dict:
+    """Where a step keeps its carries: the fields object (serial steps) or a
+    role-map rank's state dict."""
+    return holder if isinstance(holder, dict) else holder.__dict__
+
+
 def _z_carry_get(fields, key: str, h):
-    """The plain inverse z pass of spectrum `h` kept by the previous serial
-    step's update (update_inv keep_z), or None: valid only while `h` is
-    still that step's state tensor, unmodified."""
-    c = fields.__dict__.get("_pfcs_z", {}).get(key)
+    """The {z, y} inverse passes of spectrum `h` kept by the previous step's
+    update (update_inv keep_z), or None: valid only while `h` is still that
+    step's state tensor, unmodified."""
+    c = _carry_slots(fields).get("_pfcs_z", {}).get(key)
     if c is None or not _CARRY_NL:
         return None
     ref, version, z = c
@@ -720,7 +726,7 @@ def _z_carry_get(fields, key: str, h):
 
 
 def _z_carry_put(fields, key: str, h, z) -> None:
-    d = fields.__dict__.setdefault("_pfcs_z", {})
+    d = _carry_slots(fields).setdefault("_pfcs_z", {})
     if isinstance(h, torch.Tensor) and z is not None and _CARRY_NL:
         d[key] = (weakref.ref(h), h._version, z)
     else:
@@ -802,8 +808,11 @@ def _parallel_hydro_step_r(worker, role_state: dict, sym: SymbolTable, params: H
     if rank == 0:
         ph = role_state["psi_hat"]
         _check_half(R, ph)
-        psi_hat, psi = _density_r(R, ph, psi0, R.adv_fwd(ph, role_state["v"], z=False), sym, params, flag,
-                                  adv_pre_z=True)
+        kpsi = _z_carry_get(role_state, "psi", ph) or {}
+        psi_hat, psi, zpsi = _density_r(R, ph, psi0, R.adv_fwd(ph, role_state["v"], t0=kpsi.get("z"),
+                                                                y0=kpsi.get("y"), z=False),
+                                        sym, params, flag, adv_pre_z=True, keep_z=True)
+        _z_carry_put(role_state, "psi", psi_hat, zpsi)
         flag.check(idx, psi_hat)
         role_state["psi_hat"], role_state["psi"] = psi_hat, psi
         worker.bcast_tensor(0, (0, 1, 2, 3), TAG_PSI, t=psi)

@@ -403,15 +403,21 @@ def _parallel_multi_step_r(worker, st: dict, sym: SymbolTable, params: MultiPara
             worker.bcast_tensor(0, s_psih, TAG_PSIHAT, t=ph)
             p = [worker.recv_tensor(5 + i, ADV_TAGS[i], torch.empty_like(st["psi"])) for i in range(3)]
             adv_hat = R.fwd(_rpw(RPW_ADD3, *p), z=False)
-        else:
-            adv_hat = R.adv_fwd(ph, st["v"], z=False)
-        st["psi_hat"], st["psi"] = _density_r(R, ph, st["psi"], adv_hat, sym, params.hydro, flag, adv_pre_z=True)
+        else:  # (the rank's previous update kept ph's inverse z / y passes)
+            kpsi = _z_carry_get(st, "psi", ph) or {}
+            adv_hat = R.adv_fwd(ph, st["v"], t0=kpsi.get("z"), y0=kpsi.get("y"), z=False)
+        st["psi_hat"], st["psi"], zpsi = _density_r(R, ph, st["psi"], adv_hat, sym, params.hydro, flag,
+                                                    adv_pre_z=True, keep_z=True)
+        _z_carry_put(st, "psi", st["psi_hat"], zpsi if G != 8 else None)  # (G = 8: the helpers form grad psi)
         flag.check(idx, st["psi_hat"])
         worker.bcast_tensor(0, s_psi, TAG_PSI, t=st["psi"])
         st["v"] = [worker.bcast_tensor(1 + i, s_v[i], V_TAGS[i], out=torch.empty_like(st["psi"]))
                    for i in range(3)]
     elif role == "c":
-        st["c_hat"], st["c"] = _composition_r(R, st["c_hat"], st["c"], st["v"], sym, params, flag)
+        kc = _z_carry_get(st, "c", st["c_hat"]) or {}
+        st["c_hat"], st["c"], zc = _composition_r(R, st["c_hat"], st["c"], st["v"], sym, params, flag,
+                                                  t0=kc.get("z"), y0=kc.get("y"), keep_z=True)
+        _z_carry_put(st, "c", st["c_hat"], zc)
         flag.check(idx, st["c_hat"])
         if beta:
             worker.bcast_tensor(4, s_c, TAG_C, t=st["c"])
